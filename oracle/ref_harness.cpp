@@ -1,0 +1,378 @@
+// ref_harness.cpp -- drives the UNMODIFIED reference library (compiled from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/) through
+// its public API, to pin the CPU oracle and to serve as the CPU baseline.
+//
+// TEST INFRASTRUCTURE ONLY.  Nothing here is product code.  The reference
+// hard-wires level sizes to M^l (estimators.cpp:57-58,121); the BASELINE
+// configs use c_l = c0 * M^l, so `ref_mlmc` composes the reference's own
+// public pieces -- RngStream::derive, the model plugin draw,
+// draw_realization, sketch_inner / sketch_matmul and detail::parallel_chunks
+// -- in the loop of estimators.cpp:105-179 with fine = c0 * M^l.  For c0 = 1
+// `ref_mlmc_native` calls mlmc_inner / mlmc_matmul themselves so the tests can
+// prove the composed loop equals the reference's.  The configs' data models
+// are supplied through the reference's plugin API (models.hpp:17-31).
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mlsketch/estimators.hpp"
+#include "mlsketch/models.hpp"
+#include "mlsketch/parallel.hpp"
+#include "mlsketch/rng.hpp"
+#include "mlsketch/sampling.hpp"
+#include "mlsketch/sketch.hpp"
+
+#include "../include/mlsk.h"
+
+using namespace mlsketch;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::exception& e) {
+    g_err = e.what();
+    return MLSK_EINVAL;
+}
+
+bool is_vector(const mlsk_model_desc* d) {
+    const int k = d->kind;
+    return k == MLSK_MODEL_PAPER_INNER ||
+           ((k == MLSK_MODEL_CONSTANT_ONES || k == MLSK_MODEL_DETERMINISTIC ||
+             k == MLSK_MODEL_GAUSS_MEAN) &&
+            d->m == 0 && d->p == 0);
+}
+
+// Config models (BASELINE.json configs 1-2) written against the reference's
+// plugin API: a = mean_a + sd * N(0,1) then b = mean_b + sd * N(0,1), drawn in
+// the documented order (models.hpp:14-16,23-24).
+VectorPairModel vector_model(const mlsk_model_desc* d) {
+    switch (d->kind) {
+    case MLSK_MODEL_PAPER_INNER: return paper_inner_model();
+    case MLSK_MODEL_CONSTANT_ONES: return constant_ones_model(d->n);
+    case MLSK_MODEL_DETERMINISTIC: return deterministic_model(d->n);
+    case MLSK_MODEL_GAUSS_MEAN: {
+        const std::size_t n = d->n;
+        const double sd = d->sd;
+        std::vector<double> ma((const double*)d->mean_a, (const double*)d->mean_a + n);
+        std::vector<double> mb((const double*)d->mean_b, (const double*)d->mean_b + n);
+        return VectorPairModel{n, "gauss-mean", [n, sd, ma, mb](RngStream& rng) {
+                                   std::vector<double> a(n), b(n);
+                                   for (std::size_t j = 0; j < n; ++j) a[j] = ma[j] + sd * rng.normal();
+                                   for (std::size_t j = 0; j < n; ++j) b[j] = mb[j] + sd * rng.normal();
+                                   return std::make_pair(DenseVector(std::move(a)),
+                                                         DenseVector(std::move(b)));
+                               }};
+    }
+    }
+    throw std::invalid_argument("harness: unsupported vector model");
+}
+
+MatrixPairModel matrix_model(const mlsk_model_desc* d) {
+    switch (d->kind) {
+    case MLSK_MODEL_PAPER_MATRIX: return paper_matrix_model();
+    case MLSK_MODEL_CONSTANT_ONES: return constant_ones_matrix_model(d->m, d->n, d->p);
+    case MLSK_MODEL_DETERMINISTIC: return deterministic_matrix_model();
+    case MLSK_MODEL_GAUSS_MEAN: {
+        const std::size_t m = d->m, n = d->n, p = d->p;
+        const double sd = d->sd;
+        std::vector<double> ma((const double*)d->mean_a, (const double*)d->mean_a + m * n);
+        std::vector<double> mb((const double*)d->mean_b, (const double*)d->mean_b + n * p);
+        return MatrixPairModel{m, n, p, "gauss-mean", [m, n, p, sd, ma, mb](RngStream& rng) {
+                                   std::vector<double> A(m * n), B(n * p);
+                                   for (std::size_t e = 0; e < m * n; ++e) A[e] = ma[e] + sd * rng.normal();
+                                   for (std::size_t e = 0; e < n * p; ++e) B[e] = mb[e] + sd * rng.normal();
+                                   return std::make_pair(DenseMatrix(m, n, std::move(A)),
+                                                         DenseMatrix(n, p, std::move(B)));
+                               }};
+    }
+    }
+    throw std::invalid_argument("harness: unsupported matrix model");
+}
+
+TargetFunction target(int32_t t, double p) {
+    switch (t) {
+    case MLSK_TARGET_F1: return target_f1();
+    case MLSK_TARGET_F2: return target_f2(p > 0.0 ? p : 1e-12);
+    default: return target_identity();
+    }
+}
+
+long long ipow(long long M, long long l) {
+    long long r = 1;
+    while (l-- > 0) r *= M;
+    return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+uint64_t ref_derive_seed(uint64_t master, uint64_t a, uint64_t b) {
+    return RngStream::derive_seed(master, a, b);
+}
+
+void ref_u64_stream(uint64_t seed, int64_t count, uint64_t* out) {
+    RngStream rng(seed);
+    for (int64_t i = 0; i < count; ++i) out[i] = rng.next_u64();
+}
+
+void ref_normals(uint64_t seed, int64_t count, double* out) {
+    RngStream rng(seed);
+    for (int64_t i = 0; i < count; ++i) out[i] = rng.normal();
+}
+
+void ref_indices(uint64_t seed, int64_t n, int64_t count, uint32_t* out) {
+    RngStream rng(seed);
+    const auto dist = IndexDistribution::uniform(n);
+    const auto r = draw_realization(dist, count, rng);
+    std::memcpy(out, r.indices.data(), sizeof(uint32_t) * count);
+}
+
+int ref_sketch_inner(const double* a, const double* b, int64_t n, const uint32_t* idx, int64_t s,
+                     double* out) {
+    try {
+        DenseVector va(std::vector<double>(a, a + n)), vb(std::vector<double>(b, b + n));
+        *out = sketch_inner(va, vb, std::span<const uint32_t>(idx, s), IndexDistribution::uniform(n));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int ref_sketch_matmul(const double* A, const double* B, int64_t m, int64_t n, int64_t d,
+                      const uint32_t* idx, int64_t s, double* out) {
+    try {
+        DenseMatrix MA(m, n, std::vector<double>(A, A + m * n));
+        DenseMatrix MB(n, d, std::vector<double>(B, B + n * d));
+        const auto o = sketch_matmul(MA, MB, std::span<const uint32_t>(idx, s),
+                                     IndexDistribution::uniform(n));
+        std::memcpy(out, o.data().data(), sizeof(double) * m * d);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// model.draw + draw_realization for replication k of stream tag (estimators.cpp:134-136)
+int ref_draw_sample(const mlsk_model_desc* d, uint64_t seed, uint64_t tag, int64_t k, int64_t c,
+                    uint32_t* idx, double* a_cols, double* b_rows) {
+    try {
+        RngStream rng = RngStream::derive(seed, tag, k);
+        if (is_vector(d)) {
+            const auto model = vector_model(d);
+            auto [a, b] = model.draw(rng);
+            const auto dist = IndexDistribution::uniform(model.n);
+            const Realization r = draw_realization(dist, c, rng);
+            for (int64_t i = 0; i < c; ++i) {
+                if (idx) idx[i] = r.indices[i];
+                if (a_cols) a_cols[i] = a(r.indices[i]);
+                if (b_rows) b_rows[i] = b(r.indices[i]);
+            }
+        } else {
+            const auto model = matrix_model(d);
+            auto [A, B] = model.draw(rng);
+            const auto dist = IndexDistribution::uniform(model.n);
+            const Realization r = draw_realization(dist, c, rng);
+            for (int64_t i = 0; i < c; ++i) {
+                const std::size_t j = r.indices[i];
+                if (idx) idx[i] = (uint32_t)j;
+                if (a_cols)
+                    for (std::size_t row = 1; row <= model.m; ++row) a_cols[(row - 1) * c + i] = A(row, j);
+                if (b_rows)
+                    for (std::size_t q = 1; q <= model.d; ++q) b_rows[i * model.d + q - 1] = B(j, q);
+            }
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+
+// The estimators.cpp:105-179 loop composed from reference parts, c_l = c0 M^l.
+int ref_mlmc(const mlsk_model_desc* d, int32_t tgt, double tp, const mlsk_plan* plan,
+             uint64_t seed, int32_t threads, mlsk_report* rep) {
+    try {
+        if (plan->M < 2 || plan->L < 0 || plan->c0 < 1) throw std::invalid_argument("estimator: malformed plan");
+        for (int64_t l = 0; l <= plan->L; ++l)
+            if (plan->N[l] < 1) throw std::invalid_argument("estimator: all N_l must be at least 1");
+        const TargetFunction f = target(tgt, tp);
+        const bool vec = is_vector(d);
+        std::unique_ptr<VectorPairModel> vm;
+        std::unique_ptr<MatrixPairModel> mm;
+        std::size_t cells, n;
+        if (vec) {
+            vm = std::make_unique<VectorPairModel>(vector_model(d));
+            cells = 1;
+            n = vm->n;
+        } else {
+            mm = std::make_unique<MatrixPairModel>(matrix_model(d));
+            cells = mm->m * mm->d;
+            n = mm->n;
+        }
+        const IndexDistribution dist = IndexDistribution::uniform(n);
+        if (rep->value) std::fill(rep->value, rep->value + cells, 0.0);
+        rep->total_cost_units = 0;
+        for (int64_t l = 0; l <= plan->L; ++l) {
+            const std::size_t fine = (std::size_t)(plan->c0 * ipow(plan->M, l));
+            const std::size_t coarse = l > 0 ? fine / plan->M : 0;
+            const std::size_t count = (std::size_t)plan->N[l];
+            const std::size_t n_chunks = (count + detail::kReductionChunk - 1) / detail::kReductionChunk;
+            std::vector<std::vector<double>> sums(n_chunks);
+            std::vector<double> sq_sums(n_chunks, 0.0);
+            detail::parallel_chunks(
+                count, detail::kReductionChunk, threads,
+                [&](std::size_t ch, std::size_t begin, std::size_t end) {
+                    std::vector<double> s(cells, 0.0);
+                    double s2 = 0.0;
+                    for (std::size_t k = begin; k < end; ++k) {
+                        RngStream rng = RngStream::derive(seed, l, k);
+                        if (vec) {
+                            auto [a, b] = vm->draw(rng);
+                            const Realization r = draw_realization(dist, fine, rng);
+                            double v = f.f(sketch_inner(a, b, r, dist));
+                            if (l > 0) {
+                                const std::span<const std::uint32_t> pre(r.indices.data(), coarse);
+                                v -= f.f(sketch_inner(a, b, pre, dist));
+                            }
+                            s[0] += v;
+                            s2 += v * v;
+                        } else {
+                            auto [A, B] = mm->draw(rng);
+                            const Realization r = draw_realization(dist, fine, rng);
+                            DenseMatrix v = sketch_matmul(A, B, r, dist);
+                            for (double& x : v.data()) x = f.f(x);
+                            if (l > 0) {
+                                const std::span<const std::uint32_t> pre(r.indices.data(), coarse);
+                                const DenseMatrix cv = sketch_matmul(A, B, pre, dist);
+                                for (std::size_t t = 0; t < cells; ++t) v.data()[t] -= f.f(cv.data()[t]);
+                            }
+                            for (std::size_t t = 0; t < cells; ++t) {
+                                const double x = v.data()[t];
+                                s[t] += x;
+                                s2 += x * x;
+                            }
+                        }
+                    }
+                    sums[ch] = std::move(s);
+                    sq_sums[ch] = s2;
+                });
+            std::vector<double> sum(cells, 0.0);
+            double sq = 0.0;
+            for (std::size_t ch = 0; ch < n_chunks; ++ch) {
+                for (std::size_t t = 0; t < cells; ++t) sum[t] += sums[ch][t];
+                sq += sq_sums[ch];
+            }
+            const double inv_n = 1.0 / static_cast<double>(count);
+            const long long cost = (long long)count * (long long)(fine + coarse) * (long long)cells;
+            for (std::size_t t = 0; t < cells; ++t) {
+                if (rep->level_sum) rep->level_sum[l * cells + t] = sum[t];
+                if (rep->level_estimate) rep->level_estimate[l * cells + t] = sum[t] * inv_n;
+                if (rep->value) rep->value[t] += sum[t] * inv_n;
+            }
+            if (rep->level_sumsq) rep->level_sumsq[l] = sq;
+            if (rep->level_mean_sq) rep->level_mean_sq[l] = sq * inv_n;
+            if (rep->level_count) rep->level_count[l] = plan->N[l];
+            if (rep->cost_units) rep->cost_units[l] = cost;
+            rep->total_cost_units += cost;
+        }
+        rep->seed = seed;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// The reference's own mlmc_inner / mlmc_matmul (c0 = 1 only).
+int ref_mlmc_native(const mlsk_model_desc* d, int32_t tgt, double tp, const mlsk_plan* plan,
+                    uint64_t seed, int32_t threads, mlsk_report* rep) {
+    try {
+        if (plan->c0 != 1) throw std::invalid_argument("native reference: c0 must be 1");
+        LevelPlan lp{(std::size_t)plan->M, (std::size_t)plan->L,
+                     std::vector<long long>(plan->N, plan->N + plan->L + 1), 0.1, 1.0, 1.0, false};
+        EstimatorOptions opt;
+        opt.threads = threads;
+        if (is_vector(d)) {
+            const auto r = mlmc_inner(vector_model(d), target(tgt, tp), lp, seed, opt);
+            if (rep->value) rep->value[0] = r.value;
+            for (std::size_t l = 0; l < r.per_level.size(); ++l) {
+                if (rep->level_estimate) rep->level_estimate[l] = r.per_level[l].estimate;
+                if (rep->level_mean_sq) rep->level_mean_sq[l] = r.per_level[l].sample_mean_of_squares;
+                if (rep->level_count) rep->level_count[l] = r.per_level[l].replication_count;
+                if (rep->cost_units) rep->cost_units[l] = r.per_level[l].cost_units;
+            }
+            rep->total_cost_units = r.total_cost_units;
+            rep->wall_time_s = r.wall_time_seconds;
+        } else {
+            const auto r = mlmc_matmul(matrix_model(d), target(tgt, tp), lp, seed, opt);
+            const std::size_t cells = r.value.rows() * r.value.cols();
+            if (rep->value) std::memcpy(rep->value, r.value.data().data(), sizeof(double) * cells);
+            for (std::size_t l = 0; l < r.per_level.size(); ++l) {
+                if (rep->level_estimate)
+                    std::memcpy(rep->level_estimate + l * cells, r.per_level[l].estimate.data().data(),
+                                sizeof(double) * cells);
+                if (rep->level_mean_sq) rep->level_mean_sq[l] = r.per_level[l].sample_mean_of_squares;
+                if (rep->level_count) rep->level_count[l] = r.per_level[l].replication_count;
+                if (rep->cost_units) rep->cost_units[l] = r.per_level[l].cost_units;
+            }
+            rep->total_cost_units = r.total_cost_units;
+            rep->wall_time_s = r.wall_time_seconds;
+        }
+        rep->seed = seed;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// The reference's own mc_inner / mc_matmul (sample size M^L).
+int ref_mc_native(const mlsk_model_desc* d, int32_t tgt, double tp, int64_t L, int64_t N,
+                  int64_t M, uint64_t seed, int32_t threads, mlsk_report* rep) {
+    try {
+        EstimatorOptions opt;
+        opt.threads = threads;
+        if (is_vector(d)) {
+            const auto r = mc_inner(vector_model(d), target(tgt, tp), L, N, M, seed, opt);
+            if (rep->value) rep->value[0] = r.value;
+            rep->total_cost_units = r.total_cost_units;
+        } else {
+            const auto r = mc_matmul(matrix_model(d), target(tgt, tp), L, N, M, seed, opt);
+            const std::size_t cells = r.value.rows() * r.value.cols();
+            if (rep->value) std::memcpy(rep->value, r.value.data().data(), sizeof(double) * cells);
+            rep->total_cost_units = r.total_cost_units;
+        }
+        rep->seed = seed;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// Reference sketch_matmul throughput probe for the CPU baseline of the large
+// configs: sketch of pre-drawn A (m x n), B (n x d) on c indices.
+double ref_time_sketch_matmul(int64_t m, int64_t n, int64_t d, int64_t c, uint64_t seed, int32_t reps) {
+    std::vector<double> a(m * n), b(n * d);
+    RngStream rng(seed);
+    for (auto& x : a) x = rng.uniform01();
+    for (auto& x : b) x = rng.uniform01();
+    DenseMatrix A(m, n, std::move(a)), B(n, d, std::move(b));
+    const auto dist = IndexDistribution::uniform(n);
+    const Realization r = draw_realization(dist, c, rng);
+    double chk = 0.0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < reps; ++i) chk += sketch_matmul(A, B, r, dist)(1, 1);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (chk == 12345.678) g_err = "unlikely";
+    return std::chrono::duration<double>(t1 - t0).count() / reps;
+}
+
+}  // extern "C"

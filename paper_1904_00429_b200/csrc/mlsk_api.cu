@@ -1,0 +1,412 @@
+// mlsk_api.cu -- the C-ABI of include/mlsk.h.
+//
+// Mirrors the reference entry points (estimators.hpp:58-80, sketch.hpp:17-51)
+// with the reference's validation order and error classes; maps internal
+// exceptions to status codes and keeps a thread-local last-error message.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <mutex>
+
+#include "mlsk_internal.h"
+
+namespace mlsk {
+thread_local int64_t g_launches = 0;
+int run_guarded(const std::function<void()>& body);
+}
+
+using namespace mlsk;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int guard(const std::function<void()>& body) {
+    try {
+        body();
+        return MLSK_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return MLSK_ERUNTIME;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return MLSK_ERUNTIME;
+    }
+}
+
+// Per-call execution context: device selection and stream.
+struct Exec {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool owns = false;
+    int engine = MLSK_ENGINE_AUTO;
+    int rank = 0, world = 1;
+    int64_t probe_k = 0;
+    uint32_t* probe_out = nullptr;
+
+    explicit Exec(const mlsk_exec_opts* o) {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw Error(MLSK_ERUNTIME, "no CUDA device available (the library has no CPU fallback)");
+        if (o) {
+            engine = o->engine;
+            rank = o->rank;
+            world = o->world <= 0 ? 1 : o->world;
+            probe_k = o->probe_k;
+            probe_out = o->probe_out;
+            if (rank < 0 || rank >= world) invalid("exec: rank out of range");
+            if (engine < MLSK_ENGINE_AUTO || engine > MLSK_ENGINE_FUSED) invalid("exec: unknown engine");
+        }
+        if (o && o->device >= 0) {
+            if (o->device >= ndev) invalid("exec: device ordinal out of range");
+            device = o->device;
+            MLSK_CUDA(cudaSetDevice(device));
+        } else {
+            MLSK_CUDA(cudaGetDevice(&device));
+        }
+        if (o && o->stream) {
+            stream = (cudaStream_t)o->stream;
+        } else {
+            MLSK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+            owns = true;
+        }
+    }
+    ~Exec() {
+        if (owns && stream) cudaStreamDestroy(stream);
+    }
+};
+
+void check_plan(const mlsk_plan* plan) {  // estimators.cpp:23-32
+    if (!plan || !plan->N || plan->M < 2 || plan->L < 0) invalid("estimator: malformed plan");
+    if (plan->c0 < 1) invalid("estimator: c0 must be at least 1");
+    for (int64_t l = 0; l <= plan->L; ++l)
+        if (plan->N[l] < 1) invalid("estimator: all N_l must be at least 1");
+    // c_L = c0 M^L must be representable
+    double cl = (double)plan->c0;
+    for (int64_t l = 0; l < plan->L; ++l) cl *= (double)plan->M;
+    if (cl > 4.0e9) invalid("estimator: c0 * M^L exceeds the index-count limit");
+}
+
+void check_target(int32_t target, double param) {
+    if (target < MLSK_TARGET_IDENTITY || target > MLSK_TARGET_F2) invalid("target: unknown target");
+    if (target == MLSK_TARGET_F2 && !(param > 0.0)) invalid("target_f2: zeta must be positive");
+}
+
+// Level driver shared by the estimators and the sessions.
+struct Runner {
+    Model model;
+    Workspace ws;
+    int target;
+    double tparam;
+    uint64_t seed;
+    int engine;  // resolved
+    int rank, world;
+
+    void resolve_engine(int requested) {
+        const bool fused_ok = fused_supported(model, target);
+        if (requested == MLSK_ENGINE_FUSED && !fused_ok)
+            invalid("engine: the fused engine needs the philox stream, an identity target and a supported model");
+        engine = requested == MLSK_ENGINE_AUTO ? (fused_ok ? MLSK_ENGINE_FUSED : MLSK_ENGINE_EXACT) : requested;
+    }
+
+    void run(const LevelSpec& lv, int64_t k0, int64_t k1, LevelState& st, cudaStream_t s, int64_t probe_k,
+             uint32_t* probe) {
+        const auto segs = plan_segments(k0, k1, rank, world, st);
+        RunArgs a{&model, target, tparam, seed, s, &ws, probe_k, probe};
+        if (engine == MLSK_ENGINE_FUSED) fused_run(a, lv, segs, st);
+        else exact_run(a, lv, segs, st);
+    }
+};
+
+// level sum / sum of squares on the host: total (+ open chunk, last in order)
+void read_level(const LevelState& st, cudaStream_t s, std::vector<double>& sum, double& sq) {
+    const int64_t cells = st.cells;
+    std::vector<double> h(2 * cells + 2);
+    MLSK_CUDA(cudaMemcpyAsync(h.data(), st.buf.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+    MLSK_CUDA(cudaStreamSynchronize(s));
+    sum.assign(h.begin(), h.begin() + cells);
+    sq = h[cells];
+    if (st.open_count > 0) {
+        for (int64_t t = 0; t < cells; ++t) sum[t] += h[cells + 1 + t];
+        sq += h[2 * cells + 1];
+    }
+}
+
+int mlmc_impl(bool matrix, const mlsk_model_desc* model, int32_t target, double tparam, const mlsk_plan* plan,
+              uint64_t seed, const mlsk_exec_opts* opts, mlsk_report* rep) {
+    return guard([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        check_plan(plan);
+        check_target(target, tparam);
+        if (!model) invalid("model: null descriptor");
+        if (model_is_vector(model) == matrix) invalid("estimator: model kind does not match the estimator");
+        Exec ex(opts);
+        Runner R;
+        build_model(R.model, model, ex.stream);
+        R.target = target;
+        R.tparam = tparam;
+        R.seed = seed;
+        R.rank = ex.rank;
+        R.world = ex.world;
+        R.resolve_engine(ex.engine);
+        const int64_t cells = R.model.rows * R.model.cols;
+        std::vector<double> value(cells, 0.0), sum;
+        int64_t total_cost = 0;
+        const int64_t cL = plan->c0 * ipow(plan->M, plan->L);
+        for (int64_t l = 0; l <= plan->L; ++l) {
+            const int64_t fine = plan->c0 * ipow(plan->M, l);
+            const int64_t coarse = l > 0 ? fine / plan->M : 0;
+            LevelState st;
+            st.init(cells, ex.stream);
+            uint32_t* probe = nullptr;
+            if (ex.probe_out && ex.probe_k > 0 && l > 0) probe = ex.probe_out + l * ex.probe_k * cL;
+            R.run(LevelSpec{(uint64_t)l, fine, coarse}, 0, plan->N[l], st, ex.stream, ex.probe_k, probe);
+            double sq;
+            read_level(st, ex.stream, sum, sq);
+            const double inv_n = 1.0 / (double)plan->N[l];
+            const int64_t cost = plan->N[l] * (fine + coarse) * cells;  // estimators.cpp:34-40
+            total_cost += cost;
+            if (rep) {
+                for (int64_t t = 0; t < cells; ++t) {
+                    if (rep->level_sum) rep->level_sum[l * cells + t] = sum[t];
+                    if (rep->level_estimate) rep->level_estimate[l * cells + t] = sum[t] * inv_n;
+                }
+                if (rep->level_sumsq) rep->level_sumsq[l] = sq;
+                if (rep->level_mean_sq) rep->level_mean_sq[l] = sq * inv_n;
+                if (rep->level_count) rep->level_count[l] = st.count;
+                if (rep->cost_units) rep->cost_units[l] = cost;
+            }
+            for (int64_t t = 0; t < cells; ++t) value[t] += sum[t] * inv_n;  // estimators.cpp:179-184
+        }
+        MLSK_CUDA(cudaStreamSynchronize(ex.stream));
+        if (rep) {
+            if (rep->value) std::memcpy(rep->value, value.data(), sizeof(double) * cells);
+            rep->total_cost_units = total_cost;
+            rep->seed = seed;
+            rep->wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+    });
+}
+
+int mc_impl(bool matrix, const mlsk_model_desc* model, int32_t target, double tparam, int64_t L, int64_t N,
+            int64_t M, int64_t c0, uint64_t seed, const mlsk_exec_opts* opts, mlsk_report* rep) {
+    return guard([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        if (M < 2 || N < 1 || L < 0 || c0 < 1) invalid(matrix ? "mc_matmul: need M >= 2 and N >= 1"
+                                                               : "mc_inner: need M >= 2 and N >= 1");
+        check_target(target, tparam);
+        if (!model) invalid("model: null descriptor");
+        if (model_is_vector(model) == matrix) invalid("estimator: model kind does not match the estimator");
+        Exec ex(opts);
+        Runner R;
+        build_model(R.model, model, ex.stream);
+        R.target = target;
+        R.tparam = tparam;
+        R.seed = seed;
+        R.rank = ex.rank;
+        R.world = ex.world;
+        R.resolve_engine(ex.engine);
+        const int64_t cells = R.model.rows * R.model.cols;
+        const int64_t s = c0 * ipow(M, L);
+        LevelState st;
+        st.init(cells, ex.stream);
+        R.run(LevelSpec{MLSK_TAG_MC, s, 0}, 0, N, st, ex.stream, 0, nullptr);
+        std::vector<double> sum;
+        double sq;
+        read_level(st, ex.stream, sum, sq);
+        if (rep) {
+            for (int64_t t = 0; t < cells; ++t) {
+                if (rep->value) rep->value[t] = sum[t] / (double)N;  // estimators.cpp:219,265
+                if (rep->level_sum) rep->level_sum[t] = sum[t];
+                if (rep->level_estimate) rep->level_estimate[t] = sum[t] / (double)N;
+            }
+            if (rep->level_sumsq) rep->level_sumsq[0] = sq;
+            if (rep->level_mean_sq) rep->level_mean_sq[0] = sq / (double)N;
+            if (rep->level_count) rep->level_count[0] = st.count;
+            if (rep->cost_units) rep->cost_units[0] = N * s * cells;
+            rep->total_cost_units = N * s * cells;
+            rep->seed = seed;
+            rep->wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+    });
+}
+
+}  // namespace
+
+int mlsk::run_guarded(const std::function<void()>& body) { return guard(body); }
+
+struct mlsk_session {
+    std::unique_ptr<Exec> ex;
+    Runner R;
+    int64_t M, c0, L;
+    std::vector<LevelState> levels;
+    std::vector<int64_t> next_k;
+    DevArray<double> packed;
+};
+
+extern "C" {
+
+int mlsk_mlmc_inner(const mlsk_model_desc* model, int32_t target, double tp, const mlsk_plan* plan,
+                    uint64_t seed, const mlsk_exec_opts* opts, mlsk_report* report) {
+    return mlmc_impl(false, model, target, tp, plan, seed, opts, report);
+}
+
+int mlsk_mlmc_matmul(const mlsk_model_desc* model, int32_t target, double tp, const mlsk_plan* plan,
+                     uint64_t seed, const mlsk_exec_opts* opts, mlsk_report* report) {
+    return mlmc_impl(true, model, target, tp, plan, seed, opts, report);
+}
+
+int mlsk_mc_inner(const mlsk_model_desc* model, int32_t target, double tp, int64_t L, int64_t N, int64_t M,
+                  int64_t c0, uint64_t seed, const mlsk_exec_opts* opts, mlsk_report* report) {
+    return mc_impl(false, model, target, tp, L, N, M, c0, seed, opts, report);
+}
+
+int mlsk_mc_matmul(const mlsk_model_desc* model, int32_t target, double tp, int64_t L, int64_t N, int64_t M,
+                   int64_t c0, uint64_t seed, const mlsk_exec_opts* opts, mlsk_report* report) {
+    return mc_impl(true, model, target, tp, L, N, M, c0, seed, opts, report);
+}
+
+int mlsk_session_create(const mlsk_model_desc* model, int32_t target, double tp, int64_t M, int64_t c0, int64_t L,
+                        uint64_t seed, const mlsk_exec_opts* opts, mlsk_session** out) {
+    return guard([&] {
+        if (!out) invalid("session: null output pointer");
+        if (M < 2 || L < 0 || c0 < 1) invalid("estimator: malformed plan");
+        check_target(target, tp);
+        auto s = std::make_unique<mlsk_session>();
+        s->ex = std::make_unique<Exec>(opts);
+        build_model(s->R.model, model, s->ex->stream);
+        s->R.target = target;
+        s->R.tparam = tp;
+        s->R.seed = seed;
+        s->R.rank = s->ex->rank;
+        s->R.world = s->ex->world;
+        s->R.resolve_engine(s->ex->engine);
+        s->M = M;
+        s->c0 = c0;
+        s->L = L;
+        const int64_t cells = s->R.model.rows * s->R.model.cols;
+        s->levels.resize(L + 1);
+        for (auto& st : s->levels) st.init(cells, s->ex->stream);
+        s->next_k.assign(L + 1, 0);
+        s->packed.alloc((size_t)(L + 1) * (cells + 2));
+        s->packed.zero(s->ex->stream);
+        *out = s.release();
+    });
+}
+
+int mlsk_session_run_round(mlsk_session* s, const int64_t* dN) {
+    return guard([&] {
+        if (!s || !dN) invalid("session: null argument");
+        for (int64_t l = 0; l <= s->L; ++l)
+            if (dN[l] < 0) invalid("session: dN must be non-negative");
+        MLSK_CUDA(cudaSetDevice(s->ex->device));
+        for (int64_t l = 0; l <= s->L; ++l) {
+            if (dN[l] == 0) continue;
+            const int64_t fine = s->c0 * ipow(s->M, l), coarse = l > 0 ? fine / s->M : 0;
+            s->R.run(LevelSpec{(uint64_t)l, fine, coarse}, s->next_k[l], s->next_k[l] + dN[l], s->levels[l],
+                     s->ex->stream, 0, nullptr);
+            s->next_k[l] += dN[l];
+        }
+    });
+}
+
+int mlsk_session_stats(mlsk_session* s, mlsk_report* rep) {
+    return guard([&] {
+        if (!s || !rep) invalid("session: null argument");
+        const int64_t cells = s->R.model.rows * s->R.model.cols;
+        std::vector<double> value(cells, 0.0), sum;
+        int64_t total_cost = 0;
+        for (int64_t l = 0; l <= s->L; ++l) {
+            double sq;
+            read_level(s->levels[l], s->ex->stream, sum, sq);
+            const int64_t n = s->levels[l].count;
+            const int64_t fine = s->c0 * ipow(s->M, l), coarse = l > 0 ? fine / s->M : 0;
+            const double inv_n = n > 0 ? 1.0 / (double)n : 0.0;
+            const int64_t cost = n * (fine + coarse) * cells;
+            total_cost += cost;
+            for (int64_t t = 0; t < cells; ++t) {
+                if (rep->level_sum) rep->level_sum[l * cells + t] = sum[t];
+                if (rep->level_estimate) rep->level_estimate[l * cells + t] = sum[t] * inv_n;
+                value[t] += sum[t] * inv_n;
+            }
+            if (rep->level_sumsq) rep->level_sumsq[l] = sq;
+            if (rep->level_mean_sq) rep->level_mean_sq[l] = sq * inv_n;
+            if (rep->level_count) rep->level_count[l] = n;
+            if (rep->cost_units) rep->cost_units[l] = cost;
+        }
+        if (rep->value) std::memcpy(rep->value, value.data(), sizeof(double) * cells);
+        rep->total_cost_units = total_cost;
+        rep->seed = s->R.seed;
+    });
+}
+
+int mlsk_session_level_buffer(mlsk_session* s, void** device_ptr, int64_t* n_doubles) {
+    return guard([&] {
+        if (!s || !device_ptr || !n_doubles) invalid("session: null argument");
+        const int64_t cells = s->R.model.rows * s->R.model.cols;
+        // pack [(sum, sumsq, count)] per level (sum includes the open chunk)
+        std::vector<double> host((size_t)(s->L + 1) * (cells + 2));
+        for (int64_t l = 0; l <= s->L; ++l) {
+            std::vector<double> sum;
+            double sq;
+            read_level(s->levels[l], s->ex->stream, sum, sq);
+            double* row = host.data() + l * (cells + 2);
+            std::memcpy(row, sum.data(), sizeof(double) * cells);
+            row[cells] = sq;
+            row[cells + 1] = (double)s->levels[l].count;
+        }
+        MLSK_CUDA(cudaMemcpyAsync(s->packed.p, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice,
+                                  s->ex->stream));
+        MLSK_CUDA(cudaStreamSynchronize(s->ex->stream));
+        *device_ptr = s->packed.p;
+        *n_doubles = (int64_t)host.size();
+    });
+}
+
+int mlsk_session_synchronize(mlsk_session* s) {
+    return guard([&] {
+        if (!s) invalid("session: null argument");
+        MLSK_CUDA(cudaStreamSynchronize(s->ex->stream));
+    });
+}
+
+int mlsk_session_destroy(mlsk_session* s) {
+    return guard([&] {
+        if (!s) return;
+        cudaStreamSynchronize(s->ex->stream);
+        delete s;
+    });
+}
+
+int mlsk_draw_sample(const mlsk_model_desc* model, uint64_t seed, uint64_t tag, int64_t k, int64_t c,
+                     uint32_t* indices, double* a_cols, double* b_rows) {
+    return guard([&] {
+        if (c <= 0) invalid("draw_realization: size must be positive");
+        Exec ex(nullptr);
+        Model M;
+        build_model(M, model, ex.stream);
+        Workspace ws;
+        exact_gather_sample(M, seed, tag, k, c, indices, a_cols, b_rows, ex.stream, ws);
+    });
+}
+
+uint64_t mlsk_derive_seed(uint64_t master, uint64_t a, uint64_t b) { return derive_seed(master, a, b); }
+
+const char* mlsk_last_error(void) { return g_last_error.c_str(); }
+
+const char* mlsk_version(void) { return MLSK_VERSION_STRING; }
+
+int mlsk_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int64_t mlsk_kernel_launch_count(void) { return g_launches; }
+
+}  // extern "C"

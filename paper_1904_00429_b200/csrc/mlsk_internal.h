@@ -1,0 +1,162 @@
+// mlsk_internal.h -- host-side plumbing shared by the engines and the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mlsk_device.cuh"
+
+namespace mlsk {
+
+// Internal failures travel as exceptions and are mapped to the C-ABI status
+// codes at the boundary (mlsk_api.cu).
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void invalid(const std::string& m) { throw Error(MLSK_EINVAL, m); }
+
+#define MLSK_CUDA(x)                                                                      \
+    do {                                                                                  \
+        cudaError_t e_ = (x);                                                             \
+        if (e_ != cudaSuccess)                                                            \
+            throw ::mlsk::Error(MLSK_ERUNTIME, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// Kernel launches made by the calling thread (mlsk_kernel_launch_count).
+extern thread_local int64_t g_launches;
+inline void launched(int n = 1) {
+    g_launches += n;
+    MLSK_CUDA(cudaGetLastError());
+}
+
+// Owning device allocation.
+template <class T>
+struct DevArray {
+    T* p = nullptr;
+    size_t n = 0;
+    DevArray() = default;
+    explicit DevArray(size_t count) { alloc(count); }
+    DevArray(const DevArray&) = delete;
+    DevArray& operator=(const DevArray&) = delete;
+    DevArray(DevArray&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevArray& operator=(DevArray&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DevArray() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count) MLSK_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void ensure(size_t count) { if (count > n) alloc(count); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void zero(cudaStream_t s) { if (n) MLSK_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
+};
+
+inline bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
+inline int log2_exact(int64_t n) { int k = 0; while ((int64_t(1) << k) < n) ++k; return k; }
+inline int64_t ipow(int64_t M, int64_t l) { int64_t r = 1; while (l-- > 0) r *= M; return r; }
+
+// A model uploaded / generated on the device (models.cpp:12-97 as descriptors).
+struct Model {
+    mlsk_model_desc desc{};
+    DevModel dm{};
+    bool vector = false;
+    int64_t rows = 1, cols = 1;
+    int64_t ref_u64 = 0;  // u64 the reference draw consumes before the indices
+    DevArray<double> cum, mean_a, mean_b, mean_at, paper_b;
+    DevArray<float> mean_a_f, mean_b_f, mean_at_f, rff_x, rff_w, rff_b;
+};
+
+// Validates the descriptor (the reference's constructor checks) and builds it.
+void build_model(Model& M, const mlsk_model_desc* d, cudaStream_t st);
+bool model_is_vector(const mlsk_model_desc* d);
+
+// A level of the MLMC hierarchy (estimators.cpp:120-122 with c_l = c0 M^l).
+struct LevelSpec {
+    uint64_t tag;  // l, or MLSK_TAG_MC for the single-level baseline
+    int64_t c;     // fine sample size
+    int64_t cc;    // coarse sample size (prefix), 0 at level 0 / MC
+};
+
+// Per-level accumulator state on the device.
+//  exact engine: `total` holds the chunk-order sum of closed 64-replication
+//  chunks, `open` the partial sum of the chunk still being filled
+//  (estimators.cpp:153-169); fused engine: everything lands in `total`.
+struct LevelState {
+    int64_t cells = 0;
+    DevArray<double> buf;  // [total(cells) | total_sq | open(cells) | open_sq]
+    int64_t count = 0;     // replications accumulated (this rank)
+    int64_t open_count = 0;
+    int64_t open_chunk = -1;
+    double* total() const { return buf.p; }
+    double* total_sq() const { return buf.p + cells; }
+    double* open() const { return buf.p + cells + 1; }
+    double* open_sq() const { return buf.p + 2 * cells + 1; }
+    void init(int64_t cells_, cudaStream_t st) {
+        cells = cells_;
+        buf.alloc(2 * cells + 2);
+        buf.zero(st);
+        count = open_count = 0;
+        open_chunk = -1;
+    }
+};
+
+// A run of consecutive replications inside one 64-replication chunk.
+struct Segment {
+    int64_t chunk;   // global chunk index q (k / 64)
+    int64_t k0;      // first replication
+    int64_t count;   // replications in this segment
+    bool resumes;    // continues the level's open chunk
+    bool closes;     // completes its chunk
+};
+
+// Replications [k_begin, k_end) of a level owned by `rank` of `world`
+// (chunk q belongs to rank q % world), as chunk segments.
+std::vector<Segment> plan_segments(int64_t k_begin, int64_t k_end, int rank, int world,
+                                   const LevelState& st);
+
+struct Workspace {
+    DevArray<uint64_t> stream;
+    DevArray<int64_t> ks;
+    DevArray<uint32_t> idx;
+    DevArray<double> a_cols, b_rows, v, seg_part;
+    DevArray<int64_t> seg_desc;
+    DevArray<double> panel_a, panel_b, partial;
+    DevArray<float> panel_af, panel_bf;
+};
+
+struct RunArgs {
+    const Model* model;
+    int target;
+    double target_param;
+    uint64_t seed;
+    cudaStream_t stream;
+    Workspace* ws;
+    // coupling probe: copy the index sets of replications k < probe_k
+    int64_t probe_k;
+    uint32_t* probe_host;  // [probe_k][c] for this level, or nullptr
+};
+
+// Engines.  Both consume segments in order and update `st`.
+void exact_run(const RunArgs& a, const LevelSpec& lv, const std::vector<Segment>& segs, LevelState& st);
+void fused_run(const RunArgs& a, const LevelSpec& lv, const std::vector<Segment>& segs, LevelState& st);
+bool fused_supported(const Model& M, int target);
+
+// Device-side sketch primitives used by the KAT entry points.
+void exact_gather_sample(const Model& M, uint64_t seed, uint64_t tag, int64_t k, int64_t c,
+                         uint32_t* idx_host, double* a_host, double* b_host, cudaStream_t st,
+                         Workspace& ws);
+
+}  // namespace mlsk
