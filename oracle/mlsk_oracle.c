@@ -146,71 +146,52 @@ static uint64_t as_u64(double d) { uint64_t b; memcpy(&b, &d, 8); return b; }
 static float as_float(uint32_t b) { float f; memcpy(&f, &b, 4); return f; }
 static uint32_t as_u32(float f) { uint32_t b; memcpy(&b, &f, 4); return b; }
 
-/* log(x) for normal x in (0, 1]; the spec's fixed operation sequence */
+static const double T_SINCOS_D[512] = {MLSK_SINCOS_D_INIT};
+static const double T_LOG_D[256] = {MLSK_LOG_D_INIT};
+static const float T_SINCOS_F[128] = {MLSK_SINCOS_F_INIT};
+static const float T_LOG_F[128] = {MLSK_LOG_F_INIT};
+
+/* log(x) for normal x in (0, 1]: the table-driven sequence of the spec */
 double orc_log_unit(double x) {
-    const uint64_t bits = as_u64(x);
-    int e = (int)((bits >> 52) & 0x7ff) - 1023;
-    double m = as_double((bits & 0x000fffffffffffffULL) | 0x3ff0000000000000ULL);
-    if (m > MLSK_SQRT2) {
-        m = m * 0.5;
-        e += 1;
-    }
-    const double f = m - 1.0;
-    const double s = f / (2.0 + f);
-    const double z = s * s;
-    double p = MLSK_LOG_D_10;
-    p = fma(p, z, MLSK_LOG_D_9);
-    p = fma(p, z, MLSK_LOG_D_8);
-    p = fma(p, z, MLSK_LOG_D_7);
-    p = fma(p, z, MLSK_LOG_D_6);
-    p = fma(p, z, MLSK_LOG_D_5);
-    p = fma(p, z, MLSK_LOG_D_4);
-    p = fma(p, z, MLSK_LOG_D_3);
-    p = fma(p, z, MLSK_LOG_D_2);
-    p = fma(p, z, MLSK_LOG_D_1);
-    p = fma(p, z, MLSK_LOG_D_0);
-    const double lm = (s + s) * p;
-    const double de = (double)e;
-    double r = fma(de, MLSK_LN2_LO, lm);
-    r = fma(de, MLSK_LN2_HI, r);
-    return r;
+    const uint64_t ix = as_u64(x);
+    const uint64_t tmp = ix - 0x3fe6000000000000ULL;
+    const int i = (int)((tmp >> 45) & 127);
+    const int64_t k = (int64_t)tmp >> 52;
+    const double z = as_double(ix - (tmp & 0xfff0000000000000ULL));
+    const double invc = T_LOG_D[2 * i], logc = T_LOG_D[2 * i + 1];
+    const double r = fma(z, invc, -1.0);
+    double p = MLSK_L1P_D_8;
+    p = fma(p, r, MLSK_L1P_D_7);
+    p = fma(p, r, MLSK_L1P_D_6);
+    p = fma(p, r, MLSK_L1P_D_5);
+    p = fma(p, r, MLSK_L1P_D_4);
+    p = fma(p, r, MLSK_L1P_D_3);
+    p = fma(p, r, MLSK_L1P_D_2);
+    const double y = fma(p, r * r, r);
+    const double kd = (double)k;
+    const double hi = fma(kd, MLSK_LN2_HI, logc);
+    const double lo = fma(kd, MLSK_LN2_LO, y);
+    return hi + lo;
 }
 
 /* (cos, sin)(2 pi u) for u in [0, 1) */
 void orc_sincos_turn(double u, double* c, double* s) {
-    const double v = u * 4.0;
-    int q = (int)v;
-    double f = v - (double)q;
-    if (f > 0.5) {
-        f = f - 1.0;
-        q += 1;
-    }
-    const double z = f * f;
-    double sp = MLSK_SIN_D_8;
-    sp = fma(sp, z, MLSK_SIN_D_7);
-    sp = fma(sp, z, MLSK_SIN_D_6);
-    sp = fma(sp, z, MLSK_SIN_D_5);
-    sp = fma(sp, z, MLSK_SIN_D_4);
-    sp = fma(sp, z, MLSK_SIN_D_3);
-    sp = fma(sp, z, MLSK_SIN_D_2);
-    sp = fma(sp, z, MLSK_SIN_D_1);
-    sp = fma(sp, z, MLSK_SIN_D_0);
-    const double sn = f * sp;
-    double cp = MLSK_COS_D_9;
-    cp = fma(cp, z, MLSK_COS_D_8);
-    cp = fma(cp, z, MLSK_COS_D_7);
-    cp = fma(cp, z, MLSK_COS_D_6);
-    cp = fma(cp, z, MLSK_COS_D_5);
-    cp = fma(cp, z, MLSK_COS_D_4);
-    cp = fma(cp, z, MLSK_COS_D_3);
-    cp = fma(cp, z, MLSK_COS_D_2);
-    cp = fma(cp, z, MLSK_COS_D_1);
-    cp = fma(cp, z, MLSK_COS_D_0);
+    const double v = u * 1024.0;
+    const int iv = (int)v;
+    const double f = v - (double)iv;
+    const int q = iv >> 8, i = iv & 255;
+    const double C = T_SINCOS_D[2 * i], S = T_SINCOS_D[2 * i + 1];
+    const double d = f * MLSK_SINCOS_D_STEP;
+    const double d2 = d * d;
+    const double sd = fma(d * d2, fma(d2, MLSK_SC_S5, MLSK_SC_S3), d);
+    const double cd = fma(d2, fma(d2, MLSK_SC_C4, MLSK_SC_C2), 1.0);
+    const double c1 = fma(C, cd, -(S * sd));
+    const double s1 = fma(S, cd, C * sd);
     switch (q & 3) {
-    case 0: *c = cp; *s = sn; break;
-    case 1: *c = -sn; *s = cp; break;
-    case 2: *c = -cp; *s = -sn; break;
-    default: *c = sn; *s = -cp; break;
+    case 0: *c = c1; *s = s1; break;
+    case 1: *c = -s1; *s = c1; break;
+    case 2: *c = -c1; *s = -s1; break;
+    default: *c = s1; *s = -c1; break;
     }
 }
 
@@ -225,57 +206,41 @@ void orc_box_muller(uint64_t ua, uint64_t ub, double* z0, double* z1) {
 }
 
 float orc_log_unit_f(float x) {
-    const uint32_t bits = as_u32(x);
-    int e = (int)((bits >> 23) & 0xff) - 127;
-    float m = as_float((bits & 0x007fffffu) | 0x3f800000u);
-    if (m > MLSK_SQRT2_F) {
-        m = m * 0.5f;
-        e += 1;
-    }
-    const float f = m - 1.0f;
-    const float s = f / (2.0f + f);
-    const float z = s * s;
-    float p = MLSK_LOG_F_5;
-    p = fmaf(p, z, MLSK_LOG_F_4);
-    p = fmaf(p, z, MLSK_LOG_F_3);
-    p = fmaf(p, z, MLSK_LOG_F_2);
-    p = fmaf(p, z, MLSK_LOG_F_1);
-    p = fmaf(p, z, MLSK_LOG_F_0);
-    const float lm = (s + s) * p;
-    const float de = (float)e;
-    float r = fmaf(de, MLSK_LN2_F_LO, lm);
-    r = fmaf(de, MLSK_LN2_F_HI, r);
-    return r;
+    const uint32_t ix = as_u32(x);
+    const uint32_t tmp = ix - 0x3f300000u;
+    const int i = (int)((tmp >> 17) & 63);
+    const int32_t k = (int32_t)tmp >> 23;
+    const float z = as_float(ix - (tmp & 0xff800000u));
+    const float invc = T_LOG_F[2 * i], logc = T_LOG_F[2 * i + 1];
+    const float r = fmaf(z, invc, -1.0f);
+    float p = MLSK_L1P_F_5;
+    p = fmaf(p, r, MLSK_L1P_F_4);
+    p = fmaf(p, r, MLSK_L1P_F_3);
+    p = fmaf(p, r, MLSK_L1P_F_2);
+    const float y = fmaf(p, r * r, r);
+    const float kf = (float)k;
+    const float hi = fmaf(kf, MLSK_LN2_F_HI, logc);
+    const float lo = fmaf(kf, MLSK_LN2_F_LO, y);
+    return hi + lo;
 }
 
 void orc_sincos_turn_f(float u, float* c, float* s) {
-    const float v = u * 4.0f;
-    int q = (int)v;
-    float f = v - (float)q;
-    if (f > 0.5f) {
-        f = f - 1.0f;
-        q += 1;
-    }
-    const float z = f * f;
-    float sp = MLSK_SIN_F_5;
-    sp = fmaf(sp, z, MLSK_SIN_F_4);
-    sp = fmaf(sp, z, MLSK_SIN_F_3);
-    sp = fmaf(sp, z, MLSK_SIN_F_2);
-    sp = fmaf(sp, z, MLSK_SIN_F_1);
-    sp = fmaf(sp, z, MLSK_SIN_F_0);
-    const float sn = f * sp;
-    float cp = MLSK_COS_F_6;
-    cp = fmaf(cp, z, MLSK_COS_F_5);
-    cp = fmaf(cp, z, MLSK_COS_F_4);
-    cp = fmaf(cp, z, MLSK_COS_F_3);
-    cp = fmaf(cp, z, MLSK_COS_F_2);
-    cp = fmaf(cp, z, MLSK_COS_F_1);
-    cp = fmaf(cp, z, MLSK_COS_F_0);
+    const float v = u * 256.0f;
+    const int iv = (int)v;
+    const float f = v - (float)iv;
+    const int q = iv >> 6, i = iv & 63;
+    const float C = T_SINCOS_F[2 * i], S = T_SINCOS_F[2 * i + 1];
+    const float d = f * MLSK_SINCOS_F_STEP;
+    const float d2 = d * d;
+    const float sd = fmaf(d * d2, MLSK_SC_S3_F, d);
+    const float cd = fmaf(d2, fmaf(d2, MLSK_SC_C4_F, MLSK_SC_C2_F), 1.0f);
+    const float c1 = fmaf(C, cd, -(S * sd));
+    const float s1 = fmaf(S, cd, C * sd);
     switch (q & 3) {
-    case 0: *c = cp; *s = sn; break;
-    case 1: *c = -sn; *s = cp; break;
-    case 2: *c = -cp; *s = -sn; break;
-    default: *c = sn; *s = -cp; break;
+    case 0: *c = c1; *s = s1; break;
+    case 1: *c = -s1; *s = c1; break;
+    case 2: *c = -c1; *s = -s1; break;
+    default: *c = s1; *s = -c1; break;
     }
 }
 

@@ -1,8 +1,529 @@
-// mlsk_fused.cu -- placeholder until the fused engine lands.
+// mlsk_fused.cu -- the fused fp64 engine (throughput path, philox stream,
+// identity target).
+//
+// Fused formulation: for a level-sample with c
+// indices and coarse prefix cc = c/M,
+//     Y = f(fine) - f(coarse) = sum_t w_t a_t b_t^T,
+//     w_t = n/c for t >= cc,   w_t = n/c - n/cc for t < cc   (level 0: n/c),
+// one signed contraction with K = c instead of the reference's two passes
+// (estimators.cpp:137-147).  Per level the work is split in two kernels:
+//
+//  k_gen_panels_f64  draws each level-sample's indices and generates ONLY the
+//                    sampled columns A[:, S] and rows B[S, :] (mean gather +
+//                    Philox/Box-Muller noise, w_t folded into B) straight into
+//                    16-wide K-chunks laid out for the MMA (k-permuted,
+//                    16-byte XOR swizzle), each element generated exactly once.
+//  k_gemm_f64        persistent CTAs, one 128 x 64 output tile per CTA over a
+//                    strided set of samples; a producer warp streams the K-chunks
+//                    with cp.async.bulk (TMA bulk copies) into a 4-stage mbarrier
+//                    ring; 8 consumer warps run DMMA (mma.sync m8n8k4 f64) into
+//                    register accumulators; at each sample boundary the epilogue
+//                    adds Y into a register-resident running sum S and Y^2 into
+//                    a scalar -- the per-sample output never touches memory.
+//  k_reduce_tiles    deterministic (fixed-order) sum of the per-CTA partials
+//                    into the level accumulators.
+#include <algorithm>
+#include <cstring>
+
 #include "mlsk_internal.h"
+
 namespace mlsk {
-bool fused_supported(const Model&, int) { return false; }
-void fused_run(const RunArgs&, const LevelSpec&, const std::vector<Segment>&, LevelState&) {
-    throw Error(MLSK_ERUNTIME, "fused engine not built");
+
+namespace {
+
+constexpr int KC = 16;        // K-chunk (indices per smem stage)
+constexpr int BM = 128;       // tile rows
+constexpr int BN = 64;        // tile cols
+constexpr int STAGES = 4;
+constexpr int CONSUMERS = 8;  // consumer warps (4 x 2 of 32 x 32)
+constexpr int GEMM_THREADS = (CONSUMERS + 1) * 32;
+constexpr int A_STAGE_BYTES = BM * KC * 8;
+constexpr int B_STAGE_BYTES = BN * KC * 8;
+constexpr int GEN_THREADS = 256;
+
+// ---------------------------------------------------------------- layout
+
+// Element (r, k) of a K-chunk tile, 16 doubles per row: k permuted so that
+// lane (g, t) finds k = t, t+4, t+8, t+12 in two 16-byte granules, granules
+// XOR-swizzled by r & 7 (conflict-free LDS.128 fragment loads).
+__device__ __forceinline__ int tile_slot(int r, int k) {
+    const int pos = (k & 3) * 4 + (k >> 2);
+    const int g = pos >> 1;
+    return r * KC + (((g ^ (r & 7)) << 1) | (pos & 1));
 }
+
+__device__ __forceinline__ void load_tables(double2* s_sc, double2* s_lg, const Tables& T) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_sc[i] = reinterpret_cast<const double2*>(T.sincos_d)[i];
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) s_lg[i] = reinterpret_cast<const double2*>(T.log_d)[i];
+}
+
+// --------------------------------------------------------- panel generator
+
+// grid-stride over work items (b, kc); each item produces the A chunk
+// (MP x 16) and the weighted B chunk (PP x 16) of sample b.
+__global__ void __launch_bounds__(GEN_THREADS)
+k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
+                 int64_t cc, double w_fine, double w_coarse, int64_t MP, int64_t PP, int64_t nkc,
+                 double* __restrict__ Apan, double* __restrict__ Bpan, uint32_t* __restrict__ idx_out) {
+    __shared__ __align__(16) double2 s_sc[256];
+    __shared__ __align__(16) double2 s_lg[128];
+    __shared__ __align__(16) double tile[BM * KC];
+    __shared__ int64_t s_j[KC];
+    __shared__ double s_w[KC];
+    load_tables(s_sc, s_lg, M.tab);
+    Tables T = M.tab;
+    T.sincos_d = reinterpret_cast<const double*>(s_sc);
+    T.log_d = reinterpret_cast<const double*>(s_lg);
+    const int tid = threadIdx.x;
+    const int64_t items = (int64_t)nb * nkc;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int b = (int)(it / nkc);
+        const int64_t kc = it - (int64_t)b * nkc;
+        const uint64_t key = derive_seed(seed, tag, (uint64_t)ks[b]);
+        __syncthreads();  // previous item's readers of s_j / tile are done
+        if (tid < KC) {
+            const int64_t t = kc * KC + tid;
+            int64_t j = -1;
+            double w = 0.0;
+            if (t < c) {
+                const u32x4 r = philox((uint32_t)(t >> 1), 0, 0, MLSK_CTR_INDEX, key);
+                const uint32_t ix = index_from_u64((t & 1) ? hi64(r) : lo64(r), M.n, M.log2n, M.cum);
+                j = (int64_t)ix - 1;
+                w = t < cc ? w_coarse : w_fine;
+                if (idx_out) idx_out[(int64_t)b * c + t] = ix;
+            }
+            s_j[tid] = j;
+            s_w[tid] = w;
+        }
+        __syncthreads();
+        // ---- A: rows in blocks of BM, row pairs share one Philox block
+        for (int64_t rb = 0; rb < MP; rb += BM) {
+            for (int item = tid; item < (BM / 2) * KC; item += GEN_THREADS) {
+                const int rp = item & (BM / 2 - 1), tt = item / (BM / 2);
+                const int64_t row0 = rb + 2 * rp;
+                const int64_t j = s_j[tt];
+                double v0 = 0.0, v1 = 0.0;
+                if (j >= 0 && row0 < M.m) {
+                    const u32x4 r = philox((uint32_t)j, (uint32_t)(row0 >> 1), 0, MLSK_CTR_A, key);
+                    double z0, z1;
+                    box_muller(lo64(r), hi64(r), z0, z1, T);
+                    const double* mt = M.mean_at + j * M.m + row0;
+                    v0 = __dadd_rn(mt[0], __dmul_rn(M.sd, z0));
+                    if (row0 + 1 < M.m) v1 = __dadd_rn(mt[1], __dmul_rn(M.sd, z1));
+                }
+                tile[tile_slot(2 * rp, tt)] = v0;
+                tile[tile_slot(2 * rp + 1, tt)] = v1;
+            }
+            __syncthreads();
+            double2* dst = reinterpret_cast<double2*>(Apan + (((int64_t)b * nkc + kc) * MP + rb) * KC);
+            const double2* src = reinterpret_cast<const double2*>(tile);
+            for (int i = tid; i < BM * KC / 2; i += GEN_THREADS) dst[i] = src[i];
+            __syncthreads();
+        }
+        // ---- B: cols in blocks of BN, col pairs share one Philox block, w_t folded in
+        for (int64_t cb = 0; cb < PP; cb += BN) {
+            for (int item = tid; item < (BN / 2) * KC; item += GEN_THREADS) {
+                const int qp = item & (BN / 2 - 1), tt = item / (BN / 2);
+                const int64_t col0 = cb + 2 * qp;
+                const int64_t j = s_j[tt];
+                double v0 = 0.0, v1 = 0.0;
+                if (j >= 0 && col0 < M.p) {
+                    const u32x4 r = philox((uint32_t)j, (uint32_t)(col0 >> 1), 0, MLSK_CTR_B, key);
+                    double z0, z1;
+                    box_muller(lo64(r), hi64(r), z0, z1, T);
+                    const double* mb = M.mean_b + j * M.p + col0;
+                    const double w = s_w[tt];
+                    v0 = __dmul_rn(w, __dadd_rn(mb[0], __dmul_rn(M.sd, z0)));
+                    if (col0 + 1 < M.p) v1 = __dmul_rn(w, __dadd_rn(mb[1], __dmul_rn(M.sd, z1)));
+                }
+                tile[tile_slot(2 * qp, tt)] = v0;
+                tile[tile_slot(2 * qp + 1, tt)] = v1;
+            }
+            __syncthreads();
+            double2* dst = reinterpret_cast<double2*>(Bpan + (((int64_t)b * nkc + kc) * PP + cb) * KC);
+            const double2* src = reinterpret_cast<const double2*>(tile);
+            for (int i = tid; i < BN * KC / 2; i += GEN_THREADS) dst[i] = src[i];
+            __syncthreads();
+        }
+    }
+}
+
+// ------------------------------------------------------------- mbarriers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// ------------------------------------------------------------------ GEMM
+
+struct GemmShape {
+    int nb;        // samples in the batch
+    int64_t nkc;   // K-chunks per sample
+    int64_t MP, PP;
+    int T;         // output tiles
+    int Gs;        // sample groups (CTAs per tile)
+    int tiles_n;   // tiles along the columns
+};
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, GemmShape sh,
+           double* __restrict__ part, double* __restrict__ part_sq) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    double* sA = reinterpret_cast<double*>(smem);
+    double* sB = reinterpret_cast<double*>(smem + STAGES * A_STAGE_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES));
+    __shared__ double s_sq[CONSUMERS];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = blockIdx.x;
+    const int tile = g % sh.T, grp = g / sh.T;
+    const int tm = tile / sh.tiles_n, tn = tile % sh.tiles_n;
+    const int my_samples = grp < sh.nb ? (sh.nb - 1 - grp) / sh.Gs + 1 : 0;
+    const int64_t iters = (int64_t)my_samples * sh.nkc;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&bars[s]), 1);                     // full: producer arrive + tx
+            mbar_init(smem_u32(&bars[STAGES + s]), CONSUMERS);    // empty: one per consumer warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == CONSUMERS) {
+        // ------------------------------------------------ producer warp
+        if (lane == 0) {
+            for (int64_t it = 0; it < iters; ++it) {
+                const int s = (int)(it % STAGES);
+                const uint32_t ph = (uint32_t)((it / STAGES) & 1);
+                const int64_t b = grp + (it / sh.nkc) * sh.Gs;
+                const int64_t kc = it % sh.nkc;
+                mbar_wait(smem_u32(&bars[STAGES + s]), ph ^ 1);
+                const uint32_t full = smem_u32(&bars[s]);
+                mbar_expect_tx(full, A_STAGE_BYTES + B_STAGE_BYTES);
+                const double* srcA = Apan + ((b * sh.nkc + kc) * sh.MP + (int64_t)tm * BM) * KC;
+                const double* srcB = Bpan + ((b * sh.nkc + kc) * sh.PP + (int64_t)tn * BN) * KC;
+                bulk_g2s(smem_u32(sA + s * (BM * KC)), srcA, A_STAGE_BYTES, full);
+                bulk_g2s(smem_u32(sB + s * (BN * KC)), srcB, B_STAGE_BYTES, full);
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------- consumer warps
+    const int wi = warp >> 1, wj = warp & 1;
+    const int gid = lane >> 2, tig = lane & 3;
+    double acc[4][4][2], S[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            acc[i][j][0] = acc[i][j][1] = 0.0;
+            S[i][j][0] = S[i][j][1] = 0.0;
+        }
+    double sq = 0.0;
+
+    for (int64_t it = 0; it < iters; ++it) {
+        const int s = (int)(it % STAGES);
+        const uint32_t ph = (uint32_t)((it / STAGES) & 1);
+        mbar_wait(smem_u32(&bars[s]), ph);
+        const double* a_st = sA + s * (BM * KC);
+        const double* b_st = sB + s * (BN * KC);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            double2 af[4], bf[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int r = wi * 32 + 8 * i + gid;
+                af[i] = *reinterpret_cast<const double2*>(a_st + r * KC + (((2 * tig + h) ^ gid) << 1));
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int q = wj * 32 + 8 * j + gid;
+                bf[j] = *reinterpret_cast<const double2*>(b_st + q * KC + (((2 * tig + h) ^ gid) << 1));
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i].x, bf[j].x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i].y, bf[j].y);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bars[STAGES + s]));
+        if ((it % sh.nkc) == sh.nkc - 1) {
+            // sample boundary: fused level epilogue (Y^2 and running sum)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const double y = acc[i][j][e];
+                        sq = __fma_rn(y, y, sq);
+                        S[i][j][e] = __dadd_rn(S[i][j][e], y);
+                        acc[i][j][e] = 0.0;
+                    }
+        }
+    }
+
+    // partial outputs of this CTA (deterministic layout / order)
+    double* out = part + (int64_t)g * (BM * BN);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r = wi * 32 + 8 * i + gid;
+            const int q = wj * 32 + 8 * j + 2 * tig;
+            *reinterpret_cast<double2*>(out + r * BN + q) = make_double2(S[i][j][0], S[i][j][1]);
+        }
+    sq = warp_sum(sq);
+    if (lane == 0) s_sq[warp] = sq;
+    asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS * 32));
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < CONSUMERS; ++w) t += s_sq[w];
+        part_sq[g] = t;
+    }
+}
+
+// total[cell] += sum over groups (fixed order) of the tile partials
+__global__ void k_reduce_tiles(const double* __restrict__ part, const double* __restrict__ part_sq, GemmShape sh,
+                               int64_t rows, int64_t cols, double* __restrict__ total, double* __restrict__ total_sq) {
+    const int64_t cells = rows * cols;
+    for (int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cell < cells;
+         cell += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = cell / cols, q = cell - r * cols;
+        const int tile = (int)((r / BM) * sh.tiles_n + q / BN);
+        const int64_t off = (r % BM) * BN + (q % BN);
+        double acc = 0.0;
+        for (int grp = 0; grp < sh.Gs; ++grp) acc += part[(int64_t)(grp * sh.T + tile) * (BM * BN) + off];
+        total[cell] += acc;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        double acc = 0.0;
+        for (int g = 0; g < sh.T * sh.Gs; ++g) acc += part_sq[g];
+        *total_sq += acc;
+    }
+}
+
+// ----------------------------------------------------- vector (config 1)
+
+// one warp per sample: Y = sum_t w_t a_t b_t with a_t, b_t drawn at the
+// sampled index from one Philox block (a takes z0, b takes z1)
+__global__ void __launch_bounds__(256)
+k_fused_inner(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
+              int64_t cc, double w_fine, double w_coarse, double* __restrict__ y_out,
+              uint32_t* __restrict__ idx_out) {
+    __shared__ __align__(16) double2 s_sc[256];
+    __shared__ __align__(16) double2 s_lg[128];
+    load_tables(s_sc, s_lg, M.tab);
+    __syncthreads();
+    Tables T = M.tab;
+    T.sincos_d = reinterpret_cast<const double*>(s_sc);
+    T.log_d = reinterpret_cast<const double*>(s_lg);
+    const int lane = threadIdx.x & 31;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    for (int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
+        const uint64_t key = derive_seed(seed, tag, (uint64_t)ks[b]);
+        double acc = 0.0;
+        for (int64_t tp = lane; 2 * tp < c; tp += 32) {
+            const u32x4 ri = philox((uint32_t)tp, 0, 0, MLSK_CTR_INDEX, key);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t t = 2 * tp + h;
+                if (t >= c) break;
+                const uint32_t ix = index_from_u64(h ? hi64(ri) : lo64(ri), M.n, M.log2n, M.cum);
+                if (idx_out) idx_out[(int64_t)b * c + t] = ix;
+                const int64_t j = (int64_t)ix - 1;
+                const u32x4 r = philox((uint32_t)j, 0, 0, MLSK_CTR_A, key);
+                double z0, z1;
+                box_muller(lo64(r), hi64(r), z0, z1, T);
+                const double a = __dadd_rn(M.mean_a[j], __dmul_rn(M.sd, z0));
+                const double bb = __dadd_rn(M.mean_b[j], __dmul_rn(M.sd, z1));
+                acc = __fma_rn(__dmul_rn(a, bb), t < cc ? w_coarse : w_fine, acc);
+            }
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) y_out[b] = acc;
+    }
+}
+
+// single block: total += sum_b y_b, total_sq += sum_b y_b^2 (fixed order)
+__global__ void k_reduce_inner(const double* __restrict__ y, int nb, double* total, double* total_sq) {
+    __shared__ double s1[256], s2[256];
+    double a = 0.0, q = 0.0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        a += y[b];
+        q = __fma_rn(y[b], y[b], q);
+    }
+    s1[threadIdx.x] = a;
+    s2[threadIdx.x] = q;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            s1[threadIdx.x] += s1[threadIdx.x + s];
+            s2[threadIdx.x] += s2[threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *total += s1[0];
+        *total_sq += s2[0];
+    }
+}
+
+int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+}  // namespace
+
+bool fused_supported(const Model& M, int target) {
+    return target == MLSK_TARGET_IDENTITY && M.dm.stream == MLSK_STREAM_PHILOX &&
+           M.dm.kind == MLSK_MODEL_GAUSS_MEAN && M.dm.dtype == MLSK_F64;
+}
+
+void fused_run(const RunArgs& a, const LevelSpec& lv, const std::vector<Segment>& segs, LevelState& st) {
+    const Model& M = *a.model;
+    Workspace& ws = *a.ws;
+    cudaStream_t s = a.stream;
+    const int64_t c = lv.c, cc = lv.cc;
+    const double n = (double)M.desc.n;
+    const double w_fine = n / (double)c;                                   // fine weight n/c
+    const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;    // n/c - n/cc on the prefix
+
+    std::vector<int64_t> ks;
+    for (const auto& sg : segs)
+        for (int64_t k = 0; k < sg.count; ++k) ks.push_back(sg.k0 + k);
+    if (ks.empty()) return;
+    const int sms = sm_count();
+
+    if (M.vector) {
+        const int64_t max_batch = 1 << 20;
+        for (size_t off = 0; off < ks.size(); off += max_batch) {
+            const int nb = (int)std::min<int64_t>(max_batch, (int64_t)ks.size() - (int64_t)off);
+            ws.ks.ensure(nb);
+            ws.v.ensure(nb);
+            MLSK_CUDA(cudaMemcpyAsync(ws.ks.p, ks.data() + off, sizeof(int64_t) * nb, cudaMemcpyHostToDevice, s));
+            uint32_t* idx = nullptr;
+            if (a.probe_host && a.probe_k > 0) {
+                ws.idx.ensure((size_t)nb * c);
+                idx = ws.idx.p;
+            }
+            const int grid = std::min<int64_t>((nb + 7) / 8, (int64_t)sms * 8);
+            k_fused_inner<<<grid, 256, 0, s>>>(M.dm, a.seed, lv.tag, ws.ks.p, nb, c, cc, w_fine, w_coarse, ws.v.p, idx);
+            k_reduce_inner<<<1, 256, 0, s>>>(ws.v.p, nb, st.total(), st.total_sq());
+            launched(2);
+            if (idx) {
+                for (int b = 0; b < nb; ++b)
+                    if (ks[off + b] < a.probe_k)
+                        MLSK_CUDA(cudaMemcpyAsync(a.probe_host + ks[off + b] * c, idx + (int64_t)b * c,
+                                                  sizeof(uint32_t) * c, cudaMemcpyDeviceToHost, s));
+            }
+            MLSK_CUDA(cudaStreamSynchronize(s));
+        }
+        st.count += (int64_t)ks.size();
+        return;
+    }
+
+    // ---- matrix path
+    const int64_t MP = (M.rows + BM - 1) / BM * BM;
+    const int64_t PP = (M.cols + BN - 1) / BN * BN;
+    const int64_t nkc = (c + KC - 1) / KC;
+    const int tiles_n = (int)(PP / BN);
+    const int T = (int)(MP / BM) * tiles_n;
+    const int Gs = std::max(1, sms / T);
+    const int64_t per_sample = (MP + PP) * nkc * KC * 8;
+    const int64_t budget = int64_t(1) << 30;
+    int64_t max_nb = std::max<int64_t>(1, budget / per_sample);
+    if (max_nb > Gs) max_nb = max_nb / Gs * Gs;  // whole rounds of the sample groups
+
+    static bool attr_set = false;
+    const int smem = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 2 * STAGES * 8;
+    if (!attr_set) {
+        MLSK_CUDA(cudaFuncSetAttribute(k_gemm_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr_set = true;
+    }
+    ws.partial.ensure((size_t)T * Gs * (BM * BN) + T * Gs);
+    double* part = ws.partial.p;
+    double* part_sq = ws.partial.p + (size_t)T * Gs * (BM * BN);
+
+    for (size_t off = 0; off < ks.size(); off += max_nb) {
+        const int nb = (int)std::min<int64_t>(max_nb, (int64_t)ks.size() - (int64_t)off);
+        ws.ks.ensure(nb);
+        ws.panel_a.ensure((size_t)nb * nkc * MP * KC);
+        ws.panel_b.ensure((size_t)nb * nkc * PP * KC);
+        MLSK_CUDA(cudaMemcpyAsync(ws.ks.p, ks.data() + off, sizeof(int64_t) * nb, cudaMemcpyHostToDevice, s));
+        uint32_t* idx = nullptr;
+        if (a.probe_host && a.probe_k > 0) {
+            ws.idx.ensure((size_t)nb * c);
+            idx = ws.idx.p;
+        }
+        const int64_t items = (int64_t)nb * nkc;
+        const int gen_grid = (int)std::min<int64_t>(items, (int64_t)sms * 4);
+        k_gen_panels_f64<<<gen_grid, GEN_THREADS, 0, s>>>(M.dm, a.seed, lv.tag, ws.ks.p, nb, c, cc, w_fine, w_coarse,
+                                                         MP, PP, nkc, ws.panel_a.p, ws.panel_b.p, idx);
+        GemmShape sh{nb, nkc, MP, PP, T, Gs, tiles_n};
+        k_gemm_f64<<<T * Gs, GEMM_THREADS, smem, s>>>(ws.panel_a.p, ws.panel_b.p, sh, part, part_sq);
+        const int64_t cells = M.rows * M.cols;
+        k_reduce_tiles<<<(int)std::min<int64_t>((cells + 255) / 256, (int64_t)sms * 8), 256, 0, s>>>(
+            part, part_sq, sh, M.rows, M.cols, st.total(), st.total_sq());
+        launched(3);
+        if (idx) {
+            for (int b = 0; b < nb; ++b)
+                if (ks[off + b] < a.probe_k)
+                    MLSK_CUDA(cudaMemcpyAsync(a.probe_host + ks[off + b] * c, idx + (int64_t)b * c,
+                                              sizeof(uint32_t) * c, cudaMemcpyDeviceToHost, s));
+        }
+    }
+    MLSK_CUDA(cudaStreamSynchronize(s));
+    st.count += (int64_t)ks.size();
+}
+
 }  // namespace mlsk

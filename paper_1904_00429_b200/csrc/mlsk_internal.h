@@ -82,6 +82,7 @@ struct Model {
 // Validates the descriptor (the reference's constructor checks) and builds it.
 void build_model(Model& M, const mlsk_model_desc* d, cudaStream_t st);
 bool model_is_vector(const mlsk_model_desc* d);
+Tables device_tables();
 
 // A level of the MLMC hierarchy (estimators.cpp:120-122 with c_l = c0 M^l).
 struct LevelSpec {

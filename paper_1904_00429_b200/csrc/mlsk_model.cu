@@ -8,6 +8,25 @@
 
 namespace mlsk {
 
+// Transform tables of the philox-mode stream (include/mlsk_stream_tables.h).
+__device__ __align__(16) const double g_sincos_d[512] = {MLSK_SINCOS_D_INIT};
+__device__ __align__(16) const double g_log_d[256] = {MLSK_LOG_D_INIT};
+__device__ __align__(16) const float g_sincos_f[128] = {MLSK_SINCOS_F_INIT};
+__device__ __align__(16) const float g_log_f[128] = {MLSK_LOG_F_INIT};
+
+Tables device_tables() {
+    static Tables t = [] {
+        Tables r{};
+        void* p;
+        MLSK_CUDA(cudaGetSymbolAddress(&p, g_sincos_d)); r.sincos_d = (const double*)p;
+        MLSK_CUDA(cudaGetSymbolAddress(&p, g_log_d)); r.log_d = (const double*)p;
+        MLSK_CUDA(cudaGetSymbolAddress(&p, g_sincos_f)); r.sincos_f = (const float*)p;
+        MLSK_CUDA(cudaGetSymbolAddress(&p, g_log_f)); r.log_f = (const float*)p;
+        return r;
+    }();
+    return t;
+}
+
 namespace {
 
 __global__ void k_means_f64(double* out, int64_t count, uint64_t key, double lo, double w) {
@@ -28,13 +47,13 @@ __global__ void k_means_f32(float* out, int64_t count, uint64_t key, float lo, f
 }
 
 // data normals (RFF X / W): element e takes z0 / z1 of block e / 2, scaled
-__global__ void k_normals_f32(float* out, int64_t count, uint64_t key, double scale) {
+__global__ void k_normals_f32(float* out, int64_t count, uint64_t key, double scale, Tables tab) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t h = e >> 1;
         const u32x4 r = philox((uint32_t)h, (uint32_t)((uint64_t)h >> 32), 1, MLSK_CTR_DATA, key);
         double z0, z1;
-        box_muller(lo64(r), hi64(r), z0, z1);
+        box_muller(lo64(r), hi64(r), z0, z1, tab);
         const double z = (e & 1) ? z1 : z0;
         out[e] = scale == 1.0 ? (float)z : (float)__dmul_rn(z, scale);
     }
@@ -138,6 +157,7 @@ void build_model(Model& M, const mlsk_model_desc* d, cudaStream_t st) {
     dm.sd = D.sd;
     dm.log2n = is_pow2(D.n) ? log2_exact(D.n) : -1;
     dm.exp_m10 = std::exp(-10.0);  // rng.hpp:75 with mean 10 (glibc)
+    dm.tab = device_tables();
 
     if (!is_pow2(D.n)) {  // sampling.cpp:32-42,96-105
         std::vector<double> cum(D.n);
@@ -230,9 +250,11 @@ void build_model(Model& M, const mlsk_model_desc* d, cudaStream_t st) {
         M.rff_w.alloc(Dd * D.n);
         M.rff_b.alloc(D.n);
         k_normals_f32<<<grid_for(D.m * Dd), 256, 0, st>>>(M.rff_x.p, D.m * Dd,
-                                                          derive_seed(D.data_seed, MLSK_TAG_DATA, 2), 1.0);
+                                                          derive_seed(D.data_seed, MLSK_TAG_DATA, 2), 1.0,
+                                                          dm.tab);
         k_normals_f32<<<grid_for(Dd * D.n), 256, 0, st>>>(M.rff_w.p, Dd * D.n,
-                                                          derive_seed(D.data_seed, MLSK_TAG_DATA, 3), 1.0 / D.sigma);
+                                                          derive_seed(D.data_seed, MLSK_TAG_DATA, 3), 1.0 / D.sigma,
+                                                          dm.tab);
         k_phases_f32<<<grid_for(D.n), 256, 0, st>>>(M.rff_b.p, D.n, derive_seed(D.data_seed, MLSK_TAG_DATA, 4));
         launched(3);
         dm.rff_x = M.rff_x.p;
