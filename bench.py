@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""bench.py -- MLMC sampled-product level estimator on B200 (BASELINE.json config 2).
+
+Workload (config 2, the metric's single-GPU configuration): A 256x4096 and
+B 4096x256 fp64, A = M + 0.5 N(0,1), B = P + 0.5 N(0,1), M, P ~ U(-1,1) fixed
+from the seed, c_l = 32 * 2^l for l = 0..6 (c_6 = 2048), coarse = first half.
+One STEP is one round of the MLMC driver at the standard allocation's level
+mix (N_l proportional to sqrt(V_l / C_l) ~ 1/c_l, so every level costs the
+same): N_l = 256 * 2^(6-l) = 16384 ... 256 level-samples per GPU.  Data are
+synthetic (no dataset is involved); inputs are generated on the device (the
+means are resident in HBM; the per-sample noise is generated in-kernel).
+
+  value  = level-samples / s over all ranks (weak scaling: every rank runs its
+           own N_l, sharded by 64-replication chunks, then one NCCL all-reduce of
+           the per-level (sum Y, sum ||Y||^2, count) buffers per round)
+  e2e    = the same metric through the public API (mlsketch.mlmc_matmul) with the
+           means passed from pinned HOST buffers and the report read back,
+           host<->device copies inside the timed region
+  roofline = the dominant kernel (k_gemm_f64, DMMA) against the fp64 tensor-pipe
+           peak measured in this run; algorithmic flops = 2 m p c per level-sample
+
+--impl reference times the reference's own CPU implementation (compiled from
+/root/reference into oracle/_ref, else the oracle port) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MASTER = 20260823
+M_, N_, P_ = 256, 4096, 256
+C0, LEVELS = 32, 6
+STEP_N = [256 * 2 ** (LEVELS - l) for l in range(LEVELS + 1)]          # 16384 ... 256
+CPU_SAMPLE_N = [512, 256, 128, 64, 32, 16, 8]                          # bounded CPU sample
+REF_STEP_N = [128, 64, 32, 16, 8, 4, 2]                                # --impl reference step
+METRIC = "MLMC level-samples/s (config 2: 256x4096x256 fp64, c_l=32*2^l, L=6, standard-allocation level mix)"
+UNIT = "level-samples/s"
+
+
+def flops_of(N):
+    return sum(2.0 * M_ * P_ * C0 * 2 ** l * n for l, n in enumerate(N))
+
+
+def data_seed():
+    from paper_1904_00429_b200.mlsketch import RngStream
+    return RngStream.derive_seed(MASTER, 0xD47A0002, 0)
+
+
+def config_dict(world, flush):
+    return {"workload": "config2: A 256x4096, B 4096x256 fp64 gaussian(U(-1,1) means, sd 0.5); "
+                        "c0=32, M=2, L=6; step = N_l = 256*2^(6-l) per GPU",
+            "m": M_, "n": N_, "p": P_, "c0": C0, "M": 2, "L": LEVELS, "N_per_gpu": STEP_N,
+            "stream": "philox4x32-10", "engine": "fused (gen_panels_f64 + gemm_f64 DMMA)",
+            "l2": flush, "parallelism": f"dp{world} (64-replication chunk sharding)"}
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------- CPU baselines
+
+
+def cpu_reference_run(N, threads=None):
+    """Reference (or oracle-port) CPU time for level counts N; returns (seconds, kind)."""
+    import ctypes as C
+    from oracle import pyoracle as po
+    from paper_1904_00429_b200 import _abi as abi
+    threads = threads or os.cpu_count()
+    desc = po.model_desc(abi.MODEL_GAUSS_MEAN, n=N_, m=M_, p=P_, sd=0.5, mean_lo=-1.0, mean_hi=1.0,
+                         stream=abi.STREAM_REF, data_seed=data_seed())
+    om = po.OracleModel(desc)
+    if os.path.exists(po.REF_SO):
+        ma, mb = om.means()
+        rdesc = po.model_desc(abi.MODEL_GAUSS_MEAN, n=N_, m=M_, p=P_, sd=0.5, stream=abi.STREAM_REF,
+                              mean_a=ma, mean_b=mb)
+        plan = po.make_plan(2, C0, N)
+        ck = C.c_double()
+        dt = po.ref_lib().ref_throughput(C.byref(rdesc), 0, 1e-12, C.byref(plan), MASTER, threads, C.byref(ck))
+        if dt < 0:
+            raise RuntimeError(po.ref_lib().ref_last_error().decode())
+        return dt, "reference", threads
+    # oracle port: single-threaded C restatement of the same per-replication work
+    t0 = time.perf_counter()
+    om.mlmc(2, C0, N, MASTER)
+    return time.perf_counter() - t0, "port", 1
+
+
+def cpu_baseline_obj(N):
+    dt, kind, cores = cpu_reference_run(N)
+    return {"value": sum(N) / dt, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"config 2, N_l={N} (full reference per-replication work: fresh 256x4096 + 4096x256 "
+                      f"mt19937_64/Box-Muller draw, draw_realization, sketch_matmul fine + coarse), "
+                      f"{dt:.2f} s wall"}
+
+
+def run_reference_arm(args, rank):
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        cpu_reference_run([1] * (LEVELS + 1))
+    times = []
+    kind, cores = None, None
+    for _ in range(args.steps):
+        dt, kind, cores = cpu_reference_run(REF_STEP_N)
+        times.append(dt)
+    total = sum(times)
+    value = args.steps * sum(REF_STEP_N) / total
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "config2 (reference CPU, bounded sample per step)", "m": M_, "n": N_, "p": P_,
+                       "c0": C0, "M": 2, "L": LEVELS, "N_per_step": REF_STEP_N, "threads": cores},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": f"N_l={REF_STEP_N} per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------- GPU arm
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mlsk", choices=["mlsk", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference_arm(args, rank)
+
+    import torch
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    from paper_1904_00429_b200 import mlsketch as g
+    from paper_1904_00429_b200._lib import lib
+    L = lib()
+
+    stream = torch.cuda.current_stream()
+    opts = g.EstimatorOptions(device=local_rank, stream=stream.cuda_stream, rank=rank, world=world, engine="fused")
+    model = g.gaussian_mean_matrix_model(M_, N_, P_, sd=0.5, mean_lo=-1.0, mean_hi=1.0, data_seed=data_seed())
+    sess = g.MlmcSession(model, g.target_identity(), 2, LEVELS, MASTER, c0=C0, options=opts)
+    dN = [n * world for n in STEP_N]          # global counts; this rank runs its chunks (~N_l)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # 512 MB > L2 (126 MB)
+
+    class _Dev:  # zero-copy torch view of the session's packed device buffer
+        def __init__(self, ptr, n):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                             "version": 3, "stream": None}
+
+    def step():
+        sess.run_round(dN)
+        if dist is not None:
+            p, n = sess.level_buffer()          # packed on the same stream (device-side)
+            dist.all_reduce(torch.as_tensor(_Dev(p, n), device="cuda"))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    peak = L.mlsk_measure_fp64_peak(local_rank)
+    L.mlsk_profile_reset()
+    L.mlsk_profile_enable(1)
+    launches0 = L.mlsk_kernel_launch_count()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = []
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            flush.zero_()                       # evict L2 between timed steps
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    L.mlsk_profile_enable(0)
+    launches = L.mlsk_kernel_launch_count() - launches0
+    total_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # per-kernel event timings (this rank)
+    import ctypes as C
+    kern = {}
+    name = C.create_string_buffer(64)
+    nl, ms = C.c_int64(), C.c_double()
+    n_entries = L.mlsk_profile_read(0, name, 64, C.byref(nl), C.byref(ms))
+    for i in range(n_entries):
+        L.mlsk_profile_read(i, name, 64, C.byref(nl), C.byref(ms))
+        kern[name.value.decode()] = {"launches": nl.value, "ms": ms.value}
+
+    samples_total = args.steps * sum(dN)
+    value = samples_total / (total_ms * 1e-3)
+    flops_total = args.steps * flops_of(dN)
+    gemm = kern.get("gemm_f64", {"launches": 0, "ms": 0.0})
+    rank_flops = args.steps * flops_of(STEP_N)
+    achieved = rank_flops / (gemm["ms"] * 1e-3) / 1e12 if gemm["ms"] > 0 else None
+    traffic = None
+    prof_json = os.path.join(ROOT, "profiles", "gemm_f64_traffic.json")
+    if os.path.exists(prof_json):
+        try:
+            traffic = json.load(open(prof_json)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    e2e = None
+    if not args.no_e2e and rank == 0:
+        e2e = run_e2e(g, torch, local_rank, args)
+
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
+        try:
+            cpu = cpu_baseline_obj(CPU_SAMPLE_N)
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "unavailable", "sample": str(e)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config_dict(world, "flushed (512 MB write) before every timed step"),
+                "sampled_gemm_tflops": flops_total / (total_ms * 1e-3) / 1e12,
+                "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                             "frac": (achieved / peak) if achieved and peak > 0 else None,
+                             "traffic": traffic, "kernel": "k_gemm_f64 (DMMA m8n8k4, fp64)",
+                             "peak_source": "fp64 DMMA throughput measured in this run "
+                                            "(MEASURED_PEAKS.json has no fp64 entry)",
+                             "algorithmic": "2*m*p*c_l flops per level-sample"},
+                "kernels": kern,
+                "step_fraction_gemm": (gemm["ms"] / sum(v["ms"] for v in kern.values())) if kern else None,
+                "gpu_launches": launches,
+                "clocks": clk.summary(),
+                "e2e": e2e,
+                "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    sess.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(g, torch, device, args):
+    """Public-API call per step: means from pinned host buffers -> device,
+    all levels, report back to the host."""
+    from oracle import pyoracle as po  # only to materialise the same host means
+    from paper_1904_00429_b200 import _abi as abi
+    om = po.OracleModel(po.model_desc(abi.MODEL_GAUSS_MEAN, n=N_, m=M_, p=P_, sd=0.5, mean_lo=-1.0,
+                                      mean_hi=1.0, data_seed=data_seed()))
+    ma, mb = om.means()
+    pa = torch.from_numpy(ma).pin_memory().numpy()
+    pb = torch.from_numpy(mb).pin_memory().numpy()
+    model = g.gaussian_mean_matrix_model(M_, N_, P_, sd=0.5, mean_a=pa, mean_b=pb)
+    plan = g.LevelPlan(2, LEVELS, STEP_N, c0=C0)
+    opts = g.EstimatorOptions(device=device, engine="fused")
+    for _ in range(max(1, args.warmup)):
+        g.mlmc_matmul(model, g.target_identity(), plan, MASTER, opts)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        r = g.mlmc_matmul(model, g.target_identity(), plan, MASTER + 1 + i, opts)
+    dt = time.perf_counter() - t0
+    cells = M_ * P_
+    levels = LEVELS + 1
+    d2h = 8 * (cells + 2 * levels * cells + 2 * levels) + 8 * 2 * levels
+    return {"value": args.steps * sum(STEP_N) / dt, "unit": UNIT,
+            "h2d_bytes_per_step": int(pa.nbytes + pb.nbytes + 8 * levels),
+            "d2h_bytes_per_step": int(d2h),
+            "note": "mlsketch.mlmc_matmul with host mean buffers; wall clock, synchronous API"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -194,6 +194,15 @@ int mlsk_device_count(void);
 /* Number of kernels this thread's library calls have launched so far. */
 int64_t mlsk_kernel_launch_count(void);
 
+/* ---- measurement (bench.py) ----------------------------------------------- */
+/* Per-kernel CUDA-event timing on the launching stream: enable, reset, then
+ * read entry i (returns the number of entries): name, launches, total ms. */
+int mlsk_profile_enable(int on);
+int mlsk_profile_reset(void);
+int mlsk_profile_read(int i, char* name, int name_len, int64_t* launches, double* ms);
+/* fp64 tensor-pipe (DMMA) throughput measured on the device, TFLOP/s. */
+double mlsk_measure_fp64_peak(int device);
+
 #ifdef __cplusplus
 }
 #endif

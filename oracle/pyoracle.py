@@ -110,6 +110,9 @@ def ref_lib():
                           C.c_int32, _P(abi.Report)]
         L.ref_mc_native.argtypes = [_P(abi.ModelDesc), C.c_int32, C.c_double, C.c_int64, C.c_int64,
                                     C.c_int64, C.c_uint64, C.c_int32, _P(abi.Report)]
+        L.ref_throughput.restype = C.c_double
+        L.ref_throughput.argtypes = [_P(abi.ModelDesc), C.c_int32, C.c_double, _P(abi.Plan), C.c_uint64,
+                                     C.c_int32, _f64p]
         L.ref_time_sketch_matmul.restype = C.c_double
         L.ref_time_sketch_matmul.argtypes = [C.c_int64] * 4 + [C.c_uint64, C.c_int32]
         L.ref_last_error.restype = C.c_char_p

@@ -15,7 +15,9 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <atomic>
 #include <memory>
+#include <thread>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -354,6 +356,74 @@ int ref_mc_native(const mlsk_model_desc* d, int32_t tgt, double tp, int64_t L, i
         return 0;
     } catch (const std::exception& e) {
         return fail(e);
+    }
+}
+
+// CPU-baseline throughput run: every (level, replication) item of the plan
+// executes the reference's per-replication body (estimators.cpp:133-158:
+// RngStream::derive, model.draw, draw_realization, sketch fine + coarse
+// prefix, f, accumulate) and the items are spread over `threads` host
+// threads with an atomic counter (the reference's parallel_chunks caps a
+// level at ceil(N_l / 64) threads, which would idle most cores on a bounded
+// sample).  Returns the wall time in seconds; *checksum gets sum of ||Y||^2.
+double ref_throughput(const mlsk_model_desc* d, int32_t tgt, double tp, const mlsk_plan* plan,
+                      uint64_t seed, int32_t threads, double* checksum) {
+    try {
+        const TargetFunction f = target(tgt, tp);
+        const bool vec = is_vector(d);
+        std::unique_ptr<VectorPairModel> vm;
+        std::unique_ptr<MatrixPairModel> mm;
+        std::size_t n;
+        if (vec) { vm = std::make_unique<VectorPairModel>(vector_model(d)); n = vm->n; }
+        else { mm = std::make_unique<MatrixPairModel>(matrix_model(d)); n = mm->n; }
+        const IndexDistribution dist = IndexDistribution::uniform(n);
+        std::vector<std::pair<int64_t, int64_t>> items;  // (level, k)
+        for (int64_t l = 0; l <= plan->L; ++l)
+            for (int64_t k = 0; k < plan->N[l]; ++k) items.emplace_back(l, k);
+        std::atomic<std::size_t> next{0};
+        std::vector<double> part(std::max(1, threads), 0.0);
+        const auto t0 = std::chrono::steady_clock::now();
+        auto worker = [&](int w) {
+            double acc = 0.0;
+            for (;;) {
+                const std::size_t i = next.fetch_add(1);
+                if (i >= items.size()) break;
+                const auto [l, k] = items[i];
+                const std::size_t fine = (std::size_t)(plan->c0 * ipow(plan->M, l));
+                const std::size_t coarse = l > 0 ? fine / plan->M : 0;
+                RngStream rng = RngStream::derive(seed, l, k);
+                if (vec) {
+                    auto [a, b] = vm->draw(rng);
+                    const Realization r = draw_realization(dist, fine, rng);
+                    double v = f.f(sketch_inner(a, b, r, dist));
+                    if (l > 0) v -= f.f(sketch_inner(a, b, std::span<const uint32_t>(r.indices.data(), coarse), dist));
+                    acc += v * v;
+                } else {
+                    auto [A, B] = mm->draw(rng);
+                    const Realization r = draw_realization(dist, fine, rng);
+                    DenseMatrix v = sketch_matmul(A, B, r, dist);
+                    for (double& x : v.data()) x = f.f(x);
+                    if (l > 0) {
+                        const DenseMatrix cv =
+                            sketch_matmul(A, B, std::span<const uint32_t>(r.indices.data(), coarse), dist);
+                        for (std::size_t t = 0; t < v.data().size(); ++t) v.data()[t] -= f.f(cv.data()[t]);
+                    }
+                    for (double x : v.data()) acc += x * x;
+                }
+            }
+            part[w] = acc;
+        };
+        std::vector<std::thread> pool;
+        for (int w = 0; w < std::max(1, threads); ++w) pool.emplace_back(worker, w);
+        for (auto& t : pool) t.join();
+        const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        double sum = 0.0;
+        for (double x : part) sum += x;
+        if (checksum) *checksum = sum;
+        return dt;
+    } catch (const std::exception& e) {
+        fail(e);
+        return -1.0;
     }
 }
 

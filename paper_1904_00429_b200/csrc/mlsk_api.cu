@@ -3,6 +3,7 @@
 // Mirrors the reference entry points (estimators.hpp:58-80, sketch.hpp:17-51)
 // with the reference's validation order and error classes; maps internal
 // exceptions to status codes and keeps a thread-local last-error message.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -114,12 +115,27 @@ struct Runner {
         engine = requested == MLSK_ENGINE_AUTO ? (fused_ok ? MLSK_ENGINE_FUSED : MLSK_ENGINE_EXACT) : requested;
     }
 
-    void run(const LevelSpec& lv, int64_t k0, int64_t k1, LevelState& st, cudaStream_t s, int64_t probe_k,
-             uint32_t* probe) {
-        const auto segs = plan_segments(k0, k1, rank, world, st);
-        RunArgs a{&model, target, tparam, seed, s, &ws, probe_k, probe};
-        if (engine == MLSK_ENGINE_FUSED) fused_run(a, lv, segs, st);
-        else exact_run(a, lv, segs, st);
+    // one level (estimators) or several levels (a session round) at once
+    struct Item {
+        LevelSpec lv;
+        int64_t k0, k1;
+        LevelState* st;
+        uint32_t* probe;
+    };
+    void run(const std::vector<Item>& items, cudaStream_t s, int64_t probe_k) {
+        if (engine == MLSK_ENGINE_FUSED) {
+            std::vector<FusedJob> jobs;
+            for (const auto& it : items)
+                jobs.push_back(FusedJob{it.lv, plan_segments(it.k0, it.k1, rank, world, *it.st), it.st, it.probe});
+            RunArgs a{&model, target, tparam, seed, s, &ws, probe_k, nullptr};
+            fused_run_round(a, jobs);
+            return;
+        }
+        for (const auto& it : items) {
+            const auto segs = plan_segments(it.k0, it.k1, rank, world, *it.st);
+            RunArgs a{&model, target, tparam, seed, s, &ws, probe_k, it.probe};
+            exact_run(a, it.lv, segs, *it.st);
+        }
     }
 };
 
@@ -158,14 +174,21 @@ int mlmc_impl(bool matrix, const mlsk_model_desc* model, int32_t target, double 
         std::vector<double> value(cells, 0.0), sum;
         int64_t total_cost = 0;
         const int64_t cL = plan->c0 * ipow(plan->M, plan->L);
+        std::vector<LevelState> states(plan->L + 1);
+        std::vector<Runner::Item> items;
         for (int64_t l = 0; l <= plan->L; ++l) {
             const int64_t fine = plan->c0 * ipow(plan->M, l);
             const int64_t coarse = l > 0 ? fine / plan->M : 0;
-            LevelState st;
-            st.init(cells, ex.stream);
+            states[l].init(cells, ex.stream);
             uint32_t* probe = nullptr;
             if (ex.probe_out && ex.probe_k > 0 && l > 0) probe = ex.probe_out + l * ex.probe_k * cL;
-            R.run(LevelSpec{(uint64_t)l, fine, coarse}, 0, plan->N[l], st, ex.stream, ex.probe_k, probe);
+            items.push_back({LevelSpec{(uint64_t)l, fine, coarse}, 0, plan->N[l], &states[l], probe});
+        }
+        R.run(items, ex.stream, ex.probe_k);  // all levels as one round
+        for (int64_t l = 0; l <= plan->L; ++l) {
+            const int64_t fine = plan->c0 * ipow(plan->M, l);
+            const int64_t coarse = l > 0 ? fine / plan->M : 0;
+            const LevelState& st = states[l];
             double sq;
             read_level(st, ex.stream, sum, sq);
             const double inv_n = 1.0 / (double)plan->N[l];
@@ -215,7 +238,7 @@ int mc_impl(bool matrix, const mlsk_model_desc* model, int32_t target, double tp
         const int64_t s = c0 * ipow(M, L);
         LevelState st;
         st.init(cells, ex.stream);
-        R.run(LevelSpec{MLSK_TAG_MC, s, 0}, 0, N, st, ex.stream, 0, nullptr);
+        R.run({{LevelSpec{MLSK_TAG_MC, s, 0}, 0, N, &st, nullptr}}, ex.stream, 0);
         std::vector<double> sum;
         double sq;
         read_level(st, ex.stream, sum, sq);
@@ -239,6 +262,18 @@ int mc_impl(bool matrix, const mlsk_model_desc* model, int32_t target, double tp
 }  // namespace
 
 int mlsk::run_guarded(const std::function<void()>& body) { return guard(body); }
+
+namespace {
+// packed[0..cells] = total (+ open), packed[cells] = sum of squares, packed[cells+1] = count
+__global__ void k_pack_level(const double* __restrict__ total, const double* __restrict__ open, int64_t cells,
+                             int has_open, double count, double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= cells + 1;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i <= cells) out[i] = has_open ? __dadd_rn(total[i], open[i]) : total[i];
+        else out[i] = count;
+    }
+}
+}  // namespace
 
 struct mlsk_session {
     std::unique_ptr<Exec> ex;
@@ -305,13 +340,15 @@ int mlsk_session_run_round(mlsk_session* s, const int64_t* dN) {
         for (int64_t l = 0; l <= s->L; ++l)
             if (dN[l] < 0) invalid("session: dN must be non-negative");
         MLSK_CUDA(cudaSetDevice(s->ex->device));
+        std::vector<Runner::Item> items;
         for (int64_t l = 0; l <= s->L; ++l) {
             if (dN[l] == 0) continue;
             const int64_t fine = s->c0 * ipow(s->M, l), coarse = l > 0 ? fine / s->M : 0;
-            s->R.run(LevelSpec{(uint64_t)l, fine, coarse}, s->next_k[l], s->next_k[l] + dN[l], s->levels[l],
-                     s->ex->stream, 0, nullptr);
+            items.push_back({LevelSpec{(uint64_t)l, fine, coarse}, s->next_k[l], s->next_k[l] + dN[l], &s->levels[l],
+                             nullptr});
             s->next_k[l] += dN[l];
         }
+        s->R.run(items, s->ex->stream, 0);
     });
 }
 
@@ -348,23 +385,18 @@ int mlsk_session_stats(mlsk_session* s, mlsk_report* rep) {
 int mlsk_session_level_buffer(mlsk_session* s, void** device_ptr, int64_t* n_doubles) {
     return guard([&] {
         if (!s || !device_ptr || !n_doubles) invalid("session: null argument");
+        MLSK_CUDA(cudaSetDevice(s->ex->device));
         const int64_t cells = s->R.model.rows * s->R.model.cols;
-        // pack [(sum, sumsq, count)] per level (sum includes the open chunk)
-        std::vector<double> host((size_t)(s->L + 1) * (cells + 2));
+        // pack [(sum Y, sum ||Y||^2, count)] per level on the device (sum includes the open chunk)
         for (int64_t l = 0; l <= s->L; ++l) {
-            std::vector<double> sum;
-            double sq;
-            read_level(s->levels[l], s->ex->stream, sum, sq);
-            double* row = host.data() + l * (cells + 2);
-            std::memcpy(row, sum.data(), sizeof(double) * cells);
-            row[cells] = sq;
-            row[cells + 1] = (double)s->levels[l].count;
+            const LevelState& st = s->levels[l];
+            k_pack_level<<<(int)std::min<int64_t>((cells + 256) / 256, 1184), 256, 0, s->ex->stream>>>(
+                st.total(), st.open(), cells, st.open_count > 0 ? 1 : 0, (double)st.count,
+                s->packed.p + l * (cells + 2));
+            launched();
         }
-        MLSK_CUDA(cudaMemcpyAsync(s->packed.p, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice,
-                                  s->ex->stream));
-        MLSK_CUDA(cudaStreamSynchronize(s->ex->stream));
         *device_ptr = s->packed.p;
-        *n_doubles = (int64_t)host.size();
+        *n_doubles = (int64_t)(s->L + 1) * (cells + 2);
     });
 }
 

@@ -429,60 +429,172 @@ bool fused_supported(const Model& M, int target) {
            M.dm.kind == MLSK_MODEL_GAUSS_MEAN && M.dm.dtype == MLSK_F64;
 }
 
-void fused_run(const RunArgs& a, const LevelSpec& lv, const std::vector<Segment>& segs, LevelState& st) {
+namespace {
+
+constexpr int NBUF = 3;  // panel buffers in flight (gen i+1, i+2 while GEMM i)
+
+// Engine-private pipeline state kept in the Workspace across rounds.
+struct Pipe {
+    cudaStream_t s_gen = nullptr, s_mm = nullptr;
+    cudaEvent_t start = nullptr, end = nullptr, staged = nullptr;
+    cudaEvent_t gen_done[NBUF] = {}, mm_done[NBUF] = {};
+    bool used[NBUF] = {};
+    DevArray<double> panels[NBUF];
+    DevArray<uint32_t> idx[NBUF];
+    DevArray<int64_t> ks;      // all replication indices of the round
+    int64_t* ks_host = nullptr;  // pinned staging
+    size_t ks_cap = 0;
+    DevArray<double> part;
+    bool staged_pending = false;
+    Pipe() {
+        int lo = 0, hi = 0;
+        MLSK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        MLSK_CUDA(cudaStreamCreateWithPriority(&s_mm, cudaStreamNonBlocking, hi));   // GEMM: highest
+        MLSK_CUDA(cudaStreamCreateWithPriority(&s_gen, cudaStreamNonBlocking, lo));  // generator: lowest
+        MLSK_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+        MLSK_CUDA(cudaEventCreateWithFlags(&end, cudaEventDisableTiming));
+        MLSK_CUDA(cudaEventCreateWithFlags(&staged, cudaEventDisableTiming));
+        for (int i = 0; i < NBUF; ++i) {
+            MLSK_CUDA(cudaEventCreateWithFlags(&gen_done[i], cudaEventDisableTiming));
+            MLSK_CUDA(cudaEventCreateWithFlags(&mm_done[i], cudaEventDisableTiming));
+        }
+    }
+    ~Pipe() {
+        if (s_gen) cudaStreamSynchronize(s_gen);
+        if (s_mm) cudaStreamSynchronize(s_mm);
+        for (int i = 0; i < NBUF; ++i) {
+            cudaEventDestroy(gen_done[i]);
+            cudaEventDestroy(mm_done[i]);
+        }
+        cudaEventDestroy(start);
+        cudaEventDestroy(end);
+        cudaEventDestroy(staged);
+        if (ks_host) cudaFreeHost(ks_host);
+        if (s_gen) cudaStreamDestroy(s_gen);
+        if (s_mm) cudaStreamDestroy(s_mm);
+    }
+    void stage_ks(const std::vector<int64_t>& h, cudaStream_t s) {
+        if (staged_pending) MLSK_CUDA(cudaEventSynchronize(staged));  // previous round's copy done
+        if (h.size() > ks_cap) {
+            if (ks_host) cudaFreeHost(ks_host);
+            ks_cap = std::max<size_t>(h.size(), 1 << 16);
+            MLSK_CUDA(cudaMallocHost(&ks_host, ks_cap * sizeof(int64_t)));
+        }
+        std::memcpy(ks_host, h.data(), h.size() * sizeof(int64_t));
+        ks.ensure(h.size());
+        MLSK_CUDA(cudaMemcpyAsync(ks.p, ks_host, h.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        MLSK_CUDA(cudaEventRecord(staged, s));
+        staged_pending = true;
+    }
+};
+
+Pipe& pipe_of(Workspace& ws) {
+    if (!ws.fused) ws.fused = std::shared_ptr<void>(new Pipe(), [](void* p) { delete static_cast<Pipe*>(p); });
+    return *static_cast<Pipe*>(ws.fused.get());
+}
+
+struct Batch {
+    size_t job;
+    int64_t off;  // into the job's replication list
+    int nb;
+    int64_t ks_off;  // into the round's device ks array
+};
+
+}  // namespace
+
+void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
     const Model& M = *a.model;
     Workspace& ws = *a.ws;
-    cudaStream_t s = a.stream;
-    const int64_t c = lv.c, cc = lv.cc;
-    const double n = (double)M.desc.n;
-    const double w_fine = n / (double)c;                                   // fine weight n/c
-    const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;    // n/c - n/cc on the prefix
-
-    std::vector<int64_t> ks;
-    for (const auto& sg : segs)
-        for (int64_t k = 0; k < sg.count; ++k) ks.push_back(sg.k0 + k);
-    if (ks.empty()) return;
+    Pipe& P = pipe_of(ws);
     const int sms = sm_count();
+    const double n = (double)M.desc.n;
+
+    // replication lists of all jobs, staged to the device once per round
+    std::vector<std::vector<int64_t>> jks(jobs.size());
+    std::vector<int64_t> all;
+    std::vector<int64_t> job_off(jobs.size());
+    for (size_t j = 0; j < jobs.size(); ++j) {
+        for (const auto& sg : jobs[j].segs)
+            for (int64_t k = 0; k < sg.count; ++k) jks[j].push_back(sg.k0 + k);
+        job_off[j] = (int64_t)all.size();
+        all.insert(all.end(), jks[j].begin(), jks[j].end());
+    }
+    if (all.empty()) return;
+    const bool probing = a.probe_k > 0;
+    MLSK_CUDA(cudaEventRecord(P.start, a.stream));
+    MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.start, 0));
+    MLSK_CUDA(cudaStreamWaitEvent(P.s_mm, P.start, 0));
+    P.stage_ks(all, P.s_gen);
 
     if (M.vector) {
-        const int64_t max_batch = 1 << 20;
-        for (size_t off = 0; off < ks.size(); off += max_batch) {
-            const int nb = (int)std::min<int64_t>(max_batch, (int64_t)ks.size() - (int64_t)off);
-            ws.ks.ensure(nb);
-            ws.v.ensure(nb);
-            MLSK_CUDA(cudaMemcpyAsync(ws.ks.p, ks.data() + off, sizeof(int64_t) * nb, cudaMemcpyHostToDevice, s));
-            uint32_t* idx = nullptr;
-            if (a.probe_host && a.probe_k > 0) {
-                ws.idx.ensure((size_t)nb * c);
-                idx = ws.idx.p;
+        // config-1 shape: one warp per replication, no panels
+        for (size_t j = 0; j < jobs.size(); ++j) {
+            FusedJob& job = jobs[j];
+            const int64_t c = job.lv.c, cc = job.lv.cc;
+            const double w_fine = n / (double)c;
+            const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;
+            const int64_t total = (int64_t)jks[j].size();
+            const int64_t max_batch = 1 << 20;
+            for (int64_t off = 0; off < total; off += max_batch) {
+                const int nb = (int)std::min<int64_t>(max_batch, total - off);
+                ws.v.ensure(nb);
+                uint32_t* idx = nullptr;
+                if (job.probe_host) {
+                    ws.idx.ensure((size_t)nb * c);
+                    idx = ws.idx.p;
+                }
+                const int grid = (int)std::min<int64_t>((nb + 7) / 8, (int64_t)sms * 8);
+                {
+                    Prof p("fused_inner_f64", P.s_gen);
+                    k_fused_inner<<<grid, 256, 0, P.s_gen>>>(M.dm, a.seed, job.lv.tag, P.ks.p + job_off[j] + off, nb,
+                                                             c, cc, w_fine, w_coarse, ws.v.p, idx);
+                }
+                {
+                    Prof p("reduce_inner", P.s_gen);
+                    k_reduce_inner<<<1, 256, 0, P.s_gen>>>(ws.v.p, nb, job.st->total(), job.st->total_sq());
+                }
+                launched(2);
+                if (idx) {
+                    MLSK_CUDA(cudaStreamSynchronize(P.s_gen));
+                    for (int b = 0; b < nb; ++b)
+                        if (jks[j][off + b] < a.probe_k)
+                            MLSK_CUDA(cudaMemcpy(job.probe_host + jks[j][off + b] * c, idx + (int64_t)b * c,
+                                                 sizeof(uint32_t) * c, cudaMemcpyDeviceToHost));
+                }
             }
-            const int grid = std::min<int64_t>((nb + 7) / 8, (int64_t)sms * 8);
-            k_fused_inner<<<grid, 256, 0, s>>>(M.dm, a.seed, lv.tag, ws.ks.p, nb, c, cc, w_fine, w_coarse, ws.v.p, idx);
-            k_reduce_inner<<<1, 256, 0, s>>>(ws.v.p, nb, st.total(), st.total_sq());
-            launched(2);
-            if (idx) {
-                for (int b = 0; b < nb; ++b)
-                    if (ks[off + b] < a.probe_k)
-                        MLSK_CUDA(cudaMemcpyAsync(a.probe_host + ks[off + b] * c, idx + (int64_t)b * c,
-                                                  sizeof(uint32_t) * c, cudaMemcpyDeviceToHost, s));
-            }
-            MLSK_CUDA(cudaStreamSynchronize(s));
+            job.st->count += total;
         }
-        st.count += (int64_t)ks.size();
+        MLSK_CUDA(cudaEventRecord(P.end, P.s_gen));
+        MLSK_CUDA(cudaStreamWaitEvent(a.stream, P.end, 0));
         return;
     }
 
-    // ---- matrix path
+    // ---- matrix path: batches of replications, software-pipelined
     const int64_t MP = (M.rows + BM - 1) / BM * BM;
     const int64_t PP = (M.cols + BN - 1) / BN * BN;
-    const int64_t nkc = (c + KC - 1) / KC;
     const int tiles_n = (int)(PP / BN);
     const int T = (int)(MP / BM) * tiles_n;
     const int Gs = std::max(1, sms / T);
-    const int64_t per_sample = (MP + PP) * nkc * KC * 8;
-    const int64_t budget = int64_t(1) << 30;
-    int64_t max_nb = std::max<int64_t>(1, budget / per_sample);
-    if (max_nb > Gs) max_nb = max_nb / Gs * Gs;  // whole rounds of the sample groups
+    const int64_t budget = int64_t(384) << 20;  // panel bytes per batch (x NBUF in flight)
+
+    std::vector<Batch> batches;
+    int64_t max_panel = 0;
+    for (size_t j = 0; j < jobs.size(); ++j) {
+        const int64_t nkc = (jobs[j].lv.c + KC - 1) / KC;
+        const int64_t per = (MP + PP) * nkc * KC;
+        int64_t max_nb = std::max<int64_t>(1, budget / (per * 8));
+        if (max_nb > Gs) max_nb = max_nb / Gs * Gs;
+        const int64_t total = (int64_t)jks[j].size();
+        for (int64_t off = 0; off < total; off += max_nb) {
+            const int nb = (int)std::min<int64_t>(max_nb, total - off);
+            batches.push_back({j, off, nb, job_off[j] + off});
+            max_panel = std::max(max_panel, nb * per);
+        }
+    }
+    for (int i = 0; i < NBUF; ++i) P.panels[i].ensure((size_t)max_panel);
+    P.part.ensure((size_t)T * Gs * (BM * BN) + (size_t)T * Gs);
+    double* part = P.part.p;
+    double* part_sq = P.part.p + (size_t)T * Gs * (BM * BN);
 
     static bool attr_set = false;
     const int smem = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 2 * STAGES * 8;
@@ -490,40 +602,65 @@ void fused_run(const RunArgs& a, const LevelSpec& lv, const std::vector<Segment>
         MLSK_CUDA(cudaFuncSetAttribute(k_gemm_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr_set = true;
     }
-    ws.partial.ensure((size_t)T * Gs * (BM * BN) + T * Gs);
-    double* part = ws.partial.p;
-    double* part_sq = ws.partial.p + (size_t)T * Gs * (BM * BN);
 
-    for (size_t off = 0; off < ks.size(); off += max_nb) {
-        const int nb = (int)std::min<int64_t>(max_nb, (int64_t)ks.size() - (int64_t)off);
-        ws.ks.ensure(nb);
-        ws.panel_a.ensure((size_t)nb * nkc * MP * KC);
-        ws.panel_b.ensure((size_t)nb * nkc * PP * KC);
-        MLSK_CUDA(cudaMemcpyAsync(ws.ks.p, ks.data() + off, sizeof(int64_t) * nb, cudaMemcpyHostToDevice, s));
+    for (size_t i = 0; i < batches.size(); ++i) {
+        const Batch& bt = batches[i];
+        FusedJob& job = jobs[bt.job];
+        const int64_t c = job.lv.c, cc = job.lv.cc;
+        const int64_t nkc = (c + KC - 1) / KC;
+        const double w_fine = n / (double)c;                                 // n/c
+        const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;  // n/c - n/cc on the prefix
+        const int buf = (int)(i % NBUF);
+        double* Apan = P.panels[buf].p;
+        double* Bpan = Apan + (size_t)bt.nb * nkc * MP * KC;
         uint32_t* idx = nullptr;
-        if (a.probe_host && a.probe_k > 0) {
-            ws.idx.ensure((size_t)nb * c);
-            idx = ws.idx.p;
+        if (job.probe_host) {
+            P.idx[buf].ensure((size_t)bt.nb * c);
+            idx = P.idx[buf].p;
         }
-        const int64_t items = (int64_t)nb * nkc;
-        const int gen_grid = (int)std::min<int64_t>(items, (int64_t)sms * 4);
-        k_gen_panels_f64<<<gen_grid, GEN_THREADS, 0, s>>>(M.dm, a.seed, lv.tag, ws.ks.p, nb, c, cc, w_fine, w_coarse,
-                                                         MP, PP, nkc, ws.panel_a.p, ws.panel_b.p, idx);
-        GemmShape sh{nb, nkc, MP, PP, T, Gs, tiles_n};
-        k_gemm_f64<<<T * Gs, GEMM_THREADS, smem, s>>>(ws.panel_a.p, ws.panel_b.p, sh, part, part_sq);
+        // generator: wait until the GEMM that last used this buffer is done
+        if (P.used[buf]) MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.mm_done[buf], 0));
+        const int64_t items = (int64_t)bt.nb * nkc;
+        {
+            Prof p("gen_panels_f64", P.s_gen);
+            k_gen_panels_f64<<<(int)std::min<int64_t>(items, (int64_t)sms * 4), GEN_THREADS, 0, P.s_gen>>>(
+                M.dm, a.seed, job.lv.tag, P.ks.p + bt.ks_off, bt.nb, c, cc, w_fine, w_coarse, MP, PP, nkc, Apan,
+                Bpan, idx);
+        }
+        MLSK_CUDA(cudaEventRecord(P.gen_done[buf], P.s_gen));
+        // GEMM + fused level epilogue + fixed-order reduction
+        MLSK_CUDA(cudaStreamWaitEvent(P.s_mm, P.gen_done[buf], 0));
+        GemmShape sh{bt.nb, nkc, MP, PP, T, Gs, tiles_n};
+        {
+            Prof p("gemm_f64", P.s_mm);
+            k_gemm_f64<<<T * Gs, GEMM_THREADS, smem, P.s_mm>>>(Apan, Bpan, sh, part, part_sq);
+        }
         const int64_t cells = M.rows * M.cols;
-        k_reduce_tiles<<<(int)std::min<int64_t>((cells + 255) / 256, (int64_t)sms * 8), 256, 0, s>>>(
-            part, part_sq, sh, M.rows, M.cols, st.total(), st.total_sq());
+        {
+            Prof p("reduce_tiles", P.s_mm);
+            k_reduce_tiles<<<(int)std::min<int64_t>((cells + 255) / 256, (int64_t)sms * 8), 256, 0, P.s_mm>>>(
+                part, part_sq, sh, M.rows, M.cols, job.st->total(), job.st->total_sq());
+        }
+        MLSK_CUDA(cudaEventRecord(P.mm_done[buf], P.s_mm));
+        P.used[buf] = true;
         launched(3);
         if (idx) {
-            for (int b = 0; b < nb; ++b)
-                if (ks[off + b] < a.probe_k)
-                    MLSK_CUDA(cudaMemcpyAsync(a.probe_host + ks[off + b] * c, idx + (int64_t)b * c,
-                                              sizeof(uint32_t) * c, cudaMemcpyDeviceToHost, s));
+            MLSK_CUDA(cudaStreamSynchronize(P.s_gen));
+            for (int b = 0; b < bt.nb; ++b) {
+                const int64_t k = jks[bt.job][bt.off + b];
+                if (k < a.probe_k)
+                    MLSK_CUDA(cudaMemcpy(job.probe_host + k * c, idx + (int64_t)b * c, sizeof(uint32_t) * c,
+                                         cudaMemcpyDeviceToHost));
+            }
         }
     }
-    MLSK_CUDA(cudaStreamSynchronize(s));
-    st.count += (int64_t)ks.size();
+    for (auto& job : jobs) {
+        int64_t cnt = 0;
+        for (const auto& sg : job.segs) cnt += sg.count;
+        job.st->count += cnt;
+    }
+    MLSK_CUDA(cudaEventRecord(P.end, P.s_mm));
+    MLSK_CUDA(cudaStreamWaitEvent(a.stream, P.end, 0));
 }
 
 }  // namespace mlsk

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -34,6 +35,16 @@ inline void launched(int n = 1) {
     g_launches += n;
     MLSK_CUDA(cudaGetLastError());
 }
+
+// Optional per-kernel timing with CUDA events on the launching stream
+// (mlsk_profile_*); used by bench.py for the roofline's kernel duration.
+struct Prof {
+    const char* name;
+    cudaStream_t stream;
+    cudaEvent_t e0 = nullptr;
+    Prof(const char* n, cudaStream_t s);
+    ~Prof();
+};
 
 // Owning device allocation.
 template <class T>
@@ -129,6 +140,7 @@ std::vector<Segment> plan_segments(int64_t k_begin, int64_t k_end, int rank, int
                                    const LevelState& st);
 
 struct Workspace {
+    std::shared_ptr<void> fused;  // engine-private pipeline state (mlsk_fused.cu)
     DevArray<uint64_t> stream;
     DevArray<int64_t> ks;
     DevArray<uint32_t> idx;
@@ -152,7 +164,19 @@ struct RunArgs {
 
 // Engines.  Both consume segments in order and update `st`.
 void exact_run(const RunArgs& a, const LevelSpec& lv, const std::vector<Segment>& segs, LevelState& st);
-void fused_run(const RunArgs& a, const LevelSpec& lv, const std::vector<Segment>& segs, LevelState& st);
+
+// One level's share of a round for the fused engine.
+struct FusedJob {
+    LevelSpec lv;
+    std::vector<Segment> segs;
+    LevelState* st;
+    uint32_t* probe_host;  // [probe_k][c] or nullptr
+};
+// Runs all jobs of a round as one software pipeline (panel generation of
+// batch i+1 overlapped with the GEMM of batch i on two streams).  Work is
+// ordered after `a.stream`'s prior work and `a.stream` waits for its end;
+// the call returns without a host synchronisation unless a probe is requested.
+void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs);
 bool fused_supported(const Model& M, int target);
 
 // Device-side sketch primitives used by the KAT entry points.

@@ -1,0 +1,151 @@
+// mlsk_probe.cu -- per-kernel event timing (mlsk_profile_*) and the in-run
+// fp64 tensor-pipe peak measurement used as the roofline denominator.
+#include <algorithm>
+#include <cstdio>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "mlsk_internal.h"
+
+namespace mlsk {
+
+namespace {
+
+struct Pending {
+    std::string name;
+    cudaEvent_t e0, e1;
+};
+
+std::mutex g_mu;
+bool g_on = false;
+std::vector<Pending> g_pending;
+std::map<std::string, std::pair<int64_t, double>> g_acc;  // launches, ms
+
+void drain() {
+    for (auto& p : g_pending) {
+        float ms = 0.f;
+        cudaEventSynchronize(p.e1);
+        cudaEventElapsedTime(&ms, p.e0, p.e1);
+        auto& a = g_acc[p.name];
+        a.first += 1;
+        a.second += ms;
+        cudaEventDestroy(p.e0);
+        cudaEventDestroy(p.e1);
+    }
+    g_pending.clear();
+}
+
+// DMMA throughput loop: 8 independent m8n8k4 accumulators per warp
+__global__ void __launch_bounds__(256) k_dmma_peak(double* out, int iters) {
+    double a = threadIdx.x * 1e-3, b = blockIdx.x * 1e-3;
+    double c[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j][0] = c[j][1] = 0.0;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(c[j][0]), "+d"(c[j][1])
+                         : "d"(a), "d"(b));
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc += c[j][0] + c[j][1];
+    if (acc == 12345.678) out[0] = acc;
+}
+
+}  // namespace
+
+Prof::Prof(const char* n, cudaStream_t s) : name(n), stream(s) {
+    if (!g_on) return;
+    cudaEventCreate(&e0);
+    cudaEventRecord(e0, stream);
+}
+
+Prof::~Prof() {
+    if (!e0) return;
+    cudaEvent_t e1;
+    cudaEventCreate(&e1);
+    cudaEventRecord(e1, stream);
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_pending.push_back({name, e0, e1});
+}
+
+int run_guarded(const std::function<void()>& body);
+
+}  // namespace mlsk
+
+using namespace mlsk;
+
+extern "C" {
+
+int mlsk_profile_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_on = on != 0;
+    return 0;
+}
+
+int mlsk_profile_reset(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    drain();
+    g_acc.clear();
+    return 0;
+}
+
+// Entries in name order; returns the number of entries, fills entry `i`.
+int mlsk_profile_read(int i, char* name, int name_len, int64_t* launches, double* ms) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    drain();
+    int k = 0;
+    for (auto& kv : g_acc) {
+        if (k == i) {
+            if (name && name_len > 0) {
+                snprintf(name, name_len, "%s", kv.first.c_str());
+            }
+            if (launches) *launches = kv.second.first;
+            if (ms) *ms = kv.second.second;
+        }
+        ++k;
+    }
+    return (int)g_acc.size();
+}
+
+// Measured fp64 tensor (DMMA) peak in TFLOP/s on `device` (-1 = current).
+double mlsk_measure_fp64_peak(int device) {
+    double result = -1.0;
+    run_guarded([&] {
+        if (device >= 0) MLSK_CUDA(cudaSetDevice(device));
+        int dev = 0, sms = 0;
+        MLSK_CUDA(cudaGetDevice(&dev));
+        MLSK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        DevArray<double> out(1);
+        const int grid = sms * 4, iters = 4096;
+        k_dmma_peak<<<grid, 256>>>(out.p, 64);
+        launched();
+        MLSK_CUDA(cudaDeviceSynchronize());
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        float best = 1e30f;
+        for (int r = 0; r < 5; ++r) {
+            cudaEventRecord(e0);
+            k_dmma_peak<<<grid, 256>>>(out.p, iters);
+            cudaEventRecord(e1);
+            launched();
+            MLSK_CUDA(cudaEventSynchronize(e1));
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            best = std::min(best, ms);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        const double flops = (double)grid * 8 /*warps*/ * iters * 8 /*mma*/ * 512.0;
+        result = flops / (best * 1e-3) / 1e12;
+    });
+    return result;
+}
+
+}  // extern "C"
