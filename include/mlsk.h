@@ -200,6 +200,8 @@ int64_t mlsk_kernel_launch_count(void);
 int mlsk_profile_enable(int on);
 int mlsk_profile_reset(void);
 int mlsk_profile_read(int i, char* name, int name_len, int64_t* launches, double* ms);
+/* Start / end (ms since the last reset) of profiled launch i; returns the count. */
+int mlsk_profile_timeline(int i, char* name, int name_len, double* t0, double* t1);
 /* fp64 tensor-pipe (DMMA) throughput measured on the device, TFLOP/s. */
 double mlsk_measure_fp64_peak(int device);
 

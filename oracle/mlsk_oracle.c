@@ -174,11 +174,8 @@ double orc_log_unit(double x) {
     return hi + lo;
 }
 
-/* (cos, sin)(2 pi u) for u in [0, 1) */
-void orc_sincos_turn(double u, double* c, double* s) {
-    const double v = u * 1024.0;
-    const int iv = (int)v;
-    const double f = v - (double)iv;
+/* (cos, sin)(2 pi (iv + f) / 1024) */
+static void sincos_iv(int iv, double f, double* c, double* s) {
     const int q = iv >> 8, i = iv & 255;
     const double C = T_SINCOS_D[2 * i], S = T_SINCOS_D[2 * i + 1];
     const double d = f * MLSK_SINCOS_D_STEP;
@@ -195,12 +192,22 @@ void orc_sincos_turn(double u, double* c, double* s) {
     }
 }
 
+/* (cos, sin)(2 pi u) for u in [0, 1) with at most 52 fraction bits */
+void orc_sincos_turn(double u, double* c, double* s) {
+    const double v = u * 1024.0;
+    const int iv = (int)v;
+    sincos_iv(iv, v - (double)iv, c, s);
+}
+
+/* 52-bit uniforms from the bit patterns (spec header, box_muller) */
 void orc_box_muller(uint64_t ua, uint64_t ub, double* z0, double* z1) {
-    const double u1 = 1.0 - (double)(ua >> 11) * 0x1.0p-53;
-    const double u2 = (double)(ub >> 11) * 0x1.0p-53;
+    const double u1 = 2.0 - as_double(0x3ff0000000000000ULL | (ua >> 12));
+    const uint64_t f2 = ub >> 12;
+    const int iv = (int)(f2 >> 42);
+    const double f = as_double(0x3ff0000000000000ULL | ((f2 & 0x3ffffffffffULL) << 10)) - 1.0;
     const double rad = sqrt(-2.0 * orc_log_unit(u1));
     double c, s;
-    orc_sincos_turn(u2, &c, &s);
+    sincos_iv(iv, f, &c, &s);
     *z0 = rad * c;
     *z1 = rad * s;
 }

@@ -23,6 +23,7 @@
 //  k_reduce_tiles    deterministic (fixed-order) sum of the per-CTA partials
 //                    into the level accumulators.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "mlsk_internal.h"
@@ -36,7 +37,7 @@ constexpr int BM = 128;       // tile rows
 constexpr int BN = 64;        // tile cols
 constexpr int STAGES = 4;
 constexpr int CONSUMERS = 8;  // consumer warps (4 x 2 of 32 x 32)
-constexpr int GEMM_THREADS = (CONSUMERS + 1) * 32;
+constexpr int GEMM_THREADS = CONSUMERS * 32;  // lane 0 of warp 0 also produces
 constexpr int A_STAGE_BYTES = BM * KC * 8;
 constexpr int B_STAGE_BYTES = BN * KC * 8;
 constexpr int GEN_THREADS = 256;
@@ -60,15 +61,20 @@ __device__ __forceinline__ void load_tables(double2* s_sc, double2* s_lg, const 
 // --------------------------------------------------------- panel generator
 
 // grid-stride over work items (b, kc); each item produces the A chunk
-// (MP x 16) and the weighted B chunk (PP x 16) of sample b.
+// (MP x 16) and the weighted B chunk (PP x 16) of sample b in phases of 128
+// rows / columns, double-buffered in shared memory: 256 threads generate one
+// phase (row pairs share one Philox block) while the previous phase's tile is
+// streamed out with coalesced 16-byte stores.
+constexpr int GROWS = 128;
+
 __global__ void __launch_bounds__(GEN_THREADS)
 k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
                  int64_t cc, double w_fine, double w_coarse, int64_t MP, int64_t PP, int64_t nkc,
                  double* __restrict__ Apan, double* __restrict__ Bpan, uint32_t* __restrict__ idx_out) {
     __shared__ __align__(16) double2 s_sc[256];
     __shared__ __align__(16) double2 s_lg[128];
-    __shared__ __align__(16) double tile[BM * KC];
-    __shared__ int64_t s_j[KC];
+    __shared__ __align__(16) double tile[2][GROWS * KC];
+    __shared__ int s_j[KC];
     __shared__ double s_w[KC];
     load_tables(s_sc, s_lg, M.tab);
     Tables T = M.tab;
@@ -76,19 +82,22 @@ k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restr
     T.log_d = reinterpret_cast<const double*>(s_lg);
     const int tid = threadIdx.x;
     const int64_t items = (int64_t)nb * nkc;
+    const int a_phases = (int)((MP + GROWS - 1) / GROWS), b_phases = (int)((PP + GROWS - 1) / GROWS);
+    const double sd = M.sd;
+    int buf = 0;
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const int b = (int)(it / nkc);
         const int64_t kc = it - (int64_t)b * nkc;
         const uint64_t key = derive_seed(seed, tag, (uint64_t)ks[b]);
-        __syncthreads();  // previous item's readers of s_j / tile are done
+        __syncthreads();  // previous item's readers of s_j are done
         if (tid < KC) {
             const int64_t t = kc * KC + tid;
-            int64_t j = -1;
+            int j = -1;
             double w = 0.0;
             if (t < c) {
                 const u32x4 r = philox((uint32_t)(t >> 1), 0, 0, MLSK_CTR_INDEX, key);
                 const uint32_t ix = index_from_u64((t & 1) ? hi64(r) : lo64(r), M.n, M.log2n, M.cum);
-                j = (int64_t)ix - 1;
+                j = (int)(ix - 1);
                 w = t < cc ? w_coarse : w_fine;
                 if (idx_out) idx_out[(int64_t)b * c + t] = ix;
             }
@@ -96,54 +105,45 @@ k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restr
             s_w[tid] = w;
         }
         __syncthreads();
-        // ---- A: rows in blocks of BM, row pairs share one Philox block
-        for (int64_t rb = 0; rb < MP; rb += BM) {
-            for (int item = tid; item < (BM / 2) * KC; item += GEN_THREADS) {
-                const int rp = item & (BM / 2 - 1), tt = item / (BM / 2);
-                const int64_t row0 = rb + 2 * rp;
-                const int64_t j = s_j[tt];
+        for (int ph = 0; ph < a_phases + b_phases; ++ph) {
+            const bool isA = ph < a_phases;
+            const int64_t rb = (int64_t)(isA ? ph : ph - a_phases) * GROWS;
+            const int64_t lim = isA ? M.m - rb : M.p - rb;  // valid rows / cols
+            const int64_t span = isA ? MP - rb : PP - rb;     // rows / cols in the panel
+            double* tl = tile[buf];
+#pragma unroll 2
+            for (int item = tid; item < (GROWS / 2) * KC; item += GEN_THREADS) {
+                const int rp = item & (GROWS / 2 - 1), tt = item / (GROWS / 2);
+                const int r0 = 2 * rp;
+                const int j = s_j[tt];
                 double v0 = 0.0, v1 = 0.0;
-                if (j >= 0 && row0 < M.m) {
-                    const u32x4 r = philox((uint32_t)j, (uint32_t)(row0 >> 1), 0, MLSK_CTR_A, key);
+                if (j >= 0 && r0 < lim) {
+                    const u32x4 r =
+                        philox((uint32_t)j, (uint32_t)((rb + r0) >> 1), 0, isA ? MLSK_CTR_A : MLSK_CTR_B, key);
                     double z0, z1;
                     box_muller(lo64(r), hi64(r), z0, z1, T);
-                    const double* mt = M.mean_at + j * M.m + row0;
-                    v0 = __dadd_rn(mt[0], __dmul_rn(M.sd, z0));
-                    if (row0 + 1 < M.m) v1 = __dadd_rn(mt[1], __dmul_rn(M.sd, z1));
+                    if (isA) {
+                        const double* mt = M.mean_at + (int64_t)j * M.m + rb + r0;
+                        v0 = __dadd_rn(mt[0], __dmul_rn(sd, z0));
+                        if (r0 + 1 < lim) v1 = __dadd_rn(mt[1], __dmul_rn(sd, z1));
+                    } else {
+                        const double* mb = M.mean_b + (int64_t)j * M.p + rb + r0;
+                        const double w = s_w[tt];
+                        v0 = __dmul_rn(w, __dadd_rn(mb[0], __dmul_rn(sd, z0)));
+                        if (r0 + 1 < lim) v1 = __dmul_rn(w, __dadd_rn(mb[1], __dmul_rn(sd, z1)));
+                    }
                 }
-                tile[tile_slot(2 * rp, tt)] = v0;
-                tile[tile_slot(2 * rp + 1, tt)] = v1;
+                tl[tile_slot(r0, tt)] = v0;
+                tl[tile_slot(r0 + 1, tt)] = v1;
             }
             __syncthreads();
-            double2* dst = reinterpret_cast<double2*>(Apan + (((int64_t)b * nkc + kc) * MP + rb) * KC);
-            const double2* src = reinterpret_cast<const double2*>(tile);
-            for (int i = tid; i < BM * KC / 2; i += GEN_THREADS) dst[i] = src[i];
-            __syncthreads();
-        }
-        // ---- B: cols in blocks of BN, col pairs share one Philox block, w_t folded in
-        for (int64_t cb = 0; cb < PP; cb += BN) {
-            for (int item = tid; item < (BN / 2) * KC; item += GEN_THREADS) {
-                const int qp = item & (BN / 2 - 1), tt = item / (BN / 2);
-                const int64_t col0 = cb + 2 * qp;
-                const int64_t j = s_j[tt];
-                double v0 = 0.0, v1 = 0.0;
-                if (j >= 0 && col0 < M.p) {
-                    const u32x4 r = philox((uint32_t)j, (uint32_t)(col0 >> 1), 0, MLSK_CTR_B, key);
-                    double z0, z1;
-                    box_muller(lo64(r), hi64(r), z0, z1, T);
-                    const double* mb = M.mean_b + j * M.p + col0;
-                    const double w = s_w[tt];
-                    v0 = __dmul_rn(w, __dadd_rn(mb[0], __dmul_rn(M.sd, z0)));
-                    if (col0 + 1 < M.p) v1 = __dmul_rn(w, __dadd_rn(mb[1], __dmul_rn(M.sd, z1)));
-                }
-                tile[tile_slot(2 * qp, tt)] = v0;
-                tile[tile_slot(2 * qp + 1, tt)] = v1;
-            }
-            __syncthreads();
-            double2* dst = reinterpret_cast<double2*>(Bpan + (((int64_t)b * nkc + kc) * PP + cb) * KC);
-            const double2* src = reinterpret_cast<const double2*>(tile);
-            for (int i = tid; i < BN * KC / 2; i += GEN_THREADS) dst[i] = src[i];
-            __syncthreads();
+            double* base = isA ? Apan + (((int64_t)b * nkc + kc) * MP + rb) * KC
+                               : Bpan + (((int64_t)b * nkc + kc) * PP + rb) * KC;
+            const int n2 = (int)((span < GROWS ? span : GROWS) * KC / 2);
+            double2* dst = reinterpret_cast<double2*>(base);
+            const double2* src = reinterpret_cast<const double2*>(tl);
+            for (int i = tid; i < n2; i += GEN_THREADS) dst[i] = src[i];
+            buf ^= 1;  // next phase writes the other tile; no second barrier needed
         }
     }
 }
@@ -183,6 +183,12 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
+}
+
+__device__ __forceinline__ double2 lds128(uint32_t addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
 }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -227,25 +233,32 @@ k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, Gem
     }
     __syncthreads();
 
-    if (warp == CONSUMERS) {
-        // ------------------------------------------------ producer warp
-        if (lane == 0) {
-            for (int64_t it = 0; it < iters; ++it) {
-                const int s = (int)(it % STAGES);
-                const uint32_t ph = (uint32_t)((it / STAGES) & 1);
-                const int64_t b = grp + (it / sh.nkc) * sh.Gs;
-                const int64_t kc = it % sh.nkc;
-                mbar_wait(smem_u32(&bars[STAGES + s]), ph ^ 1);
-                const uint32_t full = smem_u32(&bars[s]);
-                mbar_expect_tx(full, A_STAGE_BYTES + B_STAGE_BYTES);
-                const double* srcA = Apan + ((b * sh.nkc + kc) * sh.MP + (int64_t)tm * BM) * KC;
-                const double* srcB = Bpan + ((b * sh.nkc + kc) * sh.PP + (int64_t)tn * BN) * KC;
-                bulk_g2s(smem_u32(sA + s * (BM * KC)), srcA, A_STAGE_BYTES, full);
-                bulk_g2s(smem_u32(sB + s * (BN * KC)), srcB, B_STAGE_BYTES, full);
-            }
+    // producer state (lane 0 of warp 0): next (sample, chunk) to load
+    const bool producer = threadIdx.x == 0;
+    int p_s = 0;
+    uint32_t p_ph = 0;
+    int64_t p_b = grp, p_kc = 0, p_it = 0;
+    auto produce = [&]() {
+        // load iteration p_it into slot p_s once every warp has released it
+        mbar_wait(smem_u32(&bars[STAGES + p_s]), p_ph ^ 1);
+        const uint32_t full = smem_u32(&bars[p_s]);
+        mbar_expect_tx(full, A_STAGE_BYTES + B_STAGE_BYTES);
+        const double* srcA = Apan + ((p_b * sh.nkc + p_kc) * sh.MP + (int64_t)tm * BM) * KC;
+        const double* srcB = Bpan + ((p_b * sh.nkc + p_kc) * sh.PP + (int64_t)tn * BN) * KC;
+        bulk_g2s(smem_u32(sA + p_s * (BM * KC)), srcA, A_STAGE_BYTES, full);
+        bulk_g2s(smem_u32(sB + p_s * (BN * KC)), srcB, B_STAGE_BYTES, full);
+        if (++p_s == STAGES) {
+            p_s = 0;
+            p_ph ^= 1u;
         }
-        return;
-    }
+        if (++p_kc == sh.nkc) {
+            p_kc = 0;
+            p_b += sh.Gs;
+        }
+        ++p_it;
+    };
+    if (producer)
+        while (p_it < iters && p_it < STAGES - 1) produce();
 
     // ---------------------------------------------------- consumer warps
     const int wi = warp >> 1, wj = warp & 1;
@@ -260,37 +273,56 @@ k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, Gem
         }
     double sq = 0.0;
 
+    const uint32_t full0 = smem_u32(&bars[0]), empty0 = smem_u32(&bars[STAGES]);
+    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+    // per-lane fragment offsets (bytes) inside a stage: rows wi*32 + 8i + gid,
+    // cols wj*32 + 8j + gid, granules (2 tig + h) ^ gid
+    const uint32_t a_off = (uint32_t)((wi * 32 + gid) * KC * 8), b_off = (uint32_t)((wj * 32 + gid) * KC * 8);
+    const uint32_t g0 = (uint32_t)((((2 * tig) ^ gid) << 4)), g1 = (uint32_t)((((2 * tig + 1) ^ gid) << 4));
+    int s = 0;
+    uint32_t ph = 0;
+    int64_t kc = 0;
     for (int64_t it = 0; it < iters; ++it) {
-        const int s = (int)(it % STAGES);
-        const uint32_t ph = (uint32_t)((it / STAGES) & 1);
-        mbar_wait(smem_u32(&bars[s]), ph);
-        const double* a_st = sA + s * (BM * KC);
-        const double* b_st = sB + s * (BN * KC);
+        mbar_wait(full0 + 8 * s, ph);
+        const uint32_t a_st = a_base + s * A_STAGE_BYTES + a_off;
+        const uint32_t b_st = b_base + s * B_STAGE_BYTES + b_off;
+        // all fragments of the stage first (16 x LDS.128), then 64 DMMAs
+        double2 af0[4], bf0[4], af1[4], bf1[4];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            double2 af[4], bf[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int r = wi * 32 + 8 * i + gid;
-                af[i] = *reinterpret_cast<const double2*>(a_st + r * KC + (((2 * tig + h) ^ gid) << 1));
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int q = wj * 32 + 8 * j + gid;
-                bf[j] = *reinterpret_cast<const double2*>(b_st + q * KC + (((2 * tig + h) ^ gid) << 1));
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i].x, bf[j].x);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i].y, bf[j].y);
+        for (int i = 0; i < 4; ++i) {
+            af0[i] = lds128(a_st + i * (8 * KC * 8) + g0);
+            af1[i] = lds128(a_st + i * (8 * KC * 8) + g1);
         }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            bf0[j] = lds128(b_st + j * (8 * KC * 8) + g0);
+            bf1[j] = lds128(b_st + j * (8 * KC * 8) + g1);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af0[i].x, bf0[j].x);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af0[i].y, bf0[j].y);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af1[i].x, bf1[j].x);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af1[i].y, bf1[j].y);
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&bars[STAGES + s]));
-        if ((it % sh.nkc) == sh.nkc - 1) {
+        if (lane == 0) mbar_arrive(empty0 + 8 * s);
+        if (producer && p_it < iters) produce();
+        if (++s == STAGES) {
+            s = 0;
+            ph ^= 1u;
+        }
+        if (++kc == sh.nkc) {
+            kc = 0;
             // sample boundary: fused level epilogue (Y^2 and running sum)
 #pragma unroll
             for (int i = 0; i < 4; ++i)
@@ -318,7 +350,7 @@ k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, Gem
         }
     sq = warp_sum(sq);
     if (lane == 0) s_sq[warp] = sq;
-    asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS * 32));
+    __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
         for (int w = 0; w < CONSUMERS; ++w) t += s_sq[w];
@@ -493,6 +525,16 @@ Pipe& pipe_of(Workspace& ws) {
     return *static_cast<Pipe*>(ws.fused.get());
 }
 
+// MLSK_SERIAL=1 serialises generator and GEMM (diagnostics: per-kernel
+// standalone durations).
+bool serial_mode() {
+    static const bool v = [] {
+        const char* e = getenv("MLSK_SERIAL");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 struct Batch {
     size_t job;
     int64_t off;  // into the job's replication list
@@ -620,12 +662,12 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         }
         // generator: wait until the GEMM that last used this buffer is done
         if (P.used[buf]) MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.mm_done[buf], 0));
-        const int64_t items = (int64_t)bt.nb * nkc;
+        if (serial_mode() && i > 0) MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.mm_done[(i - 1) % NBUF], 0));
         {
             Prof p("gen_panels_f64", P.s_gen);
-            k_gen_panels_f64<<<(int)std::min<int64_t>(items, (int64_t)sms * 4), GEN_THREADS, 0, P.s_gen>>>(
-                M.dm, a.seed, job.lv.tag, P.ks.p + bt.ks_off, bt.nb, c, cc, w_fine, w_coarse, MP, PP, nkc, Apan,
-                Bpan, idx);
+            k_gen_panels_f64<<<(int)std::min<int64_t>((int64_t)bt.nb * nkc, (int64_t)sms * 4), GEN_THREADS, 0,
+                               P.s_gen>>>(M.dm, a.seed, job.lv.tag, P.ks.p + bt.ks_off, bt.nb, c, cc, w_fine, w_coarse,
+                                          MP, PP, nkc, Apan, Bpan, idx);
         }
         MLSK_CUDA(cudaEventRecord(P.gen_done[buf], P.s_gen));
         // GEMM + fused level epilogue + fixed-order reduction

@@ -23,6 +23,12 @@ std::mutex g_mu;
 bool g_on = false;
 std::vector<Pending> g_pending;
 std::map<std::string, std::pair<int64_t, double>> g_acc;  // launches, ms
+cudaEvent_t g_base = nullptr;                              // timeline origin
+struct Span {
+    std::string name;
+    double t0, t1;
+};
+std::vector<Span> g_timeline;
 
 void drain() {
     for (auto& p : g_pending) {
@@ -32,6 +38,12 @@ void drain() {
         auto& a = g_acc[p.name];
         a.first += 1;
         a.second += ms;
+        if (g_base && g_timeline.size() < 100000) {
+            float t0 = 0.f, t1 = 0.f;
+            cudaEventElapsedTime(&t0, g_base, p.e0);
+            cudaEventElapsedTime(&t1, g_base, p.e1);
+            g_timeline.push_back({p.name, t0, t1});
+        }
         cudaEventDestroy(p.e0);
         cudaEventDestroy(p.e1);
     }
@@ -92,7 +104,23 @@ int mlsk_profile_reset(void) {
     std::lock_guard<std::mutex> lk(g_mu);
     drain();
     g_acc.clear();
+    g_timeline.clear();
+    if (!g_base) cudaEventCreate(&g_base);
+    cudaEventRecord(g_base, 0);
+    cudaEventSynchronize(g_base);
     return 0;
+}
+
+// Timeline entry i (launch order of completion draining): returns the count.
+int mlsk_profile_timeline(int i, char* name, int name_len, double* t0, double* t1) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    drain();
+    if (i >= 0 && i < (int)g_timeline.size()) {
+        if (name && name_len > 0) snprintf(name, name_len, "%s", g_timeline[i].name.c_str());
+        if (t0) *t0 = g_timeline[i].t0;
+        if (t1) *t1 = g_timeline[i].t1;
+    }
+    return (int)g_timeline.size();
 }
 
 // Entries in name order; returns the number of entries, fills entry `i`.

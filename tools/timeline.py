@@ -1,0 +1,34 @@
+"""Run a few bench-like rounds and print the per-kernel timeline (diagnostics)."""
+import ctypes as C
+import sys
+
+sys.path.insert(0, ".")
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_1904_00429_b200 import mlsketch as g  # noqa: E402
+from paper_1904_00429_b200._lib import lib  # noqa: E402
+
+L = lib()
+stream = torch.cuda.current_stream()
+opts = g.EstimatorOptions(stream=stream.cuda_stream, engine="fused")
+model = g.gaussian_mean_matrix_model(256, 4096, 256, sd=0.5, data_seed=bench.data_seed())
+sess = g.MlmcSession(model, g.target_identity(), 2, 6, 1, c0=32, options=opts)
+for _ in range(3):
+    sess.run_round(bench.STEP_N)
+torch.cuda.synchronize()
+L.mlsk_profile_reset()
+L.mlsk_profile_enable(1)
+sess.run_round(bench.STEP_N)
+torch.cuda.synchronize()
+L.mlsk_profile_enable(0)
+name = C.create_string_buffer(64)
+t0, t1 = C.c_double(), C.c_double()
+n = L.mlsk_profile_timeline(0, name, 64, C.byref(t0), C.byref(t1))
+rows = []
+for i in range(n):
+    L.mlsk_profile_timeline(i, name, 64, C.byref(t0), C.byref(t1))
+    rows.append((t0.value, t1.value, name.value.decode()))
+rows.sort()
+for a, b, nm in rows:
+    print(f"{a:8.3f} {b:8.3f} {b - a:7.3f}  {nm}")
