@@ -421,7 +421,11 @@ int orc_model_create(const mlsk_model_desc* desc, orc_model** out) {
     m->cols = m->vector ? 1 : m->d.p;
     const int64_t n = m->d.n;
     const int f32 = desc->dtype == MLSK_F32;
-    if (k == MLSK_MODEL_GAUSS_MEAN || k == MLSK_MODEL_STUDENT_T) {
+    if (k == MLSK_MODEL_STUDENT_T && (desc->mean_a || desc->mean_b)) {
+        free(m);
+        return fail(MLSK_EINVAL, "student-t: means are generated from data_seed");
+    }
+    if (k == MLSK_MODEL_GAUSS_MEAN) {
         const int64_t na = m->vector ? n : m->d.m * n;
         const int64_t nb = m->vector ? n : n * m->d.p;
         m->mean_a = (double*)malloc(sizeof(double) * na);
@@ -578,9 +582,9 @@ static double philox_entry(const orc_model* m, uint64_t key, int which, int64_t 
         return mean + m->d.sd * z;
     }
     case MLSK_MODEL_STUDENT_T: {
-        /* t_nu = z0 / sqrt((z1^2 + ... + z_nu^2) / nu), nu = 3: one block = 4 normals */
-        const double mean = which == 0 ? m->mean_a[m->vector ? col : rq * n + col]
-                                       : m->mean_b[m->vector ? col : col * m->cols + rq];
+        /* t_nu = z0 / sqrt((z1^2 + ... + z_nu^2) / nu), nu = 3: one block = 4
+         * normals; the U(lo, hi) mean is generated on the fly (config 5 stores
+         * nothing): element e = row*n + col of A / col*p + q of B */
         uint32_t r[4];
         philox_block(key, (uint32_t)col, (uint32_t)rq, (uint32_t)which, MLSK_CTR_T, r);
         float z[4];
@@ -588,7 +592,14 @@ static double philox_entry(const orc_model* m, uint64_t key, int which, int64_t 
         orc_box_muller_f(r[2], r[3], &z[2], &z[3]);
         const float v = (z[1] * z[1] + z[2] * z[2]) + z[3] * z[3];
         const float t = z[0] / sqrtf(v / 3.0f);
-        return (double)((float)mean + t);
+        const uint64_t e = which == 0 ? (uint64_t)rq * (uint64_t)n + (uint64_t)col
+                                      : (uint64_t)col * (uint64_t)m->cols + (uint64_t)rq;
+        const uint64_t dkey = orc_derive_seed(m->d.data_seed, MLSK_TAG_DATA, (uint64_t)which);
+        uint32_t rd[4];
+        philox_block(dkey, (uint32_t)e, (uint32_t)(e >> 32), 0, MLSK_CTR_DATA, rd);
+        const float flo = (float)m->d.mean_lo, fw = (float)(m->d.mean_hi - m->d.mean_lo);
+        const float mean = flo + fw * ((float)(rd[0] >> 8) * 0x1.0p-24f);
+        return (double)(mean + t);
     }
     case MLSK_MODEL_RFF: {
         /* A[x][col] = sqrt(2/n) cos(w_col . x + b_col); B = A^T */

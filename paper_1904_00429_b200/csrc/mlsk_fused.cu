@@ -456,9 +456,13 @@ int sm_count() {
 
 }  // namespace
 
+bool tc_supported(const Model& M, int target);                                   // mlsk_tc.cu
+void tc_run_round(const RunArgs& a, std::vector<FusedJob>& jobs, cudaStream_t s);  // mlsk_tc.cu
+
 bool fused_supported(const Model& M, int target) {
-    return target == MLSK_TARGET_IDENTITY && M.dm.stream == MLSK_STREAM_PHILOX &&
-           M.dm.kind == MLSK_MODEL_GAUSS_MEAN && M.dm.dtype == MLSK_F64;
+    return (target == MLSK_TARGET_IDENTITY && M.dm.stream == MLSK_STREAM_PHILOX &&
+            M.dm.kind == MLSK_MODEL_GAUSS_MEAN && M.dm.dtype == MLSK_F64) ||
+           tc_supported(M, target);
 }
 
 namespace {
@@ -567,6 +571,15 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
     MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.start, 0));
     MLSK_CUDA(cudaStreamWaitEvent(P.s_mm, P.start, 0));
     P.stage_ks(all, P.s_gen);
+
+    if (tc_supported(M, a.target)) {  // fp32 models: tcgen05 3xTF32 engine
+        MLSK_CUDA(cudaEventRecord(P.staged, P.s_gen));
+        MLSK_CUDA(cudaStreamWaitEvent(P.s_mm, P.staged, 0));
+        tc_run_round(a, jobs, P.s_mm);
+        MLSK_CUDA(cudaEventRecord(P.end, P.s_mm));
+        MLSK_CUDA(cudaStreamWaitEvent(a.stream, P.end, 0));
+        return;
+    }
 
     if (M.vector) {
         // config-1 shape: one warp per replication, no panels

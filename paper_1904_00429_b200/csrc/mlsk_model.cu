@@ -176,7 +176,15 @@ void build_model(Model& M, const mlsk_model_desc* d, cudaStream_t st) {
         MLSK_CUDA(cudaMemcpyAsync(M.paper_b.p, t.data(), sizeof(double) * 1001, cudaMemcpyHostToDevice, st));
         dm.paper_b = M.paper_b.p;
     }
-    if (k == MLSK_MODEL_GAUSS_MEAN || k == MLSK_MODEL_STUDENT_T) {
+    if (k == MLSK_MODEL_STUDENT_T) {
+        // means generated on the fly from the data stream (config 5: nothing stored)
+        if (D.mean_a || D.mean_b) invalid("student-t: means are generated from data_seed");
+        dm.st_key_a = derive_seed(D.data_seed, MLSK_TAG_DATA, 0);
+        dm.st_key_b = derive_seed(D.data_seed, MLSK_TAG_DATA, 1);
+        dm.st_lo = (float)D.mean_lo;
+        dm.st_w = (float)(D.mean_hi - D.mean_lo);
+    }
+    if (k == MLSK_MODEL_GAUSS_MEAN) {
         const int64_t na = M.vector ? D.n : D.m * D.n;
         const int64_t nb = M.vector ? D.n : D.n * D.p;
         const double lo = D.mean_lo, w = D.mean_hi - D.mean_lo;

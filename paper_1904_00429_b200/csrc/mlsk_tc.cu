@@ -1,0 +1,544 @@
+// mlsk_tc.cu -- the fp32 configurations (BASELINE configs 3-5) on the 5th-gen
+// tensor cores: 3xTF32 sampled GEMM with tcgen05.mma, TMEM accumulators and the
+// level epilogue (Y^2, running sum) fused into dedicated epilogue warps.
+//
+// Same fused formulation as the fp64 engine (mlsk_fused.cu): per level-sample
+// Y = sum_t w_t a_t b_t^T with signed weights, K = c.  fp32 accuracy from TF32
+// tensor cores by the 3xTF32 split  a b ~= a_hi b_hi + a_hi b_lo + a_lo b_hi,
+// a_hi = a (the MMA reads the fp32 word and uses its TF32 part), a_lo = a -
+// tf32(a) (exact in fp32) -- three MMAs per K-step into one fp32 accumulator.
+//
+//  k_gen_panels_tf32  sampled indices + the sampled columns of A / rows of B
+//                     (gauss f32, Student-t or random-Fourier features,
+//                     generated on the fly), written as hi / lo K-chunks in the
+//                     UMMA canonical K-major SWIZZLE_128B layout.
+//  k_gemm_tf32x3      persistent CTAs, one 128 x 128 output tile per CTA over a
+//                     strided set of samples.  warp 0: cp.async.bulk producer
+//                     (3-stage mbarrier ring, 64 KB per stage); warp 1: TMEM
+//                     allocation + single-thread tcgen05.mma issue into two
+//                     128-column TMEM accumulators (double-buffered across
+//                     samples); warps 2-5: epilogue (tcgen05.ld, Y^2 into fp64,
+//                     running sum in 128 registers per thread, flushed to an
+//                     fp64 per-CTA partial every 32 samples).
+#include <algorithm>
+#include <cstring>
+
+#include "mlsk_internal.h"
+
+namespace mlsk {
+
+namespace {
+
+constexpr int TBM = 128, TBN = 128, TBK = 32;       // TBK tf32 = 128 bytes per row
+constexpr int TSTAGES = 3;
+constexpr int TTILE = TBM * TBK * 4;                // 16 KB
+constexpr int TSTAGE_BYTES = 4 * TTILE;             // A_hi, A_lo, B_hi, B_lo
+constexpr int TC_THREADS = 192;                     // producer, MMA, 4 epilogue warps
+constexpr int FLUSH = 32;                           // samples per fp32 running-sum flush
+constexpr uint32_t TMEM_COLS = 2 * TBN;             // two accumulators
+constexpr int GEN_T = 256;
+
+// ----------------------------------------------------------------- PTX
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// 32 lanes x 32 consecutive 32-bit columns: lane i of the warp gets row
+// (quadrant*32 + i), columns [col, col + 32)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_128B: 8-row groups 1024 B
+// apart (SBO), version 1 (sm_100), layout type 2.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+    d |= (uint64_t)1 << 16;              // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;    // SBO
+    d |= (uint64_t)1 << 46;              // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+    return d;
+}
+
+// kind::tf32 instruction descriptor: F32 accumulate, TF32 A / B, K-major, M x N
+__host__ __device__ constexpr uint32_t tf32_idesc(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// byte offset of element (r, k) in a 128-row x 32-tf32 SW128 K-major tile
+__device__ __forceinline__ int sw128_off(int r, int k) {
+    return r * 128 + ((((k >> 2) ^ (r & 7)) << 4) | ((k & 3) << 2));
+}
+
+// ---------------------------------------------------------------- entries
+
+__device__ __forceinline__ float tf32_lo(float x) {
+    return __fsub_rn(x, __uint_as_float(__float_as_uint(x) & 0xFFFFE000u));
+}
+
+struct TcModel {
+    DevModel M;
+};
+
+// Student-t(3) entry with an on-the-fly mean: A[row][col] (which = 0) or B[col][row] (which = 1)
+__device__ __forceinline__ float student_t_entry(const TcModel& S, uint64_t key, int64_t col, int64_t rq, int which,
+                                                 const Tables& T) {
+    const u32x4 r = philox((uint32_t)col, (uint32_t)rq, (uint32_t)which, MLSK_CTR_T, key);
+    float z[4];
+    box_muller_f(r.x, r.y, z[0], z[1], T);
+    box_muller_f(r.z, r.w, z[2], z[3], T);
+    const float v = __fadd_rn(__fadd_rn(__fmul_rn(z[1], z[1]), __fmul_rn(z[2], z[2])), __fmul_rn(z[3], z[3]));
+    const float t = __fdiv_rn(z[0], __fsqrt_rn(__fdiv_rn(v, 3.0f)));
+    const uint64_t e = which == 0 ? (uint64_t)rq * (uint64_t)S.M.n + (uint64_t)col
+                                  : (uint64_t)col * (uint64_t)S.M.p + (uint64_t)rq;
+    const float mean = data_mean_f32(which == 0 ? S.M.st_key_a : S.M.st_key_b, e, S.M.st_lo, S.M.st_w);
+    return __fadd_rn(mean, t);
+}
+
+// RFF feature sqrt(2/n) cos(w_col . x_row + b_col) (fp32 dot, accurate cosf)
+__device__ __forceinline__ float rff_entry(const DevModel& M, int64_t col, int64_t row) {
+    float acc = 0.f;
+    const float* x = M.rff_x + row * M.rff_dim;
+    for (int64_t t = 0; t < M.rff_dim; ++t) acc = __fmaf_rn(x[t], M.rff_w[t * M.n + col], acc);
+    return (float)M.rff_scale * cosf(acc + M.rff_b[col]);
+}
+
+// ------------------------------------------------------------ generator
+
+// work item (b, kc): 32 sampled columns; phases of 128 rows of A / cols of B;
+// hi and lo tiles staged in shared memory in the SW128 layout, then copied out.
+__global__ void __launch_bounds__(GEN_T)
+k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
+                  int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc,
+                  float* __restrict__ Ahi, float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
+                  uint32_t* __restrict__ idx_out) {
+    __shared__ __align__(1024) unsigned char thi[TTILE];
+    __shared__ __align__(1024) unsigned char tlo[TTILE];
+    __shared__ __align__(16) float2 s_sc[64];
+    __shared__ __align__(16) float2 s_lg[64];
+    __shared__ int s_j[TBK];
+    __shared__ float s_w[TBK];
+    const DevModel& M = S.M;
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+        s_sc[i] = reinterpret_cast<const float2*>(M.tab.sincos_f)[i];
+        s_lg[i] = reinterpret_cast<const float2*>(M.tab.log_f)[i];
+    }
+    Tables T = M.tab;
+    T.sincos_f = reinterpret_cast<const float*>(s_sc);
+    T.log_f = reinterpret_cast<const float*>(s_lg);
+    const int tid = threadIdx.x;
+    const int64_t items = (int64_t)nb * nkc;
+    const int a_ph = (int)(MP / TBM), b_ph = (int)(PP / TBN);
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int b = (int)(it / nkc);
+        const int64_t kc = it - (int64_t)b * nkc;
+        const uint64_t key = derive_seed(seed, tag, (uint64_t)ks[b]);
+        __syncthreads();
+        if (tid < TBK) {
+            const int64_t t = kc * TBK + tid;
+            int j = -1;
+            float w = 0.f;
+            if (t < c) {
+                const u32x4 r = philox((uint32_t)(t >> 1), 0, 0, MLSK_CTR_INDEX, key);
+                const uint32_t ix = index_from_u64((t & 1) ? hi64(r) : lo64(r), M.n, M.log2n, M.cum);
+                j = (int)(ix - 1);
+                w = t < cc ? w_coarse : w_fine;
+                if (idx_out) idx_out[(int64_t)b * c + t] = ix;
+            }
+            s_j[tid] = j;
+            s_w[tid] = w;
+        }
+        __syncthreads();
+        for (int ph = 0; ph < a_ph + b_ph; ++ph) {
+            const bool isA = ph < a_ph;
+            const int64_t rb = (int64_t)(isA ? ph : ph - a_ph) * TBM;
+            const int64_t lim = isA ? M.m - rb : M.p - rb;
+            if (M.kind == MLSK_MODEL_GAUSS_MEAN) {
+                // one Philox block -> 4 normals for rows 4q..4q+3 of one column
+                for (int item = tid; item < (TBM / 4) * TBK; item += GEN_T) {
+                    const int qd = item & (TBM / 4 - 1), tt = item / (TBM / 4);
+                    const int r0 = 4 * qd;
+                    const int j = s_j[tt];
+                    float v[4] = {0.f, 0.f, 0.f, 0.f};
+                    if (j >= 0 && r0 < lim) {
+                        const u32x4 r = philox((uint32_t)j, (uint32_t)((rb + r0) >> 2), 0,
+                                               isA ? MLSK_CTR_A : MLSK_CTR_B, key);
+                        float z[4];
+                        box_muller_f(r.x, r.y, z[0], z[1], T);
+                        box_muller_f(r.z, r.w, z[2], z[3], T);
+                        const float sd = (float)M.sd;
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            if (r0 + e < lim) {
+                                const float mean = isA ? M.mean_at_f[(int64_t)j * M.m + rb + r0 + e]
+                                                       : M.mean_b_f[(int64_t)j * M.p + rb + r0 + e];
+                                const float x = __fadd_rn(mean, __fmul_rn(sd, z[e]));
+                                v[e] = isA ? x : __fmul_rn(s_w[tt], x);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        *reinterpret_cast<float*>(thi + sw128_off(r0 + e, tt)) = v[e];
+                        *reinterpret_cast<float*>(tlo + sw128_off(r0 + e, tt)) = tf32_lo(v[e]);
+                    }
+                }
+            } else {
+                for (int item = tid; item < TBM * TBK; item += GEN_T) {
+                    const int rr = item & (TBM - 1), tt = item / TBM;
+                    const int j = s_j[tt];
+                    float v = 0.f;
+                    if (j >= 0 && rr < lim) {
+                        float x;
+                        if (M.kind == MLSK_MODEL_STUDENT_T) x = student_t_entry(S, key, j, rb + rr, isA ? 0 : 1, T);
+                        else x = rff_entry(M, j, rb + rr);  // RFF: B = A^T
+                        v = isA ? x : __fmul_rn(s_w[tt], x);
+                    }
+                    *reinterpret_cast<float*>(thi + sw128_off(rr, tt)) = v;
+                    *reinterpret_cast<float*>(tlo + sw128_off(rr, tt)) = tf32_lo(v);
+                }
+            }
+            __syncthreads();
+            const int64_t off = (((int64_t)b * nkc + kc) * (isA ? MP : PP) + rb) * TBK;
+            float4* dh = reinterpret_cast<float4*>((isA ? Ahi : Bhi) + off);
+            float4* dl = reinterpret_cast<float4*>((isA ? Alo : Blo) + off);
+            const float4* sh = reinterpret_cast<const float4*>(thi);
+            const float4* sl = reinterpret_cast<const float4*>(tlo);
+            for (int i = tid; i < TTILE / 16; i += GEN_T) {
+                dh[i] = sh[i];
+                dl[i] = sl[i];
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// --------------------------------------------------------------- GEMM
+
+struct TcShape {
+    int nb;
+    int64_t nkc;
+    int64_t MP, PP;
+    int T, Gs, tiles_n;
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, const float* __restrict__ Bhi,
+              const float* __restrict__ Blo, TcShape sh, double* __restrict__ part, double* __restrict__ part_sq) {
+    extern __shared__ __align__(1024) unsigned char dsm[];
+    // 1024-byte aligned stage ring (SW128 atoms)
+    unsigned char* ring = dsm + ((1024 - (smem_addr(dsm) & 1023)) & 1023);
+    __shared__ __align__(8) uint64_t bars[2 * TSTAGES + 4];  // full, empty, tmem_full[2], tmem_empty[2]
+    __shared__ uint32_t s_tmem;
+    __shared__ double s_sq[4];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = blockIdx.x;
+    const int tile = g % sh.T, grp = g / sh.T;
+    const int tm = tile / sh.tiles_n, tn = tile % sh.tiles_n;
+    const int my_samples = grp < sh.nb ? (sh.nb - 1 - grp) / sh.Gs + 1 : 0;
+    const int64_t iters = (int64_t)my_samples * sh.nkc;
+
+    const uint32_t full0 = smem_addr(&bars[0]), empty0 = smem_addr(&bars[TSTAGES]);
+    const uint32_t tfull0 = smem_addr(&bars[2 * TSTAGES]), tempty0 = smem_addr(&bars[2 * TSTAGES + 2]);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TSTAGES; ++s) {
+            bar_init(full0 + 8 * s, 1);
+            bar_init(empty0 + 8 * s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            bar_init(tfull0 + 8 * a, 1);
+            bar_init(tempty0 + 8 * a, 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&s_tmem)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    if (warp == 0) {
+        // --------------------------------------------------- producer
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            int64_t b = grp, kc = 0;
+            for (int64_t it = 0; it < iters; ++it) {
+                bar_wait(empty0 + 8 * s, ph ^ 1);
+                const uint32_t full = full0 + 8 * s;
+                bar_expect_tx(full, TSTAGE_BYTES);
+                const int64_t oa = ((b * sh.nkc + kc) * sh.MP + (int64_t)tm * TBM) * TBK;
+                const int64_t ob = ((b * sh.nkc + kc) * sh.PP + (int64_t)tn * TBN) * TBK;
+                const uint32_t st = smem_addr(ring + s * TSTAGE_BYTES);
+                bulk_load(st, Ahi + oa, TTILE, full);
+                bulk_load(st + TTILE, Alo + oa, TTILE, full);
+                bulk_load(st + 2 * TTILE, Bhi + ob, TTILE, full);
+                bulk_load(st + 3 * TTILE, Blo + ob, TTILE, full);
+                if (++s == TSTAGES) { s = 0; ph ^= 1; }
+                if (++kc == sh.nkc) { kc = 0; b += sh.Gs; }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc = tf32_idesc(TBM, TBN);
+            int s = 0;
+            uint32_t ph = 0;
+            int64_t kc = 0;
+            int abuf = 0;
+            uint32_t aph[2] = {0, 0};
+            for (int64_t it = 0; it < iters; ++it) {
+                if (kc == 0) {
+                    bar_wait(tempty0 + 8 * abuf, aph[abuf] ^ 1);  // epilogue released this accumulator
+                    tc_fence_after();
+                }
+                bar_wait(full0 + 8 * s, ph);
+                tc_fence_after();
+                const uint32_t st = smem_addr(ring + s * TSTAGE_BYTES);
+                const uint32_t dcol = tmem + (uint32_t)abuf * TBN;
+#pragma unroll
+                for (int kk = 0; kk < TBK / 8; ++kk) {
+                    const uint64_t ah = sw128_desc(st + kk * 32), al = sw128_desc(st + TTILE + kk * 32);
+                    const uint64_t bh = sw128_desc(st + 2 * TTILE + kk * 32), bl = sw128_desc(st + 3 * TTILE + kk * 32);
+                    tc_mma_tf32(dcol, ah, bh, idesc, (kc > 0 || kk > 0) ? 1u : 0u);
+                    tc_mma_tf32(dcol, ah, bl, idesc, 1u);
+                    tc_mma_tf32(dcol, al, bh, idesc, 1u);
+                }
+                tc_commit(empty0 + 8 * s);  // smem stage free once these MMAs complete
+                if (++s == TSTAGES) { s = 0; ph ^= 1; }
+                if (++kc == sh.nkc) {
+                    kc = 0;
+                    tc_commit(tfull0 + 8 * abuf);  // accumulator complete
+                    aph[abuf] ^= 1;
+                    abuf ^= 1;
+                }
+            }
+        }
+    } else {
+        // --------------------------------------------------- epilogue
+        const int q = warp & 3;               // TMEM lane quadrant of this warp
+        const int row = q * 32 + lane;        // tile row owned by this thread
+        float S[TBN];
+#pragma unroll
+        for (int i = 0; i < TBN; ++i) S[i] = 0.f;
+        double sq = 0.0;
+        double* out = part + (int64_t)g * (TBM * TBN) + (int64_t)row * TBN;
+        int abuf = 0;
+        uint32_t aph[2] = {0, 0};
+        for (int smp = 0; smp < my_samples; ++smp) {
+            bar_wait(tfull0 + 8 * abuf, aph[abuf]);
+            tc_fence_after();
+            float ssq = 0.f;
+#pragma unroll
+            for (int ch = 0; ch < TBN / 32; ++ch) {
+                float y[32];
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * TBN + ch * 32), y);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    ssq = __fmaf_rn(y[i], y[i], ssq);
+                    S[ch * 32 + i] = __fadd_rn(S[ch * 32 + i], y[i]);
+                }
+            }
+            sq += (double)ssq;
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(tempty0 + 8 * abuf);
+            aph[abuf] ^= 1;
+            abuf ^= 1;
+            if ((smp + 1) % FLUSH == 0 || smp + 1 == my_samples) {
+#pragma unroll
+                for (int i = 0; i < TBN; ++i) {
+                    out[i] += (double)S[i];
+                    S[i] = 0.f;
+                }
+            }
+        }
+        sq = warp_sum(sq);
+        if (lane == 0) s_sq[q] = sq;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) part_sq[g] = (s_sq[0] + s_sq[1]) + (s_sq[2] + s_sq[3]);
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+}
+
+__global__ void k_reduce_tiles_tc(const double* __restrict__ part, const double* __restrict__ part_sq, TcShape sh,
+                                  int64_t rows, int64_t cols, double* __restrict__ total,
+                                  double* __restrict__ total_sq) {
+    const int64_t cells = rows * cols;
+    for (int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cell < cells;
+         cell += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = cell / cols, q = cell - r * cols;
+        const int tile = (int)((r / TBM) * sh.tiles_n + q / TBN);
+        const int64_t off = (r % TBM) * TBN + (q % TBN);
+        double acc = 0.0;
+        for (int grp = 0; grp < sh.Gs; ++grp) acc += part[(int64_t)(grp * sh.T + tile) * (TBM * TBN) + off];
+        total[cell] += acc;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        double acc = 0.0;
+        for (int g = 0; g < sh.T * sh.Gs; ++g) acc += part_sq[g];
+        *total_sq += acc;
+    }
+}
+
+int sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+}  // namespace
+
+bool tc_supported(const Model& M, int target) {
+    return target == MLSK_TARGET_IDENTITY && M.dm.stream == MLSK_STREAM_PHILOX && !M.vector &&
+           M.dm.dtype == MLSK_F32 &&
+           (M.dm.kind == MLSK_MODEL_GAUSS_MEAN || M.dm.kind == MLSK_MODEL_STUDENT_T || M.dm.kind == MLSK_MODEL_RFF);
+}
+
+// Runs the jobs (levels) of a round on the tensor-core engine; same contract
+// as fused_run_round (ordered after a.stream, a.stream waits for the end).
+void tc_run_round(const RunArgs& a, std::vector<FusedJob>& jobs, cudaStream_t s) {
+    const Model& M = *a.model;
+    Workspace& ws = *a.ws;
+    const int nsm = sms();
+    const int64_t MP = (M.rows + TBM - 1) / TBM * TBM;
+    const int64_t PP = (M.cols + TBN - 1) / TBN * TBN;
+    const int tiles_n = (int)(PP / TBN);
+    const int T = (int)(MP / TBM) * tiles_n;
+    const int Gs = std::max(1, nsm / T);
+    const double n = (double)M.desc.n;
+
+    TcModel S{};
+    S.M = M.dm;
+    static bool attr = false;
+    const int smem = TSTAGES * TSTAGE_BYTES + 1024;
+    if (!attr) {
+        MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    ws.partial.ensure((size_t)T * Gs * (TBM * TBN) + (size_t)T * Gs);
+    double* part = ws.partial.p;
+    double* part_sq = part + (size_t)T * Gs * (TBM * TBN);
+    const int64_t budget = int64_t(1) << 31;  // panel bytes per batch (hi + lo, A + B)
+
+    for (auto& job : jobs) {
+        std::vector<int64_t> ks;
+        for (const auto& sg : job.segs)
+            for (int64_t k = 0; k < sg.count; ++k) ks.push_back(sg.k0 + k);
+        if (ks.empty()) continue;
+        const int64_t c = job.lv.c, cc = job.lv.cc;
+        const int64_t nkc = (c + TBK - 1) / TBK;
+        const int64_t per = (MP + PP) * nkc * TBK * 8;
+        int64_t max_nb = std::max<int64_t>(1, budget / per);
+        if (max_nb > Gs) max_nb = max_nb / Gs * Gs;
+        const float w_fine = (float)(n / (double)c);
+        const float w_coarse = cc > 0 ? (float)(n / (double)c - n / (double)cc) : w_fine;
+        for (size_t off = 0; off < ks.size(); off += (size_t)max_nb) {
+            const int nb = (int)std::min<int64_t>(max_nb, (int64_t)ks.size() - (int64_t)off);
+            ws.ks.ensure(nb);
+            MLSK_CUDA(cudaMemcpyAsync(ws.ks.p, ks.data() + off, sizeof(int64_t) * nb, cudaMemcpyHostToDevice, s));
+            const size_t na = (size_t)nb * nkc * MP * TBK, nbp = (size_t)nb * nkc * PP * TBK;
+            ws.panel_af.ensure(2 * na);
+            ws.panel_bf.ensure(2 * nbp);
+            float *Ahi = ws.panel_af.p, *Alo = Ahi + na, *Bhi = ws.panel_bf.p, *Blo = Bhi + nbp;
+            uint32_t* idx = nullptr;
+            if (job.probe_host) {
+                ws.idx.ensure((size_t)nb * c);
+                idx = ws.idx.p;
+            }
+            {
+                Prof p("gen_panels_tf32", s);
+                k_gen_panels_tf32<<<(int)std::min<int64_t>((int64_t)nb * nkc, (int64_t)nsm * 8), GEN_T, 0, s>>>(
+                    S, a.seed, job.lv.tag, ws.ks.p, nb, c, cc, w_fine, w_coarse, MP, PP, nkc, Ahi, Alo, Bhi, Blo,
+                    idx);
+            }
+            MLSK_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * (size_t)T * Gs * (TBM * TBN), s));
+            TcShape sh{nb, nkc, MP, PP, T, Gs, tiles_n};
+            {
+                Prof p("gemm_tf32x3", s);
+                k_gemm_tf32x3<<<T * Gs, TC_THREADS, smem, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq);
+            }
+            {
+                Prof p("reduce_tiles_tc", s);
+                const int64_t cells = M.rows * M.cols;
+                k_reduce_tiles_tc<<<(int)std::min<int64_t>((cells + 255) / 256, (int64_t)nsm * 8), 256, 0, s>>>(
+                    part, part_sq, sh, M.rows, M.cols, job.st->total(), job.st->total_sq());
+            }
+            launched(3);
+            if (idx) {
+                MLSK_CUDA(cudaStreamSynchronize(s));
+                for (int b = 0; b < nb; ++b)
+                    if (ks[off + b] < a.probe_k)
+                        MLSK_CUDA(cudaMemcpy(job.probe_host + ks[off + b] * c, idx + (int64_t)b * c,
+                                             sizeof(uint32_t) * c, cudaMemcpyDeviceToHost));
+            }
+        }
+        job.st->count += (int64_t)ks.size();
+        MLSK_CUDA(cudaStreamSynchronize(s));  // host ks vector reused per job
+    }
+}
+
+}  // namespace mlsk

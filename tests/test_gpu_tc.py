@@ -1,0 +1,61 @@
+"""fp32 configurations on the tcgen05 3xTF32 engine vs the exact-order
+engine (fp64 arithmetic on the same fp32 draws) and the CPU oracle.
+Tolerance (BASELINE.json north_star): 1e-5 relative, Frobenius norm."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+TOL32 = 1e-5
+MASTER = 20260823
+
+
+def frob_rel(a, b):
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def check(rf, re_, tol=TOL32):
+    for sf, se in zip(rf.per_level, re_.per_level):
+        assert sf.replication_count == se.replication_count
+        assert frob_rel(sf.sum, se.sum) <= tol, (sf.level, frob_rel(sf.sum, se.sum))
+        assert abs(sf.sum_of_squares - se.sum_of_squares) <= tol * se.sum_of_squares
+
+
+def models(g):
+    f32 = 1
+    return {
+        "gauss_f32": g.gaussian_mean_matrix_model(256, 4096, 384, sd=1.0, mean_lo=-1.0, mean_hi=1.0, data_seed=7,
+                                                  dtype=f32),
+        "student_t": g.student_t_matrix_model(256, 8192, 128, data_seed=9),
+        "rff": g.rff_gram_model(256, 4096, dim=64, sigma=4.0, data_seed=11),
+    }
+
+
+@pytest.mark.parametrize("name", ["gauss_f32", "student_t", "rff"])
+def test_tc_engine_vs_exact(gpu, name):
+    model = models(gpu)[name]
+    plan = gpu.LevelPlan(2, 2, [37, 20, 9], c0=64)
+    rf = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
+    re_ = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="exact"))
+    check(rf, re_)
+
+
+def test_tc_gauss_vs_oracle(gpu, oracle):
+    model = gpu.gaussian_mean_matrix_model(128, 1024, 128, sd=1.0, mean_lo=-1.0, mean_hi=1.0, data_seed=3, dtype=1)
+    plan = gpu.LevelPlan(2, 1, [5, 3], c0=64)
+    rf = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
+    o = oracle.OracleModel(model.desc()).mlmc(2, 64, [5, 3], MASTER)
+    for l, st in enumerate(rf.per_level):
+        assert frob_rel(st.sum, o.level_sum[l]) <= TOL32
+        assert abs(st.sum_of_squares - o.level_sumsq[l]) <= TOL32 * o.level_sumsq[l]
+
+
+def test_tc_probe_indices_match_exact(gpu):
+    model = models(gpu)["gauss_f32"]
+    plan = gpu.LevelPlan(2, 1, [4, 3], c0=64)
+    seen = {"fused": [], "exact": []}
+    for eng in seen:
+        gpu.mlmc_matmul(model, gpu.target_identity(), plan, 5,
+                        gpu.EstimatorOptions(engine=eng, probe=lambda l, k, f, c, e=eng: seen[e].append((l, k, f))))
+    assert seen["fused"] == seen["exact"] and len(seen["fused"]) == 3
