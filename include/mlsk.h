@@ -99,7 +99,10 @@ typedef struct mlsk_plan {
 typedef struct mlsk_exec_opts {
     int32_t device;      /* CUDA ordinal, -1 = current device */
     int32_t engine;      /* MLSK_ENGINE_* */
-    void* stream;        /* cudaStream_t to run on, NULL = library stream */
+    void* stream;        /* cudaStream_t to order the work on; NULL = a library stream
+                            and every call returns only when its work is done.  With
+                            a caller stream, mlsk_session_run_round returns once the
+                            round is enqueued (results ordered on that stream). */
     int32_t rank;        /* sample sharding: 64-sample chunk q runs on rank q % world */
     int32_t world;       /* 1 for a single GPU */
     int64_t probe_k;     /* coupling probe: dump index sets of the first probe_k
@@ -204,6 +207,8 @@ int mlsk_profile_read(int i, char* name, int name_len, int64_t* launches, double
 int mlsk_profile_timeline(int i, char* name, int name_len, double* t0, double* t1);
 /* fp64 tensor-pipe (DMMA) throughput measured on the device, TFLOP/s. */
 double mlsk_measure_fp64_peak(int device);
+/* Dense TF32 tcgen05 throughput (M=128, N=n, one CTA per SM), TFLOP/s. */
+double mlsk_measure_tf32_peak(int device, int n);
 
 #ifdef __cplusplus
 }

@@ -62,6 +62,8 @@ def lib():
     L.mlsk_profile_timeline.argtypes = [C.c_int, C.c_char_p, C.c_int, _P(C.c_double), _P(C.c_double)]
     L.mlsk_measure_fp64_peak.restype = C.c_double
     L.mlsk_measure_fp64_peak.argtypes = [C.c_int]
+    L.mlsk_measure_tf32_peak.restype = C.c_double
+    L.mlsk_measure_tf32_peak.argtypes = [C.c_int, C.c_int]
     _lib = L
     return L
 

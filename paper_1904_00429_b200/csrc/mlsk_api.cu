@@ -349,6 +349,9 @@ int mlsk_session_run_round(mlsk_session* s, const int64_t* dN) {
             s->next_k[l] += dN[l];
         }
         s->R.run(items, s->ex->stream, 0);
+        // without a caller stream the call is synchronous; with one, the round is
+        // ordered on that stream and the call returns once it is enqueued
+        if (s->ex->owns) MLSK_CUDA(cudaStreamSynchronize(s->ex->stream));
     });
 }
 

@@ -110,27 +110,33 @@ k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restr
             const int64_t rb = (int64_t)(isA ? ph : ph - a_phases) * GROWS;
             const int64_t lim = isA ? M.m - rb : M.p - rb;  // valid rows / cols
             const int64_t span = isA ? MP - rb : PP - rb;     // rows / cols in the panel
+            const bool pair_aligned = ((isA ? M.m : M.p) & 1) == 0;  // 16-byte mean pairs
             double* tl = tile[buf];
 #pragma unroll 2
+            // lanes span row pairs of one column: coalesced mean loads
             for (int item = tid; item < (GROWS / 2) * KC; item += GEN_THREADS) {
                 const int rp = item & (GROWS / 2 - 1), tt = item / (GROWS / 2);
                 const int r0 = 2 * rp;
                 const int j = s_j[tt];
                 double v0 = 0.0, v1 = 0.0;
                 if (j >= 0 && r0 < lim) {
+                    // issue the mean loads first so their latency hides behind the RNG
+                    const double* mp = isA ? M.mean_at + (int64_t)j * M.m + rb + r0
+                                           : M.mean_b + (int64_t)j * M.p + rb + r0;
+                    const bool pair = r0 + 1 < lim;
+                    double2 mv;
+                    if (pair && pair_aligned) mv = __ldg(reinterpret_cast<const double2*>(mp));
+                    else mv = make_double2(__ldg(mp), pair ? __ldg(mp + 1) : 0.0);
                     const u32x4 r =
                         philox((uint32_t)j, (uint32_t)((rb + r0) >> 1), 0, isA ? MLSK_CTR_A : MLSK_CTR_B, key);
                     double z0, z1;
                     box_muller(lo64(r), hi64(r), z0, z1, T);
-                    if (isA) {
-                        const double* mt = M.mean_at + (int64_t)j * M.m + rb + r0;
-                        v0 = __dadd_rn(mt[0], __dmul_rn(sd, z0));
-                        if (r0 + 1 < lim) v1 = __dadd_rn(mt[1], __dmul_rn(sd, z1));
-                    } else {
-                        const double* mb = M.mean_b + (int64_t)j * M.p + rb + r0;
+                    v0 = __dadd_rn(mv.x, __dmul_rn(sd, z0));
+                    if (pair) v1 = __dadd_rn(mv.y, __dmul_rn(sd, z1));
+                    if (!isA) {
                         const double w = s_w[tt];
-                        v0 = __dmul_rn(w, __dadd_rn(mb[0], __dmul_rn(sd, z0)));
-                        if (r0 + 1 < lim) v1 = __dmul_rn(w, __dadd_rn(mb[1], __dmul_rn(sd, z1)));
+                        v0 = __dmul_rn(w, v0);
+                        v1 = __dmul_rn(w, v1);
                     }
                 }
                 tl[tile_slot(r0, tt)] = v0;
@@ -457,7 +463,6 @@ int sm_count() {
 }  // namespace
 
 bool tc_supported(const Model& M, int target);                                   // mlsk_tc.cu
-void tc_run_round(const RunArgs& a, std::vector<FusedJob>& jobs, cudaStream_t s);  // mlsk_tc.cu
 
 bool fused_supported(const Model& M, int target) {
     return (target == MLSK_TARGET_IDENTITY && M.dm.stream == MLSK_STREAM_PHILOX &&
@@ -466,6 +471,67 @@ bool fused_supported(const Model& M, int target) {
 }
 
 namespace {
+
+class F64Engine final : public PanelEngine {
+   public:
+    F64Engine(const Model& M, Workspace& ws) : M_(M), ws_(ws) {
+        nsm_ = sm_count();
+        MP_ = (M.rows + BM - 1) / BM * BM;
+        PP_ = (M.cols + BN - 1) / BN * BN;
+        tiles_n_ = (int)(PP_ / BN);
+        T_ = (int)(MP_ / BM) * tiles_n_;
+        Gs_ = std::max(1, nsm_ / T_);
+        smem_ = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 2 * STAGES * 8;
+        static bool attr = false;
+        if (!attr) {
+            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+            attr = true;
+        }
+        ws_.partial.ensure((size_t)T_ * Gs_ * (BM * BN) + (size_t)T_ * Gs_);
+    }
+    int64_t panel_bytes(int64_t c) const override { return (MP_ + PP_) * nkc(c) * KC * 8; }
+    int64_t group_size() const override { return Gs_; }
+    void gen(cudaStream_t s, uint64_t seed, uint64_t tag, const int64_t* ks, int nb, int64_t c, int64_t cc,
+             double w_fine, double w_coarse, void* panels, uint32_t* idx) override {
+        const int64_t k = nkc(c);
+        double* Apan = static_cast<double*>(panels);
+        double* Bpan = Apan + (size_t)nb * k * MP_ * KC;
+        Prof p("gen_panels_f64", s);
+        k_gen_panels_f64<<<(int)std::min<int64_t>((int64_t)nb * k, (int64_t)nsm_ * 4), GEN_THREADS, 0, s>>>(
+            M_.dm, seed, tag, ks, nb, c, cc, w_fine, w_coarse, MP_, PP_, k, Apan, Bpan, idx);
+        launched();
+    }
+    void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, LevelState& st) override {
+        const int64_t k = nkc(c);
+        const double* Apan = static_cast<const double*>(panels);
+        const double* Bpan = Apan + (size_t)nb * k * MP_ * KC;
+        double* part = ws_.partial.p;
+        double* part_sq = part + (size_t)T_ * Gs_ * (BM * BN);
+        GemmShape sh{nb, k, MP_, PP_, T_, Gs_, tiles_n_};
+        {
+            Prof p("gemm_f64", s);
+            k_gemm_f64<<<T_ * Gs_, GEMM_THREADS, smem_, s>>>(Apan, Bpan, sh, part, part_sq);
+        }
+        const int64_t cells = M_.rows * M_.cols;
+        {
+            Prof p("reduce_tiles", s);
+            k_reduce_tiles<<<(int)std::min<int64_t>((cells + 255) / 256, (int64_t)nsm_ * 8), 256, 0, s>>>(
+                part, part_sq, sh, M_.rows, M_.cols, st.total(), st.total_sq());
+        }
+        launched(2);
+    }
+
+   private:
+    static int64_t nkc(int64_t c) { return (c + KC - 1) / KC; }
+    const Model& M_;
+    Workspace& ws_;
+    int nsm_, T_, Gs_, tiles_n_, smem_;
+    int64_t MP_, PP_;
+};
+
+std::unique_ptr<PanelEngine> make_f64_engine(const Model& M, Workspace& ws) {
+    return std::unique_ptr<PanelEngine>(new F64Engine(M, ws));
+}
 
 constexpr int NBUF = 3;  // panel buffers in flight (gen i+1, i+2 while GEMM i)
 
@@ -482,6 +548,8 @@ struct Pipe {
     size_t ks_cap = 0;
     DevArray<double> part;
     bool staged_pending = false;
+    std::unique_ptr<PanelEngine> engine;
+    const Model* engine_model = nullptr;
     Pipe() {
         int lo = 0, hi = 0;
         MLSK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -566,20 +634,10 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         all.insert(all.end(), jks[j].begin(), jks[j].end());
     }
     if (all.empty()) return;
-    const bool probing = a.probe_k > 0;
     MLSK_CUDA(cudaEventRecord(P.start, a.stream));
     MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.start, 0));
     MLSK_CUDA(cudaStreamWaitEvent(P.s_mm, P.start, 0));
     P.stage_ks(all, P.s_gen);
-
-    if (tc_supported(M, a.target)) {  // fp32 models: tcgen05 3xTF32 engine
-        MLSK_CUDA(cudaEventRecord(P.staged, P.s_gen));
-        MLSK_CUDA(cudaStreamWaitEvent(P.s_mm, P.staged, 0));
-        tc_run_round(a, jobs, P.s_mm);
-        MLSK_CUDA(cudaEventRecord(P.end, P.s_mm));
-        MLSK_CUDA(cudaStreamWaitEvent(a.stream, P.end, 0));
-        return;
-    }
 
     if (M.vector) {
         // config-1 shape: one warp per replication, no panels
@@ -624,20 +682,21 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         return;
     }
 
-    // ---- matrix path: batches of replications, software-pipelined
-    const int64_t MP = (M.rows + BM - 1) / BM * BM;
-    const int64_t PP = (M.cols + BN - 1) / BN * BN;
-    const int tiles_n = (int)(PP / BN);
-    const int T = (int)(MP / BM) * tiles_n;
-    const int Gs = std::max(1, sms / T);
+    // ---- matrix path: batches of replications, software-pipelined over a
+    // panel engine (fp64 DMMA or the tcgen05 3xTF32 engine for fp32 models)
+    if (!P.engine || P.engine_model != &M) {
+        P.engine = tc_supported(M, a.target) ? make_tc_engine(M, ws) : make_f64_engine(M, ws);
+        P.engine_model = &M;
+    }
+    PanelEngine& E = *P.engine;
+    const int64_t Gs = E.group_size();
     const int64_t budget = int64_t(384) << 20;  // panel bytes per batch (x NBUF in flight)
 
     std::vector<Batch> batches;
     int64_t max_panel = 0;
     for (size_t j = 0; j < jobs.size(); ++j) {
-        const int64_t nkc = (jobs[j].lv.c + KC - 1) / KC;
-        const int64_t per = (MP + PP) * nkc * KC;
-        int64_t max_nb = std::max<int64_t>(1, budget / (per * 8));
+        const int64_t per = E.panel_bytes(jobs[j].lv.c);
+        int64_t max_nb = std::max<int64_t>(1, budget / per);
         if (max_nb > Gs) max_nb = max_nb / Gs * Gs;
         const int64_t total = (int64_t)jks[j].size();
         for (int64_t off = 0; off < total; off += max_nb) {
@@ -646,28 +705,16 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
             max_panel = std::max(max_panel, nb * per);
         }
     }
-    for (int i = 0; i < NBUF; ++i) P.panels[i].ensure((size_t)max_panel);
-    P.part.ensure((size_t)T * Gs * (BM * BN) + (size_t)T * Gs);
-    double* part = P.part.p;
-    double* part_sq = P.part.p + (size_t)T * Gs * (BM * BN);
-
-    static bool attr_set = false;
-    const int smem = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 2 * STAGES * 8;
-    if (!attr_set) {
-        MLSK_CUDA(cudaFuncSetAttribute(k_gemm_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr_set = true;
-    }
+    for (int i = 0; i < NBUF; ++i) P.panels[i].ensure((size_t)(max_panel + 7) / 8);
 
     for (size_t i = 0; i < batches.size(); ++i) {
         const Batch& bt = batches[i];
         FusedJob& job = jobs[bt.job];
         const int64_t c = job.lv.c, cc = job.lv.cc;
-        const int64_t nkc = (c + KC - 1) / KC;
         const double w_fine = n / (double)c;                                 // n/c
         const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;  // n/c - n/cc on the prefix
         const int buf = (int)(i % NBUF);
-        double* Apan = P.panels[buf].p;
-        double* Bpan = Apan + (size_t)bt.nb * nkc * MP * KC;
+        void* panels = P.panels[buf].p;
         uint32_t* idx = nullptr;
         if (job.probe_host) {
             P.idx[buf].ensure((size_t)bt.nb * c);
@@ -676,29 +723,13 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         // generator: wait until the GEMM that last used this buffer is done
         if (P.used[buf]) MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.mm_done[buf], 0));
         if (serial_mode() && i > 0) MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.mm_done[(i - 1) % NBUF], 0));
-        {
-            Prof p("gen_panels_f64", P.s_gen);
-            k_gen_panels_f64<<<(int)std::min<int64_t>((int64_t)bt.nb * nkc, (int64_t)sms * 4), GEN_THREADS, 0,
-                               P.s_gen>>>(M.dm, a.seed, job.lv.tag, P.ks.p + bt.ks_off, bt.nb, c, cc, w_fine, w_coarse,
-                                          MP, PP, nkc, Apan, Bpan, idx);
-        }
+        E.gen(P.s_gen, a.seed, job.lv.tag, P.ks.p + bt.ks_off, bt.nb, c, cc, w_fine, w_coarse, panels, idx);
         MLSK_CUDA(cudaEventRecord(P.gen_done[buf], P.s_gen));
         // GEMM + fused level epilogue + fixed-order reduction
         MLSK_CUDA(cudaStreamWaitEvent(P.s_mm, P.gen_done[buf], 0));
-        GemmShape sh{bt.nb, nkc, MP, PP, T, Gs, tiles_n};
-        {
-            Prof p("gemm_f64", P.s_mm);
-            k_gemm_f64<<<T * Gs, GEMM_THREADS, smem, P.s_mm>>>(Apan, Bpan, sh, part, part_sq);
-        }
-        const int64_t cells = M.rows * M.cols;
-        {
-            Prof p("reduce_tiles", P.s_mm);
-            k_reduce_tiles<<<(int)std::min<int64_t>((cells + 255) / 256, (int64_t)sms * 8), 256, 0, P.s_mm>>>(
-                part, part_sq, sh, M.rows, M.cols, job.st->total(), job.st->total_sq());
-        }
+        E.gemm(P.s_mm, panels, bt.nb, c, *job.st);
         MLSK_CUDA(cudaEventRecord(P.mm_done[buf], P.s_mm));
         P.used[buf] = true;
-        launched(3);
         if (idx) {
             MLSK_CUDA(cudaStreamSynchronize(P.s_gen));
             for (int b = 0; b < bt.nb; ++b) {

@@ -172,6 +172,18 @@ struct FusedJob {
     LevelState* st;
     uint32_t* probe_host;  // [probe_k][c] or nullptr
 };
+// A sampled-GEMM engine as seen by the pipelined batch loop (mlsk_fused.cu):
+// a panel generator and a GEMM + fused level epilogue + fixed-order reduction.
+struct PanelEngine {
+    virtual ~PanelEngine() = default;
+    virtual int64_t panel_bytes(int64_t c) const = 0;  // per level-sample
+    virtual int64_t group_size() const = 0;            // samples per round of the CTA groups
+    virtual void gen(cudaStream_t s, uint64_t seed, uint64_t tag, const int64_t* ks, int nb, int64_t c, int64_t cc,
+                     double w_fine, double w_coarse, void* panels, uint32_t* idx) = 0;
+    virtual void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, LevelState& st) = 0;
+};
+std::unique_ptr<PanelEngine> make_tc_engine(const Model& M, Workspace& ws);  // mlsk_tc.cu
+
 // Runs all jobs of a round as one software pipeline (panel generation of
 // batch i+1 overlapped with the GEMM of batch i on two streams).  Work is
 // ordered after `a.stream`'s prior work and `a.stream` waits for its end;

@@ -69,6 +69,67 @@ __global__ void __launch_bounds__(256) k_dmma_peak(double* out, int iters) {
     if (acc == 12345.678) out[0] = acc;
 }
 
+// TF32 tcgen05 throughput loop: one CTA per SM, M=128 N=256 K=8 MMAs from
+// (zeroed) shared memory into TMEM, committed to an mbarrier every 64 MMAs.
+__global__ void __launch_bounds__(128, 1) k_tf32_peak(int rounds, int n, uint32_t* sink) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    unsigned char* base = sm + ((1024 - ((uint32_t)__cvta_generic_to_shared(sm) & 1023)) & 1023);
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t s_tmem;
+    for (int i = threadIdx.x; i < 48 * 1024 / 16; i += blockDim.x) reinterpret_cast<uint4*>(base)[i] = make_uint4(0, 0, 0, 0);
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&s_tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = s_tmem;
+    if (threadIdx.x == 0) {
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(base), sb = sa + 16384;
+        auto desc = [](uint32_t a) {
+            return (uint64_t)((a & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) | ((uint64_t)1 << 46) |
+                   ((uint64_t)2 << 61);
+        };
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | (8u << 24);
+        uint32_t ph = 0;
+        for (int r = 0; r < rounds; ++r) {
+            for (int i = 0; i < 64; ++i) {
+                const uint64_t ad = desc(sa + (i & 3) * 32), bd = desc(sb + (i & 3) * 32);
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                             "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                             "l"(ad), "l"(bd), "r"(idesc), "r"(1u)
+                             : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(b)
+                         : "memory");
+            uint32_t done;
+            do {
+                asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                             "selp.u32 %0, 1, 0, p;\n\t}"
+                             : "=r"(done)
+                             : "r"(b), "r"(ph)
+                             : "memory");
+            } while (!done);
+            ph ^= 1;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    }
+    if (threadIdx.x == 0 && rounds < 0) sink[0] = tmem;
+}
+
 }  // namespace
 
 Prof::Prof(const char* n, cudaStream_t s) : name(n), stream(s) {
@@ -171,6 +232,45 @@ double mlsk_measure_fp64_peak(int device) {
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         const double flops = (double)grid * 8 /*warps*/ * iters * 8 /*mma*/ * 512.0;
+        result = flops / (best * 1e-3) / 1e12;
+    });
+    return result;
+}
+
+// Dense TF32 tcgen05 throughput measured on the device (M=128, N=n, K=8 per
+// instruction, one CTA per SM), TFLOP/s.  The 3xTF32 fp32 engine's peak is a third.
+double mlsk_measure_tf32_peak(int device, int n) {
+    double result = -1.0;
+    run_guarded([&] {
+        if (device >= 0) MLSK_CUDA(cudaSetDevice(device));
+        int dev = 0, sms = 0;
+        MLSK_CUDA(cudaGetDevice(&dev));
+        MLSK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        if (n <= 0 || n > 256 || n % 16) n = 256;
+        const int smem = 48 * 1024 + 1024;
+        MLSK_CUDA(cudaFuncSetAttribute(k_tf32_peak, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        DevArray<uint32_t> sink(1);
+        k_tf32_peak<<<sms, 128, smem>>>(4, n, sink.p);
+        launched();
+        MLSK_CUDA(cudaDeviceSynchronize());
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        float best = 1e30f;
+        const int rounds = 400;
+        for (int r = 0; r < 5; ++r) {
+            cudaEventRecord(e0);
+            k_tf32_peak<<<sms, 128, smem>>>(rounds, n, sink.p);
+            cudaEventRecord(e1);
+            launched();
+            MLSK_CUDA(cudaEventSynchronize(e1));
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            best = std::min(best, ms);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        const double flops = (double)sms * rounds * 64 * 2.0 * 128 * n * 8;
         result = flops / (best * 1e-3) / 1e12;
     });
     return result;

@@ -203,27 +203,39 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
             const bool isA = ph < a_ph;
             const int64_t rb = (int64_t)(isA ? ph : ph - a_ph) * TBM;
             const int64_t lim = isA ? M.m - rb : M.p - rb;
+            const bool quad_aligned = ((isA ? M.m : M.p) & 3) == 0;
             if (M.kind == MLSK_MODEL_GAUSS_MEAN) {
                 // one Philox block -> 4 normals for rows 4q..4q+3 of one column
+                // lanes span the 32 columns of a row quad: conflict-free SW128 stores
                 for (int item = tid; item < (TBM / 4) * TBK; item += GEN_T) {
-                    const int qd = item & (TBM / 4 - 1), tt = item / (TBM / 4);
+                    const int tt = item & (TBK - 1), qd = item / TBK;
                     const int r0 = 4 * qd;
                     const int j = s_j[tt];
                     float v[4] = {0.f, 0.f, 0.f, 0.f};
                     if (j >= 0 && r0 < lim) {
+                        // mean quad first (vector load when aligned) so its latency hides behind the RNG
+                        const float* mp = isA ? M.mean_at_f + (int64_t)j * M.m + rb + r0
+                                              : M.mean_b_f + (int64_t)j * M.p + rb + r0;
+                        float mv[4];
+                        if (quad_aligned && r0 + 3 < lim) {
+                            const float4 q4 = __ldg(reinterpret_cast<const float4*>(mp));
+                            mv[0] = q4.x; mv[1] = q4.y; mv[2] = q4.z; mv[3] = q4.w;
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) mv[e] = r0 + e < lim ? __ldg(mp + e) : 0.f;
+                        }
                         const u32x4 r = philox((uint32_t)j, (uint32_t)((rb + r0) >> 2), 0,
                                                isA ? MLSK_CTR_A : MLSK_CTR_B, key);
                         float z[4];
                         box_muller_f(r.x, r.y, z[0], z[1], T);
                         box_muller_f(r.z, r.w, z[2], z[3], T);
                         const float sd = (float)M.sd;
+                        const float w = isA ? 1.0f : s_w[tt];
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             if (r0 + e < lim) {
-                                const float mean = isA ? M.mean_at_f[(int64_t)j * M.m + rb + r0 + e]
-                                                       : M.mean_b_f[(int64_t)j * M.p + rb + r0 + e];
-                                const float x = __fadd_rn(mean, __fmul_rn(sd, z[e]));
-                                v[e] = isA ? x : __fmul_rn(s_w[tt], x);
+                                const float x = __fadd_rn(mv[e], __fmul_rn(sd, z[e]));
+                                v[e] = isA ? x : __fmul_rn(w, x);
                             }
                         }
                     }
@@ -235,7 +247,7 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                 }
             } else {
                 for (int item = tid; item < TBM * TBK; item += GEN_T) {
-                    const int rr = item & (TBM - 1), tt = item / TBM;
+                    const int tt = item & (TBK - 1), rr = item / TBK;
                     const int j = s_j[tt];
                     float v = 0.f;
                     if (j >= 0 && rr < lim) {
@@ -257,6 +269,101 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
             for (int i = tid; i < TTILE / 16; i += GEN_T) {
                 dh[i] = sh[i];
                 dl[i] = sl[i];
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// RFF features: Z[x][j] = sqrt(2/n) cos(w_j . x + b_j).  A_S = Z[:, S] and
+// B_S = (w_t Z[:, j_t])^T, so the B chunk of columns [rb, rb+128) is the A
+// chunk of rows [rb, rb+128) scaled by w_t: both come from one evaluation.
+// The 128 x 32 dot products of a row block run from shared memory (X tile
+// transposed for conflict-free reads, W columns broadcast).
+constexpr int RFF_DMAX = 64;
+
+__global__ void __launch_bounds__(GEN_T)
+k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
+                 int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t nkc, float* __restrict__ Ahi,
+                 float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
+                 uint32_t* __restrict__ idx_out) {
+    extern __shared__ __align__(1024) unsigned char rsm[];
+    unsigned char* tiles = rsm;                                      // 4 x 16 KB: A hi, A lo, B hi, B lo
+    float* xs = reinterpret_cast<float*>(rsm + 4 * TTILE);           // [D][128]
+    float* wsm = xs + RFF_DMAX * TBM;                                // [D][32]
+    __shared__ int s_j[TBK];
+    __shared__ float s_w[TBK], s_b[TBK];
+    const DevModel& M = S.M;
+    const int D = (int)M.rff_dim;
+    const int tid = threadIdx.x;
+    const float scale = (float)M.rff_scale;
+    const int64_t items = (int64_t)nb * nkc;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int b = (int)(it / nkc);
+        const int64_t kc = it - (int64_t)b * nkc;
+        const uint64_t key = derive_seed(seed, tag, (uint64_t)ks[b]);
+        __syncthreads();
+        if (tid < TBK) {
+            const int64_t t = kc * TBK + tid;
+            int j = -1;
+            float w = 0.f;
+            if (t < c) {
+                const u32x4 r = philox((uint32_t)(t >> 1), 0, 0, MLSK_CTR_INDEX, key);
+                const uint32_t ix = index_from_u64((t & 1) ? hi64(r) : lo64(r), M.n, M.log2n, M.cum);
+                j = (int)(ix - 1);
+                w = t < cc ? w_coarse : w_fine;
+                if (idx_out) idx_out[(int64_t)b * c + t] = ix;
+            }
+            s_j[tid] = j;
+            s_w[tid] = w;
+            s_b[tid] = j >= 0 ? M.rff_b[j] : 0.f;
+        }
+        __syncthreads();
+        for (int e = tid; e < D * TBK; e += GEN_T) {
+            const int d = e / TBK, t = e - d * TBK;
+            const int j = s_j[t];
+            wsm[d * TBK + t] = j >= 0 ? M.rff_w[(int64_t)d * M.n + j] : 0.f;
+        }
+        for (int64_t rb = 0; rb < MP; rb += TBM) {
+            const int64_t lim = M.m - rb;
+            for (int e = tid; e < TBM * D; e += GEN_T) {
+                const int r = e / D, d = e - r * D;
+                xs[d * TBM + r] = r < lim ? M.rff_x[(rb + r) * D + d] : 0.f;
+            }
+            __syncthreads();
+            // lane = column t (W reads conflict-free, stores conflict-free), warp = 16 rows
+            // (X reads broadcast)
+            const int t = tid & (TBK - 1), r0 = (tid >> 5) * 16;
+            float acc[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+            for (int d = 0; d < D; ++d) {
+                const float w = wsm[d * TBK + t];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) acc[i] = __fmaf_rn(xs[d * TBM + r0 + i], w, acc[i]);
+            }
+            const bool valid = s_j[t] >= 0;
+            const float bt = s_b[t], wt = s_w[t];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int r = r0 + i;
+                float z = 0.f;
+                if (valid && r < lim) z = scale * cosf(acc[i] + bt);
+                const float v = __fmul_rn(wt, z);
+                const int off = sw128_off(r, t);
+                *reinterpret_cast<float*>(tiles + off) = z;
+                *reinterpret_cast<float*>(tiles + TTILE + off) = tf32_lo(z);
+                *reinterpret_cast<float*>(tiles + 2 * TTILE + off) = v;
+                *reinterpret_cast<float*>(tiles + 3 * TTILE + off) = tf32_lo(v);
+            }
+            __syncthreads();
+            const int64_t o = (((int64_t)b * nkc + kc) * MP + rb) * TBK;  // PP == MP for RFF
+            float* dst[4] = {Ahi + o, Alo + o, Bhi + o, Blo + o};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                float4* dq = reinterpret_cast<float4*>(dst[q]);
+                const float4* sq = reinterpret_cast<const float4*>(tiles + q * TTILE);
+                for (int i = tid; i < TTILE / 16; i += GEN_T) dq[i] = sq[i];
             }
             __syncthreads();
         }
@@ -458,87 +565,89 @@ bool tc_supported(const Model& M, int target) {
            (M.dm.kind == MLSK_MODEL_GAUSS_MEAN || M.dm.kind == MLSK_MODEL_STUDENT_T || M.dm.kind == MLSK_MODEL_RFF);
 }
 
-// Runs the jobs (levels) of a round on the tensor-core engine; same contract
-// as fused_run_round (ordered after a.stream, a.stream waits for the end).
-void tc_run_round(const RunArgs& a, std::vector<FusedJob>& jobs, cudaStream_t s) {
-    const Model& M = *a.model;
-    Workspace& ws = *a.ws;
-    const int nsm = sms();
-    const int64_t MP = (M.rows + TBM - 1) / TBM * TBM;
-    const int64_t PP = (M.cols + TBN - 1) / TBN * TBN;
-    const int tiles_n = (int)(PP / TBN);
-    const int T = (int)(MP / TBM) * tiles_n;
-    const int Gs = std::max(1, nsm / T);
-    const double n = (double)M.desc.n;
+namespace {
 
-    TcModel S{};
-    S.M = M.dm;
-    static bool attr = false;
-    const int smem = TSTAGES * TSTAGE_BYTES + 1024;
-    if (!attr) {
-        MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-    }
-    ws.partial.ensure((size_t)T * Gs * (TBM * TBN) + (size_t)T * Gs);
-    double* part = ws.partial.p;
-    double* part_sq = part + (size_t)T * Gs * (TBM * TBN);
-    const int64_t budget = int64_t(1) << 31;  // panel bytes per batch (hi + lo, A + B)
-
-    for (auto& job : jobs) {
-        std::vector<int64_t> ks;
-        for (const auto& sg : job.segs)
-            for (int64_t k = 0; k < sg.count; ++k) ks.push_back(sg.k0 + k);
-        if (ks.empty()) continue;
-        const int64_t c = job.lv.c, cc = job.lv.cc;
-        const int64_t nkc = (c + TBK - 1) / TBK;
-        const int64_t per = (MP + PP) * nkc * TBK * 8;
-        int64_t max_nb = std::max<int64_t>(1, budget / per);
-        if (max_nb > Gs) max_nb = max_nb / Gs * Gs;
-        const float w_fine = (float)(n / (double)c);
-        const float w_coarse = cc > 0 ? (float)(n / (double)c - n / (double)cc) : w_fine;
-        for (size_t off = 0; off < ks.size(); off += (size_t)max_nb) {
-            const int nb = (int)std::min<int64_t>(max_nb, (int64_t)ks.size() - (int64_t)off);
-            ws.ks.ensure(nb);
-            MLSK_CUDA(cudaMemcpyAsync(ws.ks.p, ks.data() + off, sizeof(int64_t) * nb, cudaMemcpyHostToDevice, s));
-            const size_t na = (size_t)nb * nkc * MP * TBK, nbp = (size_t)nb * nkc * PP * TBK;
-            ws.panel_af.ensure(2 * na);
-            ws.panel_bf.ensure(2 * nbp);
-            float *Ahi = ws.panel_af.p, *Alo = Ahi + na, *Bhi = ws.panel_bf.p, *Blo = Bhi + nbp;
-            uint32_t* idx = nullptr;
-            if (job.probe_host) {
-                ws.idx.ensure((size_t)nb * c);
-                idx = ws.idx.p;
-            }
-            {
-                Prof p("gen_panels_tf32", s);
-                k_gen_panels_tf32<<<(int)std::min<int64_t>((int64_t)nb * nkc, (int64_t)nsm * 8), GEN_T, 0, s>>>(
-                    S, a.seed, job.lv.tag, ws.ks.p, nb, c, cc, w_fine, w_coarse, MP, PP, nkc, Ahi, Alo, Bhi, Blo,
-                    idx);
-            }
-            MLSK_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * (size_t)T * Gs * (TBM * TBN), s));
-            TcShape sh{nb, nkc, MP, PP, T, Gs, tiles_n};
-            {
-                Prof p("gemm_tf32x3", s);
-                k_gemm_tf32x3<<<T * Gs, TC_THREADS, smem, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq);
-            }
-            {
-                Prof p("reduce_tiles_tc", s);
-                const int64_t cells = M.rows * M.cols;
-                k_reduce_tiles_tc<<<(int)std::min<int64_t>((cells + 255) / 256, (int64_t)nsm * 8), 256, 0, s>>>(
-                    part, part_sq, sh, M.rows, M.cols, job.st->total(), job.st->total_sq());
-            }
-            launched(3);
-            if (idx) {
-                MLSK_CUDA(cudaStreamSynchronize(s));
-                for (int b = 0; b < nb; ++b)
-                    if (ks[off + b] < a.probe_k)
-                        MLSK_CUDA(cudaMemcpy(job.probe_host + ks[off + b] * c, idx + (int64_t)b * c,
-                                             sizeof(uint32_t) * c, cudaMemcpyDeviceToHost));
-            }
+class TcEngine final : public PanelEngine {
+   public:
+    TcEngine(const Model& M, Workspace& ws) : M_(M), ws_(ws) {
+        nsm_ = sms();
+        MP_ = (M.rows + TBM - 1) / TBM * TBM;
+        PP_ = (M.cols + TBN - 1) / TBN * TBN;
+        tiles_n_ = (int)(PP_ / TBN);
+        T_ = (int)(MP_ / TBM) * tiles_n_;
+        Gs_ = std::max(1, nsm_ / T_);
+        S_.M = M.dm;
+        smem_ = TSTAGES * TSTAGE_BYTES + 1024;
+        static bool attr = false;
+        if (!attr) {
+            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+            attr = true;
         }
-        job.st->count += (int64_t)ks.size();
-        MLSK_CUDA(cudaStreamSynchronize(s));  // host ks vector reused per job
+        ws_.partial.ensure((size_t)T_ * Gs_ * (TBM * TBN) + (size_t)T_ * Gs_);
+        rff_smem_ = 4 * TTILE + (RFF_DMAX * TBM + RFF_DMAX * TBK) * 4;
+        static bool rattr = false;
+        if (!rattr) {
+            MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_rff, cudaFuncAttributeMaxDynamicSharedMemorySize, rff_smem_));
+            rattr = true;
+        }
     }
+    int64_t panel_bytes(int64_t c) const override { return (MP_ + PP_) * nkc(c) * TBK * 8; }  // hi + lo
+    int64_t group_size() const override { return Gs_; }
+    void gen(cudaStream_t s, uint64_t seed, uint64_t tag, const int64_t* ks, int nb, int64_t c, int64_t cc,
+             double w_fine, double w_coarse, void* panels, uint32_t* idx) override {
+        float *Ahi, *Alo, *Bhi, *Blo;
+        split(panels, nb, c, Ahi, Alo, Bhi, Blo);
+        const int64_t k = nkc(c);
+        Prof p("gen_panels_tf32", s);
+        if (M_.dm.kind == MLSK_MODEL_RFF && M_.dm.rff_dim <= RFF_DMAX) {
+            k_gen_panels_rff<<<(int)std::min<int64_t>((int64_t)nb * k, (int64_t)nsm_ * 4), GEN_T, rff_smem_, s>>>(
+                S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, k, Ahi, Alo, Bhi, Blo, idx);
+        } else {
+            k_gen_panels_tf32<<<(int)std::min<int64_t>((int64_t)nb * k, (int64_t)nsm_ * 8), GEN_T, 0, s>>>(
+                S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, Ahi, Alo, Bhi, Blo, idx);
+        }
+        launched();
+    }
+    void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, LevelState& st) override {
+        float *Ahi, *Alo, *Bhi, *Blo;
+        split(const_cast<void*>(panels), nb, c, Ahi, Alo, Bhi, Blo);
+        double* part = ws_.partial.p;
+        double* part_sq = part + (size_t)T_ * Gs_ * (TBM * TBN);
+        MLSK_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * (size_t)T_ * Gs_ * (TBM * TBN), s));
+        TcShape sh{nb, nkc(c), MP_, PP_, T_, Gs_, tiles_n_};
+        {
+            Prof p("gemm_tf32x3", s);
+            k_gemm_tf32x3<<<T_ * Gs_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq);
+        }
+        {
+            Prof p("reduce_tiles_tc", s);
+            const int64_t cells = M_.rows * M_.cols;
+            k_reduce_tiles_tc<<<(int)std::min<int64_t>((cells + 255) / 256, (int64_t)nsm_ * 8), 256, 0, s>>>(
+                part, part_sq, sh, M_.rows, M_.cols, st.total(), st.total_sq());
+        }
+        launched(2);
+    }
+
+   private:
+    static int64_t nkc(int64_t c) { return (c + TBK - 1) / TBK; }
+    void split(void* panels, int nb, int64_t c, float*& Ahi, float*& Alo, float*& Bhi, float*& Blo) const {
+        const size_t na = (size_t)nb * nkc(c) * MP_ * TBK, nbp = (size_t)nb * nkc(c) * PP_ * TBK;
+        Ahi = static_cast<float*>(panels);
+        Alo = Ahi + na;
+        Bhi = Alo + na;
+        Blo = Bhi + nbp;
+    }
+    const Model& M_;
+    Workspace& ws_;
+    TcModel S_{};
+    int nsm_, T_, Gs_, tiles_n_, smem_, rff_smem_;
+    int64_t MP_, PP_;
+};
+
+}  // namespace
+
+std::unique_ptr<PanelEngine> make_tc_engine(const Model& M, Workspace& ws) {
+    return std::unique_ptr<PanelEngine>(new TcEngine(M, ws));
 }
 
 }  // namespace mlsk

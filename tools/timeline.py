@@ -10,7 +10,8 @@ from paper_1904_00429_b200 import mlsketch as g  # noqa: E402
 from paper_1904_00429_b200._lib import lib  # noqa: E402
 
 L = lib()
-stream = torch.cuda.current_stream()
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)
 opts = g.EstimatorOptions(stream=stream.cuda_stream, engine="fused")
 model = g.gaussian_mean_matrix_model(256, 4096, 256, sd=0.5, data_seed=bench.data_seed())
 sess = g.MlmcSession(model, g.target_identity(), 2, 6, 1, c0=32, options=opts)
