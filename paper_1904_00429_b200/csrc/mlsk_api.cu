@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <memory>
 #include <mutex>
 
@@ -98,10 +99,20 @@ void check_target(int32_t target, double param) {
     if (target == MLSK_TARGET_F2 && !(param > 0.0)) invalid("target_f2: zeta must be positive");
 }
 
+// Workspaces of the one-shot estimator calls are cached per host thread and
+// device, so repeated calls reuse the panel buffers and pipeline streams.
+Workspace& cached_workspace(int device) {
+    static thread_local std::map<int, std::unique_ptr<Workspace>> cache;
+    auto& w = cache[device];
+    if (!w) w.reset(new Workspace());
+    return *w;
+}
+
 // Level driver shared by the estimators and the sessions.
 struct Runner {
     Model model;
-    Workspace ws;
+    Workspace own_ws;
+    Workspace* wsp = &own_ws;
     int target;
     double tparam;
     uint64_t seed;
@@ -127,13 +138,13 @@ struct Runner {
             std::vector<FusedJob> jobs;
             for (const auto& it : items)
                 jobs.push_back(FusedJob{it.lv, plan_segments(it.k0, it.k1, rank, world, *it.st), it.st, it.probe});
-            RunArgs a{&model, target, tparam, seed, s, &ws, probe_k, nullptr};
+            RunArgs a{&model, target, tparam, seed, s, wsp, probe_k, nullptr};
             fused_run_round(a, jobs);
             return;
         }
         for (const auto& it : items) {
             const auto segs = plan_segments(it.k0, it.k1, rank, world, *it.st);
-            RunArgs a{&model, target, tparam, seed, s, &ws, probe_k, it.probe};
+            RunArgs a{&model, target, tparam, seed, s, wsp, probe_k, it.probe};
             exact_run(a, it.lv, segs, *it.st);
         }
     }
@@ -163,6 +174,7 @@ int mlmc_impl(bool matrix, const mlsk_model_desc* model, int32_t target, double 
         if (model_is_vector(model) == matrix) invalid("estimator: model kind does not match the estimator");
         Exec ex(opts);
         Runner R;
+        R.wsp = &cached_workspace(ex.device);
         build_model(R.model, model, ex.stream);
         R.target = target;
         R.tparam = tparam;
@@ -227,6 +239,7 @@ int mc_impl(bool matrix, const mlsk_model_desc* model, int32_t target, double tp
         if (model_is_vector(model) == matrix) invalid("estimator: model kind does not match the estimator");
         Exec ex(opts);
         Runner R;
+        R.wsp = &cached_workspace(ex.device);
         build_model(R.model, model, ex.stream);
         R.target = target;
         R.tparam = tparam;

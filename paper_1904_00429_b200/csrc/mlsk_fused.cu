@@ -548,8 +548,7 @@ struct Pipe {
     size_t ks_cap = 0;
     DevArray<double> part;
     bool staged_pending = false;
-    std::unique_ptr<PanelEngine> engine;
-    const Model* engine_model = nullptr;
+
     Pipe() {
         int lo = 0, hi = 0;
         MLSK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -684,11 +683,9 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
 
     // ---- matrix path: batches of replications, software-pipelined over a
     // panel engine (fp64 DMMA or the tcgen05 3xTF32 engine for fp32 models)
-    if (!P.engine || P.engine_model != &M) {
-        P.engine = tc_supported(M, a.target) ? make_tc_engine(M, ws) : make_f64_engine(M, ws);
-        P.engine_model = &M;
-    }
-    PanelEngine& E = *P.engine;
+    // geometry-only object, rebuilt per round (the workspace may be shared by models)
+    std::unique_ptr<PanelEngine> engine = tc_supported(M, a.target) ? make_tc_engine(M, ws) : make_f64_engine(M, ws);
+    PanelEngine& E = *engine;
     const int64_t Gs = E.group_size();
     const int64_t budget = int64_t(384) << 20;  // panel bytes per batch (x NBUF in flight)
 
