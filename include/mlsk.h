@@ -187,6 +187,12 @@ int mlsk_sketch_matmul(const double* A, const double* B, int64_t m, int64_t n, i
 int mlsk_draw_sample(const mlsk_model_desc* model, uint64_t seed, uint64_t tag, int64_t k,
                      int64_t c, uint32_t* indices, double* a_cols, double* b_rows);
 
+/* Fixed model data as generated on the device (for ground truth): which = 0
+ * means of A / a (RFF: points X, m x D), 1 means of B / b (RFF: W, D x n),
+ * 2 RFF phases.  With out == NULL only *count is set; else *count values of
+ * the model dtype are copied to out. */
+int mlsk_model_data(const mlsk_model_desc* model, int32_t which, void* out, int64_t* count);
+
 /* RngStream::derive_seed (rng.hpp:31-37) -- pure host arithmetic. */
 uint64_t mlsk_derive_seed(uint64_t master, uint64_t a, uint64_t b);
 

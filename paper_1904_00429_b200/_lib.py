@@ -51,6 +51,7 @@ def lib():
                                      _P(C.c_uint32), C.c_int64, _P(C.c_double), _P(C.c_double)]
     L.mlsk_draw_sample.argtypes = [_P(abi.ModelDesc), C.c_uint64, C.c_uint64, C.c_int64, C.c_int64,
                                    _P(C.c_uint32), _P(C.c_double), _P(C.c_double)]
+    L.mlsk_model_data.argtypes = [_P(abi.ModelDesc), C.c_int32, C.c_void_p, _P(C.c_int64)]
     L.mlsk_derive_seed.restype = C.c_uint64
     L.mlsk_derive_seed.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
     L.mlsk_last_error.restype = C.c_char_p

@@ -443,6 +443,35 @@ int mlsk_draw_sample(const mlsk_model_desc* model, uint64_t seed, uint64_t tag, 
     });
 }
 
+int mlsk_model_data(const mlsk_model_desc* model, int32_t which, void* out, int64_t* count) {
+    return guard([&] {
+        if (!count) invalid("model_data: null count");
+        Exec ex(nullptr);
+        Model M;
+        build_model(M, model, ex.stream);
+        const void* src = nullptr;
+        size_t elem = 8, n = 0;
+        const bool f32 = M.dm.dtype == MLSK_F32;
+        if (M.dm.kind == MLSK_MODEL_GAUSS_MEAN) {
+            if (which == 0) { src = f32 ? (const void*)M.mean_a_f.p : (const void*)M.mean_a.p; n = f32 ? M.mean_a_f.n : M.mean_a.n; }
+            if (which == 1) { src = f32 ? (const void*)M.mean_b_f.p : (const void*)M.mean_b.p; n = f32 ? M.mean_b_f.n : M.mean_b.n; }
+            elem = f32 ? 4 : 8;
+        } else if (M.dm.kind == MLSK_MODEL_RFF) {
+            elem = 4;
+            if (which == 0) { src = M.rff_x.p; n = M.rff_x.n; }
+            if (which == 1) { src = M.rff_w.p; n = M.rff_w.n; }
+            if (which == 2) { src = M.rff_b.p; n = M.rff_b.n; }
+        }
+        if (!src) invalid("model_data: this model has no such stored data");
+        if (out) {
+            if ((size_t)*count < n) invalid("model_data: output buffer too small");
+            MLSK_CUDA(cudaMemcpyAsync(out, src, n * elem, cudaMemcpyDeviceToHost, ex.stream));
+            MLSK_CUDA(cudaStreamSynchronize(ex.stream));
+        }
+        *count = (int64_t)n;
+    });
+}
+
 uint64_t mlsk_derive_seed(uint64_t master, uint64_t a, uint64_t b) { return derive_seed(master, a, b); }
 
 const char* mlsk_last_error(void) { return g_last_error.c_str(); }

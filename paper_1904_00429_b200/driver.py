@@ -1,0 +1,183 @@
+"""Adaptive multilevel driver over the round API, sharded across ranks.
+
+The reference plans N_l a priori only (planner.cpp:65-81, make_plan :94-100;
+adaptive allocation is an explicit non-goal).  BASELINE
+configs 2, 3 and 5 need the standard MLMC allocation computed from measured
+level variances, so this module adds the classic adaptive loop (Giles,
+"Multilevel Monte Carlo methods", Acta Numerica 2015, Alg. 1 with fixed L):
+
+  1. pilot round of N_pilot replications per level;
+  2. V_l = E||Y_l||_F^2 - ||E Y_l||_F^2 from the per-level sums, C_l = cost of
+     one level-l replication (c_l + c_{l-1} sampled indices x cells, the
+     reference's cost units, estimators.cpp:34-40);
+  3. N_l = ceil( (1/(theta eps^2)) sqrt(V_l / C_l) sum_k sqrt(V_k C_k) ),
+     run the missing dN_l = N_l - n_l; repeat until nothing is missing.
+
+Every level's identity-target sketch is unbiased for E[A B],
+so the MSE is the variance sum_l V_l / N_l <= theta eps^2 (theta = 1 by
+default; 1/2 reserves half of the MSE for a bias term).
+
+Multi-GPU: one process per GPU.  Rank r runs the 64-replication chunks
+q = r (mod world) of every round (the library's exec option), then ONE
+all-reduce of the packed per-level buffer [(sum Y, sum ||Y||^2, count)] per
+round -- NCCL on the device buffer when the process group's backend is NCCL,
+gloo on a host copy otherwise.  Every rank then holds the same global
+statistics and computes the same next allocation; there is no other
+communication.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+
+@dataclass
+class LevelStats:
+    """Global (all-rank) per-level accumulators."""
+
+    sums: np.ndarray       # [L+1, cells]
+    sumsq: np.ndarray      # [L+1]
+    counts: np.ndarray     # [L+1]
+
+    @property
+    def estimates(self) -> np.ndarray:
+        return self.sums / np.maximum(self.counts, 1)[:, None]
+
+    @property
+    def variances(self) -> np.ndarray:
+        """V_l = E||Y||^2 - ||E Y||^2 (Frobenius), floored at 0."""
+        n = np.maximum(self.counts, 1)
+        meansq = self.sumsq / n
+        return np.maximum(meansq - np.sum(self.estimates ** 2, axis=1), 0.0)
+
+    @property
+    def value(self) -> np.ndarray:
+        return self.estimates.sum(axis=0)
+
+    @property
+    def mse(self) -> float:
+        n = np.maximum(self.counts, 1)
+        return float(np.sum(self.variances / n))
+
+
+@dataclass
+class AdaptiveResult:
+    value: np.ndarray
+    stats: LevelStats
+    rounds: int
+    N: List[int]
+    eps: float
+    rmse_estimate: float
+    cost_units: int
+    history: List[List[int]] = field(default_factory=list)
+
+
+def pack(sums: np.ndarray, sumsq: np.ndarray, counts: np.ndarray) -> np.ndarray:
+    L1, cells = sums.shape
+    buf = np.zeros((L1, cells + 2))
+    buf[:, :cells] = sums
+    buf[:, cells] = sumsq
+    buf[:, cells + 1] = counts
+    return buf.ravel()
+
+
+def unpack(buf: np.ndarray, levels: int) -> LevelStats:
+    b = np.asarray(buf, dtype=np.float64).reshape(levels, -1)
+    cells = b.shape[1] - 2
+    return LevelStats(b[:, :cells].copy(), b[:, cells].copy(), np.rint(b[:, cells + 1]).astype(np.int64))
+
+
+def allreduce_stats(session, levels: int, group=None) -> LevelStats:
+    """One all-reduce of the packed level buffer across the process group."""
+    import torch.distributed as dist
+
+    if group is None and not (dist.is_available() and dist.is_initialized()):
+        return unpack(session.packed_stats(), levels)
+    backend = dist.get_backend(group)
+    if backend == "nccl" and hasattr(session, "level_buffer"):
+        import torch
+
+        ptr, n = session.level_buffer()
+        t = torch.as_tensor(_DevBuf(ptr, n), device="cuda")
+        dist.all_reduce(t, group=group)
+        return unpack(t.double().cpu().numpy(), levels)
+    import torch
+
+    t = torch.from_numpy(session.packed_stats())
+    dist.all_reduce(t, group=group)
+    return unpack(t.numpy(), levels)
+
+
+class _DevBuf:
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3,
+                                         "stream": None}
+
+
+def optimal_allocation(V: Sequence[float], C: Sequence[float], eps: float, theta: float = 1.0) -> List[int]:
+    """N_l = ceil( sqrt(V_l/C_l) * sum_k sqrt(V_k C_k) / (theta eps^2) )."""
+    V = np.asarray(V, dtype=np.float64)
+    C = np.asarray(C, dtype=np.float64)
+    s = float(np.sum(np.sqrt(V * C)))
+    return [int(math.ceil(math.sqrt(v / c) * s / (theta * eps * eps))) if v > 0 else 1 for v, c in zip(V, C)]
+
+
+def level_costs(M: int, c0: int, L: int, cells: int) -> List[float]:
+    """Reference cost units per replication: (c_l + [l>0] c_{l-1}) * cells."""
+    out = []
+    for l in range(L + 1):
+        c = c0 * M ** l
+        out.append(float((c + (c // M if l > 0 else 0)) * cells))
+    return out
+
+
+def adaptive_mlmc(session, M: int, c0: int, L: int, eps: float, n_pilot: int = 256, theta: float = 1.0,
+                  max_rounds: int = 20, max_total: Optional[int] = None, group=None) -> AdaptiveResult:
+    """Run rounds on `session` (an MlmcSession, or any object with run_round /
+    packed_stats / cells) until sum_l V_l / N_l <= theta eps^2.
+
+    `session` must be created with rank / world matching the process group:
+    each rank then runs its chunk share of every round's dN.
+    """
+    levels = L + 1
+    cells = session.cells
+    C = level_costs(M, c0, L, cells)
+    n = [0] * levels
+    history = []
+    session.run_round([n_pilot] * levels)
+    n = [n_pilot] * levels
+    history.append(list(n))
+    stats = allreduce_stats(session, levels, group)
+    rounds = 1
+    while rounds < max_rounds:
+        target = optimal_allocation(stats.variances, C, eps, theta)
+        dN = [max(0, t - k) for t, k in zip(target, n)]
+        if max_total is not None:
+            room = max(0, max_total - sum(n))
+            if sum(dN) > room:
+                scale = room / max(sum(dN), 1)
+                dN = [int(d * scale) for d in dN]
+        if sum(dN) == 0:
+            break
+        session.run_round(dN)
+        n = [a + b for a, b in zip(n, dN)]
+        history.append(list(dN))
+        stats = allreduce_stats(session, levels, group)
+        rounds += 1
+    cost = int(sum(k * c for k, c in zip(stats.counts, C)))
+    return AdaptiveResult(stats.value, stats, rounds, [int(x) for x in stats.counts], eps,
+                          math.sqrt(stats.mse), cost, history)
+
+
+def relative_error(estimate, reference) -> float:
+    """Frobenius relative error, +inf when the reference is 0 (tensor.cpp:152-174)."""
+    e = np.asarray(estimate, dtype=np.float64).ravel()
+    r = np.asarray(reference, dtype=np.float64).ravel()
+    den = float(np.sum(r * r))
+    num = float(np.sum((e - r) ** 2))
+    if den == 0.0:
+        return 0.0 if num == 0.0 else math.inf
+    return math.sqrt(num / den)

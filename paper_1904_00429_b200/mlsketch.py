@@ -25,6 +25,7 @@ All computation runs in the CUDA library; a missing library raises on import.
 from __future__ import annotations
 
 import ctypes as C
+import math
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional, Sequence
 
@@ -471,6 +472,58 @@ def draw_sample(model, seed: int, tag: int, k: int, c: int):
     return idx, a, b
 
 
+# ------------------------------------------------------ model data / truth
+
+
+def model_data(model, which: int) -> np.ndarray:
+    """Fixed model data as generated on the device: which = 0 -> means of A / a
+    (RFF: the points X, m x D), 1 -> means of B / b (RFF: W, D x n), 2 -> RFF
+    phases b."""
+    d = model.desc()
+    n = C.c_int64()
+    check(lib().mlsk_model_data(C.byref(d), which, None, C.byref(n)))
+    dt = np.float32 if model.dtype == abi.F32 else np.float64
+    out = np.zeros(n.value, dtype=dt)
+    check(lib().mlsk_model_data(C.byref(d), which, out.ctypes.data_as(C.c_void_p), C.byref(n)))
+    return out
+
+
+def ground_truth(model, device: str = "cuda"):
+    """The exact target of the estimators for identity f: E[a^T b] / E[A B]
+    (gauss-mean and deterministic models: the product of the means, one dense
+    fp64 GEMM), or for the RFF model the full-feature Gram matrix K_n = Z Z^T
+    together with the exact Gaussian kernel exp(-|x-y|^2 / (2 sigma^2)).
+    (reference_inner / reference_matmul estimate this by MC, models.cpp:140-227.)"""
+    import torch
+
+    if model.kind == abi.MODEL_CONSTANT_ONES:
+        return float(model.n) if isinstance(model, VectorPairModel) else np.full((model.m, model.p), float(model.n))
+    if model.kind == abi.MODEL_DETERMINISTIC:
+        if isinstance(model, VectorPairModel):
+            j = np.arange(1, model.n + 1, dtype=np.float64)
+            return float(np.dot(j, model.n + j))
+        return np.array([[19.0, 22.0], [43.0, 50.0]])
+    if model.kind == abi.MODEL_GAUSS_MEAN:
+        a = torch.as_tensor(model_data(model, 0), dtype=torch.float64, device=device)
+        b = torch.as_tensor(model_data(model, 1), dtype=torch.float64, device=device)
+        if isinstance(model, VectorPairModel):
+            return float(torch.dot(a, b))
+        return (a.view(model.m, model.n) @ b.view(model.n, model.p)).cpu().numpy()
+    if model.kind == abi.MODEL_RFF:
+        X = torch.as_tensor(model_data(model, 0), dtype=torch.float64, device=device).view(model.m, model.rff_dim)
+        W = torch.as_tensor(model_data(model, 1), dtype=torch.float64, device=device).view(model.rff_dim, model.n)
+        bph = torch.as_tensor(model_data(model, 2), dtype=torch.float64, device=device)
+        Kn = torch.zeros(model.m, model.m, dtype=torch.float64, device=device)
+        step = 8192
+        for j0 in range(0, model.n, step):
+            Z = torch.cos(X @ W[:, j0:j0 + step] + bph[j0:j0 + step]) * math.sqrt(2.0 / model.n)
+            Kn += Z @ Z.T
+        d2 = torch.cdist(X, X) ** 2
+        K = torch.exp(-d2 / (2.0 * model.sigma ** 2))
+        return Kn.cpu().numpy(), K.cpu().numpy()
+    raise ValueError("ground_truth: no closed form for this model kind")
+
+
 # ----------------------------------------------------------- round API
 
 
@@ -510,6 +563,21 @@ class MlmcSession:
         n = C.c_int64()
         check(lib().mlsk_session_level_buffer(self._h, C.byref(ptr), C.byref(n)))
         return int(ptr.value), int(n.value)
+
+    @property
+    def cells(self) -> int:
+        return self.rows * self.cols
+
+    def packed_stats(self) -> np.ndarray:
+        """Host copy of this rank's [(sum Y, sum ||Y||^2, count)] per level."""
+        r = self.stats()
+        cells = self.cells
+        buf = np.zeros((self.L + 1, cells + 2))
+        for l, st in enumerate(r.per_level):
+            buf[l, :cells] = np.asarray(st.sum, dtype=np.float64).ravel()
+            buf[l, cells] = st.sum_of_squares
+            buf[l, cells + 1] = st.replication_count
+        return buf.ravel()
 
     def synchronize(self) -> None:
         check(lib().mlsk_session_synchronize(self._h))
