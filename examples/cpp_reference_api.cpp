@@ -1,0 +1,27 @@
+// Example: reference-style C++ call through include/mlsk.hpp (link libmlsk.so).
+//   g++ -std=c++17 -Iinclude examples/cpp_reference_api.cpp \
+//       -Lpaper_1904_00429_b200/_lib -lmlsk -Wl,-rpath,$PWD/paper_1904_00429_b200/_lib
+#include <cstdio>
+
+#include "mlsk.hpp"
+
+using namespace mlsketch_b200;
+
+int main() {
+    try {
+        // test_estimators.cpp:39-60: constant data collapses every level above zero
+        const auto r = mlmc_inner(constant_ones_model(37), target_identity(), LevelPlan{3, 2, {9, 3, 1}}, 77);
+        std::printf("value %.1f level1 %.1f\n", r.value, r.per_level[1].estimate);
+        // config-2 shapes through the fused DMMA engine
+        const auto m = mlmc_matmul(gaussian_mean_matrix_model(256, 4096, 256, 0.5, -1.0, 1.0, 5), target_identity(),
+                                   LevelPlan{2, 2, {64, 32, 16}, 32}, 20260823);
+        std::printf("config2 value[0] %.6f cost %lld\n", m.value[0], m.total_cost_units);
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        std::printf("invalid_argument: %s\n", e.what());
+        return 1;
+    } catch (const std::exception& e) {
+        std::printf("runtime error: %s\n", e.what());
+        return 3;
+    }
+}

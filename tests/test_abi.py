@@ -64,3 +64,34 @@ def test_invalid_arguments_map_to_value_error_before_device_use():
         g.target_f2(-1.0)
     with pytest.raises(ValueError):
         g.constant_ones_model(0)
+
+
+def _build_cpp_example(tmp_path):
+    import subprocess
+    lib = os.path.join(ROOT, "paper_1904_00429_b200", "_lib")
+    exe = str(tmp_path / "cppex")
+    subprocess.run(["g++", "-std=c++17", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "cpp_reference_api.cpp"), "-L" + lib, "-lmlsk",
+                    "-Wl,-rpath," + lib, "-o", exe], check=True)
+    return exe
+
+
+def test_cpp_wrapper_restores_reference_signatures(tmp_path):
+    """include/mlsk.hpp compiles against the ABI; without a device the call
+    fails loudly (std::runtime_error -> exit 3, the CLI's runtime code)."""
+    import subprocess
+    from paper_1904_00429_b200 import _lib
+    exe = _build_cpp_example(tmp_path)
+    if _lib.lib().mlsk_device_count() > 0:
+        pytest.skip("a CUDA device is visible (tests/test_gpu_* run the example)")
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 3 and "no CUDA device" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_wrapper_on_device(tmp_path):
+    import subprocess
+    exe = _build_cpp_example(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout
+    assert r.stdout.startswith("value 37.0 level1 0.0")
