@@ -46,18 +46,28 @@ struct Prof {
     ~Prof();
 };
 
-// Owning device allocation.
+// Owning device allocation.  alloc_on() uses the stream-ordered allocator
+// (pooled, no implicit device synchronisation on free) for per-call objects;
+// alloc() is a plain cudaMalloc for long-lived workspaces.
+void configure_mempool();  // retain pooled memory across calls (mlsk_model.cu)
+
 template <class T>
 struct DevArray {
     T* p = nullptr;
     size_t n = 0;
+    cudaStream_t s = nullptr;
+    bool pooled = false;
     DevArray() = default;
     explicit DevArray(size_t count) { alloc(count); }
     DevArray(const DevArray&) = delete;
     DevArray& operator=(const DevArray&) = delete;
-    DevArray(DevArray&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevArray(DevArray&& o) noexcept : p(o.p), n(o.n), s(o.s), pooled(o.pooled) { o.p = nullptr; o.n = 0; }
     DevArray& operator=(DevArray&& o) noexcept {
-        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        if (this != &o) {
+            release();
+            p = o.p; n = o.n; s = o.s; pooled = o.pooled;
+            o.p = nullptr; o.n = 0;
+        }
         return *this;
     }
     ~DevArray() { release(); }
@@ -65,14 +75,26 @@ struct DevArray {
         release();
         if (count) MLSK_CUDA(cudaMalloc(&p, count * sizeof(T)));
         n = count;
+        pooled = false;
+    }
+    void alloc_on(size_t count, cudaStream_t st) {
+        release();
+        configure_mempool();
+        if (count) MLSK_CUDA(cudaMallocAsync(&p, count * sizeof(T), st));
+        n = count;
+        s = st;
+        pooled = true;
     }
     void ensure(size_t count) { if (count > n) alloc(count); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            if (pooled) cudaFreeAsync(p, s);
+            else cudaFree(p);
+        }
         p = nullptr;
         n = 0;
     }
-    void zero(cudaStream_t s) { if (n) MLSK_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
+    void zero(cudaStream_t st) { if (n) MLSK_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), st)); }
 };
 
 inline bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
@@ -118,7 +140,7 @@ struct LevelState {
     double* open_sq() const { return buf.p + 2 * cells + 1; }
     void init(int64_t cells_, cudaStream_t st) {
         cells = cells_;
-        buf.alloc(2 * cells + 2);
+        buf.alloc_on(2 * cells + 2, st);
         buf.zero(st);
         count = open_count = 0;
         open_chunk = -1;

@@ -14,6 +14,18 @@ __device__ __align__(16) const double g_log_d[256] = {MLSK_LOG_D_INIT};
 __device__ __align__(16) const float g_sincos_f[128] = {MLSK_SINCOS_F_INIT};
 __device__ __align__(16) const float g_log_f[128] = {MLSK_LOG_F_INIT};
 
+void configure_mempool() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;  // keep freed blocks pooled between calls
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done_dev = dev;
+}
+
 Tables device_tables() {
     static Tables t = [] {
         Tables r{};
@@ -165,14 +177,14 @@ void build_model(Model& M, const mlsk_model_desc* d, cudaStream_t st) {
         double run = 0.0;
         for (int64_t j = 0; j < D.n; ++j) { run += p; cum[j] = run; }
         cum[D.n - 1] = 1.0;
-        M.cum.alloc(D.n);
+        M.cum.alloc_on(D.n, st);
         MLSK_CUDA(cudaMemcpyAsync(M.cum.p, cum.data(), sizeof(double) * D.n, cudaMemcpyHostToDevice, st));
         dm.cum = M.cum.p;
     }
     if (k == MLSK_MODEL_PAPER_MATRIX) {  // models.cpp:47-48 cos(p) * H(5 - p), p <= 1000
         std::vector<double> t(1001);
         for (int pz = 0; pz <= 1000; ++pz) t[pz] = std::cos((double)pz) * (5.0 - pz >= 0.0 ? 1.0 : 0.0);
-        M.paper_b.alloc(1001);
+        M.paper_b.alloc_on(1001, st);
         MLSK_CUDA(cudaMemcpyAsync(M.paper_b.p, t.data(), sizeof(double) * 1001, cudaMemcpyHostToDevice, st));
         dm.paper_b = M.paper_b.p;
     }
@@ -189,8 +201,8 @@ void build_model(Model& M, const mlsk_model_desc* d, cudaStream_t st) {
         const int64_t nb = M.vector ? D.n : D.n * D.p;
         const double lo = D.mean_lo, w = D.mean_hi - D.mean_lo;
         if (f32) {
-            M.mean_a_f.alloc(na);
-            M.mean_b_f.alloc(nb);
+            M.mean_a_f.alloc_on(na, st);
+            M.mean_b_f.alloc_on(nb, st);
             if (D.mean_a) {
                 const float* h = (const float*)D.mean_a;
                 for (int64_t e = 0; e < na; ++e) if (h[e] != h[e]) invalid("DenseMatrix: NaN entry rejected");
@@ -212,14 +224,15 @@ void build_model(Model& M, const mlsk_model_desc* d, cudaStream_t st) {
             dm.mean_a_f = M.mean_a_f.p;
             dm.mean_b_f = M.mean_b_f.p;
             if (!M.vector) {
-                M.mean_at_f.alloc(na);
+                M.mean_at_f.alloc_on(na, st);
                 transpose<float>(M.mean_a_f.p, M.mean_at_f.p, D.m, D.n, st);
                 dm.mean_at_f = M.mean_at_f.p;
             }
         } else {
-            M.mean_a.alloc(na);
-            M.mean_b.alloc(nb);
-            DevArray<int> flag(1);
+            M.mean_a.alloc_on(na, st);
+            M.mean_b.alloc_on(nb, st);
+            DevArray<int> flag;
+            flag.alloc_on(1, st);
             flag.zero(st);
             if (D.mean_a) {
                 MLSK_CUDA(cudaMemcpyAsync(M.mean_a.p, D.mean_a, sizeof(double) * na, cudaMemcpyHostToDevice, st));
@@ -246,7 +259,7 @@ void build_model(Model& M, const mlsk_model_desc* d, cudaStream_t st) {
             dm.mean_a = M.mean_a.p;
             dm.mean_b = M.mean_b.p;
             if (!M.vector) {
-                M.mean_at.alloc(na);
+                M.mean_at.alloc_on(na, st);
                 transpose<double>(M.mean_a.p, M.mean_at.p, D.m, D.n, st);
                 dm.mean_at = M.mean_at.p;
             }
@@ -254,9 +267,9 @@ void build_model(Model& M, const mlsk_model_desc* d, cudaStream_t st) {
     }
     if (k == MLSK_MODEL_RFF) {
         const int64_t Dd = D.rff_dim;
-        M.rff_x.alloc(D.m * Dd);
-        M.rff_w.alloc(Dd * D.n);
-        M.rff_b.alloc(D.n);
+        M.rff_x.alloc_on(D.m * Dd, st);
+        M.rff_w.alloc_on(Dd * D.n, st);
+        M.rff_b.alloc_on(D.n, st);
         k_normals_f32<<<grid_for(D.m * Dd), 256, 0, st>>>(M.rff_x.p, D.m * Dd,
                                                           derive_seed(D.data_seed, MLSK_TAG_DATA, 2), 1.0,
                                                           dm.tab);
