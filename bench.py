@@ -192,11 +192,16 @@ def main():
         return run_reference_arm(args, rank)
 
     import torch
-    torch.cuda.set_device(local_rank)
+    device = local_rank % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(device)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("MLSK_DIST_BACKEND", "nccl")  # gloo: multi-rank tests on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group(backend)
 
     from paper_1904_00429_b200 import mlsketch as g
     from paper_1904_00429_b200._lib import lib
@@ -204,7 +209,7 @@ def main():
 
     stream = torch.cuda.Stream()            # explicit stream: the library orders its work on it
     torch.cuda.set_stream(stream)
-    opts = g.EstimatorOptions(device=local_rank, stream=stream.cuda_stream, rank=rank, world=world, engine="fused")
+    opts = g.EstimatorOptions(device=device, stream=stream.cuda_stream, rank=rank, world=world, engine="fused")
     model = g.gaussian_mean_matrix_model(M_, N_, P_, sd=0.5, mean_lo=-1.0, mean_hi=1.0, data_seed=data_seed())
     sess = g.MlmcSession(model, g.target_identity(), 2, LEVELS, MASTER, c0=C0, options=opts)
     dN = [n * world for n in STEP_N]          # global counts; this rank runs its chunks (~N_l)
@@ -225,7 +230,7 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    peak = L.mlsk_measure_fp64_peak(local_rank)
+    peak = L.mlsk_measure_fp64_peak(device)
     L.mlsk_profile_reset()
     L.mlsk_profile_enable(1)
     launches0 = L.mlsk_kernel_launch_count()
@@ -236,7 +241,7 @@ def main():
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(device) as clk:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -282,7 +287,7 @@ def main():
 
     e2e = None
     if not args.no_e2e and rank == 0:
-        e2e = run_e2e(g, torch, local_rank, args)
+        e2e = run_e2e(g, torch, device, args)
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1:
