@@ -67,6 +67,73 @@ __device__ __forceinline__ void load_tables(double2* s_sc, double2* s_lg, const 
 // streamed out with coalesced 16-byte stores.
 constexpr int GROWS = 128;
 
+// One phase: 128 rows of A (IS_A) or 128 columns of B, 16 sampled columns.
+// Thread (rp = tid % 64, tq = tid / 64) owns row pair rp of chunk columns
+// tq, tq+4, tq+8, tq+12 (lanes span row pairs: coalesced mean loads); the four
+// items are unrolled so their mean loads issue up front and four independent
+// Philox / Box-Muller chains interleave.
+template <bool IS_A>
+__device__ __forceinline__ void gen_phase(const DevModel& M, const Tables& T, uint64_t key, int64_t rb,
+                                          const int* s_j, const double* s_w, double* tl, int tid) {
+    constexpr int U = KC / (GEN_THREADS / (GROWS / 2));  // items per thread (4)
+    const int rp = tid & (GROWS / 2 - 1), tq = tid / (GROWS / 2);
+    const int r0 = 2 * rp;
+    const int64_t dim = IS_A ? M.m : M.p;
+    const int64_t lim = dim - rb;                      // valid rows / cols of this phase
+    const double* mrow = (IS_A ? M.mean_at : M.mean_b) + rb + r0;
+    const uint32_t rowpair = (uint32_t)((rb + r0) >> 1);
+    const double sd = M.sd;
+    if (r0 + 1 < lim && (dim & 1) == 0) {
+        // full aligned pair: vector mean loads first, then the generators
+        double2 mv[U];
+        int jj[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            jj[u] = s_j[tq + 4 * u];
+            mv[u] = __ldg(reinterpret_cast<const double2*>(mrow + (int64_t)(jj[u] < 0 ? 0 : jj[u]) * dim));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const u32x4 r = philox((uint32_t)jj[u], rowpair, 0, IS_A ? MLSK_CTR_A : MLSK_CTR_B, key);
+            double z0, z1;
+            box_muller(lo64(r), hi64(r), z0, z1, T);
+            double a = __dadd_rn(mv[u].x, __dmul_rn(sd, z0));
+            double b = __dadd_rn(mv[u].y, __dmul_rn(sd, z1));
+            if (!IS_A) {
+                const double w = s_w[tq + 4 * u];
+                a = __dmul_rn(w, a);
+                b = __dmul_rn(w, b);
+            }
+            tl[tile_slot(r0, tq + 4 * u)] = jj[u] < 0 ? 0.0 : a;
+            tl[tile_slot(r0 + 1, tq + 4 * u)] = jj[u] < 0 ? 0.0 : b;
+        }
+    } else {
+        // ragged edge (odd dimension or the last rows of the phase)
+#pragma unroll 1
+        for (int u = 0; u < U; ++u) {
+            const int j = s_j[tq + 4 * u];
+            double a = 0.0, b = 0.0;
+            if (j >= 0 && r0 < lim) {
+                const double* mp = mrow + (int64_t)j * dim;
+                const bool pair = r0 + 1 < lim;
+                const double m0 = __ldg(mp), m1 = pair ? __ldg(mp + 1) : 0.0;
+                const u32x4 r = philox((uint32_t)j, rowpair, 0, IS_A ? MLSK_CTR_A : MLSK_CTR_B, key);
+                double z0, z1;
+                box_muller(lo64(r), hi64(r), z0, z1, T);
+                a = __dadd_rn(m0, __dmul_rn(sd, z0));
+                if (pair) b = __dadd_rn(m1, __dmul_rn(sd, z1));
+                if (!IS_A) {
+                    const double w = s_w[tq + 4 * u];
+                    a = __dmul_rn(w, a);
+                    b = __dmul_rn(w, b);
+                }
+            }
+            tl[tile_slot(r0, tq + 4 * u)] = a;
+            tl[tile_slot(r0 + 1, tq + 4 * u)] = b;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(GEN_THREADS)
 k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
                  int64_t cc, double w_fine, double w_coarse, int64_t MP, int64_t PP, int64_t nkc,
@@ -83,7 +150,6 @@ k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restr
     const int tid = threadIdx.x;
     const int64_t items = (int64_t)nb * nkc;
     const int a_phases = (int)((MP + GROWS - 1) / GROWS), b_phases = (int)((PP + GROWS - 1) / GROWS);
-    const double sd = M.sd;
     int buf = 0;
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const int b = (int)(it / nkc);
@@ -108,40 +174,10 @@ k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restr
         for (int ph = 0; ph < a_phases + b_phases; ++ph) {
             const bool isA = ph < a_phases;
             const int64_t rb = (int64_t)(isA ? ph : ph - a_phases) * GROWS;
-            const int64_t lim = isA ? M.m - rb : M.p - rb;  // valid rows / cols
             const int64_t span = isA ? MP - rb : PP - rb;     // rows / cols in the panel
-            const bool pair_aligned = ((isA ? M.m : M.p) & 1) == 0;  // 16-byte mean pairs
             double* tl = tile[buf];
-#pragma unroll 2
-            // lanes span row pairs of one column: coalesced mean loads
-            for (int item = tid; item < (GROWS / 2) * KC; item += GEN_THREADS) {
-                const int rp = item & (GROWS / 2 - 1), tt = item / (GROWS / 2);
-                const int r0 = 2 * rp;
-                const int j = s_j[tt];
-                double v0 = 0.0, v1 = 0.0;
-                if (j >= 0 && r0 < lim) {
-                    // issue the mean loads first so their latency hides behind the RNG
-                    const double* mp = isA ? M.mean_at + (int64_t)j * M.m + rb + r0
-                                           : M.mean_b + (int64_t)j * M.p + rb + r0;
-                    const bool pair = r0 + 1 < lim;
-                    double2 mv;
-                    if (pair && pair_aligned) mv = __ldg(reinterpret_cast<const double2*>(mp));
-                    else mv = make_double2(__ldg(mp), pair ? __ldg(mp + 1) : 0.0);
-                    const u32x4 r =
-                        philox((uint32_t)j, (uint32_t)((rb + r0) >> 1), 0, isA ? MLSK_CTR_A : MLSK_CTR_B, key);
-                    double z0, z1;
-                    box_muller(lo64(r), hi64(r), z0, z1, T);
-                    v0 = __dadd_rn(mv.x, __dmul_rn(sd, z0));
-                    if (pair) v1 = __dadd_rn(mv.y, __dmul_rn(sd, z1));
-                    if (!isA) {
-                        const double w = s_w[tt];
-                        v0 = __dmul_rn(w, v0);
-                        v1 = __dmul_rn(w, v1);
-                    }
-                }
-                tl[tile_slot(r0, tt)] = v0;
-                tl[tile_slot(r0 + 1, tt)] = v1;
-            }
+            if (isA) gen_phase<true>(M, T, key, rb, s_j, s_w, tl, tid);
+            else gen_phase<false>(M, T, key, rb, s_j, s_w, tl, tid);
             __syncthreads();
             double* base = isA ? Apan + (((int64_t)b * nkc + kc) * MP + rb) * KC
                                : Bpan + (((int64_t)b * nkc + kc) * PP + rb) * KC;
