@@ -87,6 +87,7 @@ __device__ __forceinline__ void gen_phase(const DevModel& M, const Tables& T, ui
         // full aligned pair: vector mean loads first, then the generators
         double2 mv[U];
         int jj[U];
+        double v0[U], v1[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             jj[u] = s_j[tq + 4 * u];
@@ -104,8 +105,14 @@ __device__ __forceinline__ void gen_phase(const DevModel& M, const Tables& T, ui
                 a = __dmul_rn(w, a);
                 b = __dmul_rn(w, b);
             }
-            tl[tile_slot(r0, tq + 4 * u)] = jj[u] < 0 ? 0.0 : a;
-            tl[tile_slot(r0 + 1, tq + 4 * u)] = jj[u] < 0 ? 0.0 : b;
+            v0[u] = jj[u] < 0 ? 0.0 : a;
+            v1[u] = jj[u] < 0 ? 0.0 : b;
+        }
+        // chunk columns k and k + 4 share one 16-byte granule: 128-bit stores
+#pragma unroll
+        for (int u = 0; u < U; u += 2) {
+            *reinterpret_cast<double2*>(tl + tile_slot(r0, tq + 4 * u)) = make_double2(v0[u], v0[u + 1]);
+            *reinterpret_cast<double2*>(tl + tile_slot(r0 + 1, tq + 4 * u)) = make_double2(v1[u], v1[u + 1]);
         }
     } else {
         // ragged edge (odd dimension or the last rows of the phase)
@@ -524,6 +531,12 @@ class F64Engine final : public PanelEngine {
             attr = true;
         }
         ws_.partial.ensure((size_t)T_ * Gs_ * (BM * BN) + (size_t)T_ * Gs_);
+        static int gen_occ = [] {
+            int b = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_gen_panels_f64, GEN_THREADS, 0);
+            return b > 0 ? b : 1;
+        }();
+        gen_ctas_ = nsm_ * gen_occ;  // one full wave of the grid-stride generator
     }
     int64_t panel_bytes(int64_t c) const override { return (MP_ + PP_) * nkc(c) * KC * 8; }
     int64_t group_size() const override { return Gs_; }
@@ -533,7 +546,7 @@ class F64Engine final : public PanelEngine {
         double* Apan = static_cast<double*>(panels);
         double* Bpan = Apan + (size_t)nb * k * MP_ * KC;
         Prof p("gen_panels_f64", s);
-        k_gen_panels_f64<<<(int)std::min<int64_t>((int64_t)nb * k, (int64_t)nsm_ * 4), GEN_THREADS, 0, s>>>(
+        k_gen_panels_f64<<<(int)std::min<int64_t>((int64_t)nb * k, (int64_t)gen_ctas_), GEN_THREADS, 0, s>>>(
             M_.dm, seed, tag, ks, nb, c, cc, w_fine, w_coarse, MP_, PP_, k, Apan, Bpan, idx);
         launched();
     }
@@ -561,7 +574,7 @@ class F64Engine final : public PanelEngine {
     static int64_t nkc(int64_t c) { return (c + KC - 1) / KC; }
     const Model& M_;
     Workspace& ws_;
-    int nsm_, T_, Gs_, tiles_n_, smem_;
+    int nsm_, T_, Gs_, tiles_n_, smem_, gen_ctas_;
     int64_t MP_, PP_;
 };
 
