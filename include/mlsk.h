@@ -151,6 +151,19 @@ int mlsk_mc_matmul(const mlsk_model_desc* model, int32_t target, double target_p
                    int64_t L, int64_t N, int64_t M, int64_t c0, uint64_t seed,
                    const mlsk_exec_opts* opts, mlsk_report* report);
 
+/* reference_inner(model, f, count, seed, threads)  models.cpp:140-175 and
+ * reference_matmul(...)  models.cpp:177-227: the MC reference value -- count
+ * full draws keyed (seed, 0, k), the exact product of each (tensor.cpp:97-131,
+ * columns in order, no sampling), f per entry, 64-replication chunk sums.
+ * mean[cells] = sum / count; *std_error = sqrt(max(0, (sq - count*|mean|^2) /
+ * (count - 1)) / count) (0 when count == 1).  Always the exact engine. */
+int mlsk_reference_inner(const mlsk_model_desc* model, int32_t target, double target_param,
+                         int64_t count, uint64_t seed, const mlsk_exec_opts* opts,
+                         double* mean, double* std_error);
+int mlsk_reference_matmul(const mlsk_model_desc* model, int32_t target, double target_param,
+                          int64_t count, uint64_t seed, const mlsk_exec_opts* opts,
+                          double* mean, double* std_error);
+
 /* ---- round API for adaptive MLMC --------------- */
 
 typedef struct mlsk_session mlsk_session;

@@ -115,6 +115,15 @@ def ref_lib():
                                      C.c_int32, _f64p]
         L.ref_time_sketch_matmul.restype = C.c_double
         L.ref_time_sketch_matmul.argtypes = [C.c_int64] * 4 + [C.c_uint64, C.c_int32]
+        L.ref_reference_value.argtypes = [_P(abi.ModelDesc), C.c_int32, C.c_double, C.c_int64, C.c_uint64,
+                                          C.c_int32, _f64p, _f64p]
+        L.ref_make_plan.argtypes = [C.c_double, C.c_int64, C.c_double, C.c_double, C.c_int64, _i64p, _i64p,
+                                    C.c_int64, _P(C.c_int32), _i64p]
+        L.ref_sweep_csv.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, _i64p, C.c_int32, C.c_double, C.c_double,
+                                    C.c_double, C.c_uint64, C.c_int32, C.c_int64, C.c_int32, C.c_char_p,
+                                    C.c_int64]
+        L.ref_estimate_text.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int64, C.c_double, C.c_double,
+                                        C.c_double, C.c_uint64, C.c_int32, C.c_char_p, C.c_int64]
         L.ref_last_error.restype = C.c_char_p
         _ref = L
     return _ref
@@ -314,3 +323,51 @@ def ref_draw(desc, seed, tag, k, c):
     if rc:
         raise ValueError(L.ref_last_error().decode())
     return idx, a, b
+
+
+def ref_reference_value(desc, count, seed, target=abi.TARGET_IDENTITY, tp=1e-12, threads=1):
+    """reference_inner / reference_matmul of the compiled reference: (mean, se)."""
+    L = ref_lib()
+    rows, cols = out_shape(desc)
+    mean = np.zeros(rows * cols)
+    se = np.zeros(1)
+    if L.ref_reference_value(C.byref(desc), target, tp, count, seed, threads, _ptr(mean, _f64p), _ptr(se, _f64p)):
+        raise ValueError(L.ref_last_error().decode())
+    return mean, float(se[0])
+
+
+def ref_make_plan(eps, M, c1, c2, n):
+    """make_plan + plan_N_mc of the compiled reference: (L, N list, n_cap_applied, N_mc)."""
+    L = ref_lib()
+    Lv = np.zeros(1, dtype=np.int64)
+    N = np.zeros(256, dtype=np.int64)
+    cap = C.c_int32(0)
+    nmc = np.zeros(1, dtype=np.int64)
+    if L.ref_make_plan(eps, M, c1, c2, n, _ptr(Lv, _i64p), _ptr(N, _i64p), 256, C.byref(cap), _ptr(nmc, _i64p)):
+        raise ValueError(L.ref_last_error().decode())
+    return int(Lv[0]), [int(x) for x in N[:int(Lv[0]) + 1]], bool(cap.value), int(nmc[0])
+
+
+def _text(fn, *args):
+    cap = 1 << 20
+    while True:
+        buf = C.create_string_buffer(cap)
+        n = fn(*args, buf, cap)
+        if n >= 0:
+            return buf.value.decode()
+        if n == -1:
+            raise ValueError(ref_lib().ref_last_error().decode())
+        cap = -n + 1
+
+
+def ref_sweep_csv(mode, model, target, m_list, eps=0.1, c1=1.0, c2=1.0, seed=1, reps=1, n_ref=100000, threads=1):
+    """The reference CLI's `sweep --no-timing` CSV (mlsketch_main.cpp:112-198)."""
+    ml = np.ascontiguousarray(m_list, dtype=np.int64)
+    return _text(ref_lib().ref_sweep_csv, mode.encode(), model.encode(), target.encode(), _ptr(ml, _i64p), len(ml),
+                 eps, c1, c2, seed, reps, n_ref, threads)
+
+
+def ref_estimate_text(mode, model, target, M=7, eps=0.1, c1=1.0, c2=1.0, seed=1, threads=1):
+    """The reference CLI's `estimate` output (mlsketch_main.cpp:250-316), wall_time_s written as 0.000."""
+    return _text(ref_lib().ref_estimate_text, mode.encode(), model.encode(), target.encode(), M, eps, c1, c2, seed,
+                 threads)

@@ -12,6 +12,8 @@
 // prove the composed loop equals the reference's.  The configs' data models
 // are supplied through the reference's plugin API (models.hpp:17-31).
 #include <chrono>
+#include <cinttypes>
+#include <cstdio>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -26,6 +28,8 @@
 #include "mlsketch/estimators.hpp"
 #include "mlsketch/models.hpp"
 #include "mlsketch/parallel.hpp"
+#include "mlsketch/planner.hpp"
+#include "mlsketch/tensor.hpp"
 #include "mlsketch/rng.hpp"
 #include "mlsketch/sampling.hpp"
 #include "mlsketch/sketch.hpp"
@@ -443,6 +447,190 @@ double ref_time_sketch_matmul(int64_t m, int64_t n, int64_t d, int64_t c, uint64
     const auto t1 = std::chrono::steady_clock::now();
     if (chk == 12345.678) g_err = "unlikely";
     return std::chrono::duration<double>(t1 - t0).count() / reps;
+}
+
+// ---- CLI output restatement (the reference CLI itself cannot be built here:
+// CLI11.hpp is missing).  These compose the reference library's public
+// functions exactly as mlsketch_main.cpp's cmd_sweep (:112-198) and
+// cmd_estimate (:250-316) do and format the same text, to produce golden
+// outputs for the B200 CLI (paper_1904_00429_b200/cli.py).
+
+namespace {
+std::string fmtd(const char* spec, double v) {
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), spec, v);
+    return buf;
+}
+int copy_out(const std::string& text, char* buf, int64_t cap) {
+    if ((int64_t)text.size() + 1 > cap) {
+        g_err = "output buffer too small";
+        return -(int)text.size() - 1;
+    }
+    std::memcpy(buf, text.c_str(), text.size() + 1);
+    return (int)text.size();
+}
+}  // namespace
+
+// reference_inner / reference_matmul (models.cpp:140-227)
+int ref_reference_value(const mlsk_model_desc* d, int32_t tgt, double tp, int64_t count, uint64_t seed,
+                        int32_t threads, double* mean, double* se) {
+    try {
+        if (is_vector(d)) {
+            const auto r = reference_inner(vector_model(d), target(tgt, tp), (std::size_t)count, seed, threads);
+            mean[0] = r.value;
+            *se = r.std_error;
+        } else {
+            const auto r = reference_matmul(matrix_model(d), target(tgt, tp), (std::size_t)count, seed, threads);
+            std::memcpy(mean, r.value.data().data(), sizeof(double) * r.value.rows() * r.value.cols());
+            *se = r.std_error;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// make_plan / plan_N_mc (planner.cpp:83-100); N_out holds up to `cap` levels
+int ref_make_plan(double eps, int64_t M, double c1, double c2, int64_t n, int64_t* L, int64_t* N_out, int64_t cap,
+                  int32_t* n_cap_applied, int64_t* N_mc) {
+    try {
+        const LevelPlan p = make_plan(eps, (std::size_t)M, c1, c2, (std::size_t)n);
+        *L = (int64_t)p.L;
+        for (std::size_t l = 0; l < p.N.size() && (int64_t)l < cap; ++l) N_out[l] = p.N[l];
+        *n_cap_applied = p.n_cap_applied ? 1 : 0;
+        *N_mc = plan_N_mc(eps, c2);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// cmd_sweep (mlsketch_main.cpp:112-198) with --no-timing; returns the CSV length
+int ref_sweep_csv(const char* mode, const char* model_key, const char* target_key, const int64_t* m_list, int32_t nm,
+                  double eps, double c1, double c2, uint64_t seed, int32_t reps, int64_t n_ref, int32_t threads,
+                  char* buf, int64_t cap) {
+    try {
+        const std::string md(mode);
+        auto t = target_by_key(target_key);
+        if (!t) throw std::invalid_argument("unknown target");
+        // plain snprintf (no iostreams: the harness is loaded into processes
+        // that carry their own libstdc++)
+        std::string out = "M,L,M_pow_L,RE_mlmc,time_mlmc_s,cost_units_mlmc,RE_mc,time_mc_s,cost_units_mc,seed\n";
+        const std::uint64_t ref_seed = RngStream::derive_seed(seed, 999983, 0);
+        EstimatorOptions opts;
+        opts.threads = threads;
+        auto row = [&](std::size_t M, std::size_t L, double re1, long long c1u, double re2, long long c2u,
+                       std::uint64_t rs) {
+            char line[512];
+            std::snprintf(line, sizeof(line), "%zu,%zu,%lld,%s,%s,%lld,%s,%s,%lld,%" PRIu64 "\n", M, L, int_pow(M, L),
+                          fmtd("%.6e", re1).c_str(), fmtd("%.3f", 0.0).c_str(), c1u, fmtd("%.6e", re2).c_str(),
+                          fmtd("%.3f", 0.0).c_str(), c2u, rs);
+            out += line;
+        };
+        if (md == "inner") {
+            auto model = vector_model_by_key(model_key);
+            if (!model) throw std::invalid_argument("unknown vector model");
+            const auto ref = reference_inner(*model, *t, (std::size_t)n_ref, ref_seed, threads);
+            for (int32_t i = 0; i < nm; ++i) {
+                const std::size_t M = (std::size_t)m_list[i];
+                const auto plan = make_plan(eps, M, c1, c2, model->n);
+                const long long N_mc = plan_N_mc(eps, c2);
+                for (int rep = 0; rep < reps; ++rep) {
+                    const std::uint64_t rs = RngStream::derive_seed(seed, M, rep);
+                    const auto ml = mlmc_inner(*model, *t, plan, RngStream::derive_seed(rs, 1, 0), opts);
+                    const auto mc = mc_inner(*model, *t, plan.L, N_mc, M, RngStream::derive_seed(rs, 2, 0), opts);
+                    row(M, plan.L, relative_error(ml.value, ref.value), ml.total_cost_units,
+                        relative_error(mc.value, ref.value), mc.total_cost_units, rs);
+                }
+            }
+        } else {
+            auto model = matrix_model_by_key(model_key);
+            if (!model) throw std::invalid_argument("unknown matrix model");
+            const auto ref = reference_matmul(*model, *t, (std::size_t)n_ref, ref_seed, threads);
+            for (int32_t i = 0; i < nm; ++i) {
+                const std::size_t M = (std::size_t)m_list[i];
+                const auto plan = make_plan(eps, M, c1, c2, model->n);
+                const long long N_mc = plan_N_mc(eps, c2);
+                for (int rep = 0; rep < reps; ++rep) {
+                    const std::uint64_t rs = RngStream::derive_seed(seed, M, rep);
+                    const auto ml = mlmc_matmul(*model, *t, plan, RngStream::derive_seed(rs, 1, 0), opts);
+                    const auto mc = mc_matmul(*model, *t, plan.L, N_mc, M, RngStream::derive_seed(rs, 2, 0), opts);
+                    row(M, plan.L, relative_error(ml.value, ref.value), ml.total_cost_units,
+                        relative_error(mc.value, ref.value), mc.total_cost_units, rs);
+                }
+            }
+        }
+        return copy_out(out, buf, cap);
+    } catch (const std::exception& e) {
+        fail(e);
+        return -1;
+    }
+}
+
+// cmd_estimate (mlsketch_main.cpp:250-316); the wall_time_s line is written as 0.000
+int ref_estimate_text(const char* mode, const char* model_key, const char* target_key, int64_t M, double eps,
+                      double c1, double c2, uint64_t seed, int32_t threads, char* buf, int64_t cap) {
+    try {
+        const std::string md(mode);
+        auto t = target_by_key(target_key);
+        if (!t) throw std::invalid_argument("unknown target");
+        EstimatorOptions opts;
+        opts.threads = threads;
+        std::string o;
+        char line[512];
+        std::snprintf(line, sizeof(line), "mode=%s model=%s target=%s\n", mode, model_key, target_key);
+        o += line;
+        if (md == "inner") {
+            auto model = vector_model_by_key(model_key);
+            if (!model) throw std::invalid_argument("unknown vector model");
+            const auto plan = make_plan(eps, (std::size_t)M, c1, c2, model->n);
+            const auto rep = mlmc_inner(*model, *t, plan, seed, opts);
+            std::snprintf(line, sizeof(line), "M=%zu L=%zu epsilon=%g n=%zu%s\n", plan.M, plan.L, plan.epsilon,
+                          model->n, plan.n_cap_applied ? " (depth set by dimension cap)" : "");
+            o += line;
+            o += "level  N          estimate        mean_sq_diff    cost_units\n";
+            for (const auto& st : rep.per_level) {
+                std::snprintf(line, sizeof(line), "%-5zu  %-9lld  %-14.8g  %-14.8g  %lld\n", st.level,
+                              st.replication_count, st.estimate, st.sample_mean_of_squares, st.cost_units);
+                o += line;
+            }
+            std::snprintf(line, sizeof(line), "estimate=%.10g\ntotal_cost_units=%lld\nwall_time_s=%.3f\nseed=%" PRIu64 "\n",
+                          rep.value, rep.total_cost_units, 0.0, rep.seed);
+            o += line;
+        } else {
+            auto model = matrix_model_by_key(model_key);
+            if (!model) throw std::invalid_argument("unknown matrix model");
+            const auto plan = make_plan(eps, (std::size_t)M, c1, c2, model->n);
+            const auto rep = mlmc_matmul(*model, *t, plan, seed, opts);
+            std::snprintf(line, sizeof(line), "M=%zu L=%zu epsilon=%g n=%zu m=%zu d=%zu%s\n", plan.M, plan.L,
+                          plan.epsilon, model->n, model->m, model->d,
+                          plan.n_cap_applied ? " (depth set by dimension cap)" : "");
+            o += line;
+            o += "level  N          frob_estimate   mean_sq_diff    cost_units\n";
+            for (const auto& st : rep.per_level) {
+                std::snprintf(line, sizeof(line), "%-5zu  %-9lld  %-14.8g  %-14.8g  %lld\n", st.level,
+                              st.replication_count, std::sqrt(frobenius_norm_sq(st.estimate)),
+                              st.sample_mean_of_squares, st.cost_units);
+                o += line;
+            }
+            std::snprintf(line, sizeof(line), "estimate (%zux%zu):\n", rep.value.rows(), rep.value.cols());
+            o += line;
+            for (std::size_t i = 1; i <= rep.value.rows(); ++i) {
+                for (std::size_t j = 1; j <= rep.value.cols(); ++j) {
+                    std::snprintf(line, sizeof(line), "%s%.8g", j == 1 ? "  " : " ", rep.value(i, j));
+                    o += line;
+                }
+                o += "\n";
+            }
+            std::snprintf(line, sizeof(line), "total_cost_units=%lld\nwall_time_s=%.3f\nseed=%" PRIu64 "\n",
+                          rep.total_cost_units, 0.0, rep.seed);
+            o += line;
+        }
+        return copy_out(o, buf, cap);
+    } catch (const std::exception& e) {
+        fail(e);
+        return -1;
+    }
 }
 
 }  // extern "C"

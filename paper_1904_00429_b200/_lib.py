@@ -38,6 +38,10 @@ def lib():
           C.c_uint64, _P(abi.ExecOpts), _P(abi.Report)]
     L.mlsk_mc_inner.argtypes = mc
     L.mlsk_mc_matmul.argtypes = mc
+    ref = [_P(abi.ModelDesc), C.c_int32, C.c_double, C.c_int64, C.c_uint64, _P(abi.ExecOpts), _P(C.c_double),
+           _P(C.c_double)]
+    L.mlsk_reference_inner.argtypes = ref
+    L.mlsk_reference_matmul.argtypes = ref
     L.mlsk_session_create.argtypes = [_P(abi.ModelDesc), C.c_int32, C.c_double, C.c_int64, C.c_int64,
                                       C.c_int64, C.c_uint64, _P(abi.ExecOpts), _P(C.c_void_p)]
     L.mlsk_session_run_round.argtypes = [C.c_void_p, _P(C.c_int64)]

@@ -272,6 +272,51 @@ int mc_impl(bool matrix, const mlsk_model_desc* model, int32_t target, double tp
     });
 }
 
+int reference_impl(bool matrix, const mlsk_model_desc* model, int32_t target, double tparam, int64_t count,
+                   uint64_t seed, const mlsk_exec_opts* opts, double* mean, double* se) {
+    return guard([&] {
+        if (count < 1) invalid(matrix ? "reference_matmul: count must be positive"
+                                      : "reference_inner: count must be positive");
+        check_target(target, tparam);
+        if (!model) invalid("model: null descriptor");
+        if (model_is_vector(model) == matrix) invalid("estimator: model kind does not match the estimator");
+        Exec ex(opts);
+        Runner R;
+        R.wsp = &cached_workspace(ex.device);
+        build_model(R.model, model, ex.stream);
+        R.target = target;
+        R.tparam = tparam;
+        R.seed = seed;
+        R.rank = 0;  // every rank computes the whole reference value
+        R.world = 1;
+        R.engine = MLSK_ENGINE_EXACT;
+        const int64_t cells = R.model.rows * R.model.cols;
+        LevelState st;
+        st.init(cells, ex.stream);
+        LevelSpec lv{0, R.model.desc.n, 0};  // key (seed, 0, k), models.cpp:152,193
+        lv.full = true;
+        R.run({{lv, 0, count, &st, nullptr}}, ex.stream, 0);
+        std::vector<double> sum;
+        double sq;
+        read_level(st, ex.stream, sum, sq);
+        const double cnt = (double)count;
+        double mean_sq = 0.0;  // frobenius_norm_sq(mean) (tensor.cpp:141-147); inner: mean * mean
+        std::vector<double> mv(cells);
+        for (int64_t t = 0; t < cells; ++t) {
+            mv[t] = sum[t] / cnt;
+            mean_sq += mv[t] * mv[t];
+        }
+        double err = 0.0;
+        if (count > 1) {
+            const double var = matrix ? std::max(0.0, (sq - cnt * mean_sq) / (double)(count - 1))
+                                      : std::max(0.0, (sq - cnt * mv[0] * mv[0]) / (double)(count - 1));
+            err = std::sqrt(var / cnt);
+        }
+        if (mean) std::memcpy(mean, mv.data(), sizeof(double) * cells);
+        if (se) *se = err;
+    });
+}
+
 }  // namespace
 
 int mlsk::run_guarded(const std::function<void()>& body) { return guard(body); }
@@ -317,6 +362,16 @@ int mlsk_mc_inner(const mlsk_model_desc* model, int32_t target, double tp, int64
 int mlsk_mc_matmul(const mlsk_model_desc* model, int32_t target, double tp, int64_t L, int64_t N, int64_t M,
                    int64_t c0, uint64_t seed, const mlsk_exec_opts* opts, mlsk_report* report) {
     return mc_impl(true, model, target, tp, L, N, M, c0, seed, opts, report);
+}
+
+int mlsk_reference_inner(const mlsk_model_desc* model, int32_t target, double tp, int64_t count, uint64_t seed,
+                         const mlsk_exec_opts* opts, double* mean, double* std_error) {
+    return reference_impl(false, model, target, tp, count, seed, opts, mean, std_error);
+}
+
+int mlsk_reference_matmul(const mlsk_model_desc* model, int32_t target, double tp, int64_t count, uint64_t seed,
+                          const mlsk_exec_opts* opts, double* mean, double* std_error) {
+    return reference_impl(true, model, target, tp, count, seed, opts, mean, std_error);
 }
 
 int mlsk_session_create(const mlsk_model_desc* model, int32_t target, double tp, int64_t M, int64_t c0, int64_t L,

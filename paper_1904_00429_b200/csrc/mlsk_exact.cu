@@ -118,6 +118,13 @@ __global__ void k_indices(DevModel M, uint64_t seed, uint64_t tag, const int64_t
     }
 }
 
+// Reference-value draws use every column in order (no index stream).
+__global__ void k_iota(int nb, int64_t c, uint32_t* __restrict__ idx) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)nb * c;
+         e += (int64_t)gridDim.x * blockDim.x)
+        idx[e] = (uint32_t)(e % c) + 1u;
+}
+
 // Gather of the sampled columns of A (a_cols[b][r][t]) and rows of B
 // (b_rows[b][t][q]) -- the model draw restricted to the sampled indices.
 __global__ void k_gather(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb,
@@ -152,7 +159,7 @@ __global__ void k_gather(DevModel M, uint64_t seed, uint64_t tag, const int64_t*
 
 // v[b][cell] = f(fine) - f(coarse) in the reference's operation order.
 __global__ void k_sketch(int vector, int64_t rows, int64_t cols, int nb, int64_t c, int64_t cc, double w,
-                         double sf, double sc, int target, double tparam,
+                         double vdiv, double sf, double sc, int target, double tparam,
                          const double* __restrict__ a_cols, const double* __restrict__ b_rows,
                          double* __restrict__ v) {
     const int64_t cells = rows * cols, total = (int64_t)nb * cells;
@@ -168,7 +175,7 @@ __global__ void k_sketch(int vector, int64_t rows, int64_t cols, int nb, int64_t
                 sum = __dadd_rn(sum, __dmul_rn(__dmul_rn(a[t], bb[t]), w));
                 if (t + 1 == cc) pre = sum;
             }
-            fine = __ddiv_rn(sum, (double)c);
+            fine = __ddiv_rn(sum, vdiv);
             if (cc > 0) coarse = __ddiv_rn(pre, (double)cc);
         } else {  // sketch.cpp:60-75
             const int64_t r = cell / cols, q = cell - r * cols;
@@ -269,13 +276,17 @@ void exact_run(const RunArgs& a, const LevelSpec& lv, const std::vector<Segment>
     cudaStream_t s = a.stream;
     const int64_t c = lv.c, cells = M.rows * M.cols;
     const bool ref = M.dm.stream == MLSK_STREAM_REF;
-    const int64_t stream_len = ref ? M.ref_u64 + c : 0;
+    const int64_t stream_len = ref ? M.ref_u64 + (lv.full ? 0 : c) : 0;
     // bytes per replication of workspace
     const int64_t per = (ref ? stream_len * 8 : 0) + c * 4 + (M.rows + M.cols) * c * 8 + cells * 8 + 8;
     const int64_t budget = int64_t(1) << 30;
     int64_t max_rep = std::max<int64_t>(1, budget / per);
-    const double w = (double)M.desc.n;  // uniform inv_probs (sampling.cpp:39)
-    const double sf = 1.0 / (double)c;
+    // uniform inv_probs = n (sampling.cpp:39), scaled by 1/s (sketch.cpp:37,73);
+    // the full draw is the plain product: exact_inner / exact_matmul
+    // (tensor.cpp:97-131) -- (a*b)*1 and o*1 are exact, so the same kernel serves
+    const double w = lv.full ? 1.0 : (double)M.desc.n;
+    const double vdiv = lv.full ? 1.0 : (double)c;
+    const double sf = lv.full ? 1.0 : 1.0 / (double)c;
     const double sc = lv.cc > 0 ? 1.0 / (double)lv.cc : 0.0;
 
     size_t i = 0;
@@ -308,11 +319,14 @@ void exact_run(const RunArgs& a, const LevelSpec& lv, const std::vector<Segment>
                 a.seed, lv.tag, ws.ks.p, nb, stream_len, ws.stream.p);
             launched();
         }
-        k_indices<<<grid_for((int64_t)nb * c), 256, 0, s>>>(M.dm, a.seed, lv.tag, ws.ks.p, nb, c, ws.stream.p,
-                                                              stream_len, M.ref_u64, ws.idx.p);
+        if (lv.full)
+            k_iota<<<grid_for((int64_t)nb * c), 256, 0, s>>>(nb, c, ws.idx.p);
+        else
+            k_indices<<<grid_for((int64_t)nb * c), 256, 0, s>>>(M.dm, a.seed, lv.tag, ws.ks.p, nb, c, ws.stream.p,
+                                                                  stream_len, M.ref_u64, ws.idx.p);
         k_gather<<<grid_for((int64_t)nb * (M.rows + M.cols) * c), 256, 0, s>>>(
             M.dm, a.seed, lv.tag, ws.ks.p, nb, c, ws.stream.p, stream_len, ws.idx.p, ws.a_cols.p, ws.b_rows.p);
-        k_sketch<<<grid_for((int64_t)nb * cells), 256, 0, s>>>(M.vector, M.rows, M.cols, nb, c, lv.cc, w, sf, sc,
+        k_sketch<<<grid_for((int64_t)nb * cells), 256, 0, s>>>(M.vector, M.rows, M.cols, nb, c, lv.cc, w, vdiv, sf, sc,
                                                                 a.target, a.target_param, ws.a_cols.p,
                                                                 ws.b_rows.p, ws.v.p);
         launched(3);

@@ -122,6 +122,8 @@ struct LevelSpec {
     uint64_t tag;  // l, or MLSK_TAG_MC for the single-level baseline
     int64_t c;     // fine sample size
     int64_t cc;    // coarse sample size (prefix), 0 at level 0 / MC
+    bool full = false;  // the whole draw, columns 1..n in order, unweighted: the
+                        // reference value (reference_inner/matmul, models.cpp:140-227)
 };
 
 // Per-level accumulator state on the device.

@@ -425,6 +425,48 @@ def mc_matmul(model: MatrixPairModel, f: TargetFunction, L: int, N: int, M: int,
     return _mc(True, model, f, L, N, M, seed, options, c0)
 
 
+@dataclass
+class ScalarReference:  # models.hpp ScalarReference
+    value: float
+    std_error: float
+    count: int
+
+
+@dataclass
+class MatrixReference:  # models.hpp MatrixReference
+    value: np.ndarray
+    std_error: float
+    count: int
+
+
+def _reference(matrix: bool, model, f: TargetFunction, count: int, seed: int, options):
+    options = options or EstimatorOptions()
+    if matrix != isinstance(model, MatrixPairModel):
+        raise ValueError("estimator: model kind does not match the estimator")
+    rows, cols = _shape(model)
+    mean = np.zeros(rows * cols)
+    se = C.c_double(0.0)
+    desc = model.desc()
+    fn = lib().mlsk_reference_matmul if matrix else lib().mlsk_reference_inner
+    check(fn(C.byref(desc), f.kind, f.param, count, seed, C.byref(options._c()), _ptr(mean, _f64p), C.byref(se)))
+    return mean, se.value
+
+
+def reference_inner(model: VectorPairModel, f: TargetFunction, count: int, seed: int,
+                    options: Optional[EstimatorOptions] = None) -> ScalarReference:
+    """MC reference value of E[f(a^T b)] from `count` full draws keyed
+    (seed, 0, k) (models.cpp:140-175), on the device."""
+    mean, se = _reference(False, model, f, count, seed, options)
+    return ScalarReference(float(mean[0]), se, count)
+
+
+def reference_matmul(model: MatrixPairModel, f: TargetFunction, count: int, seed: int,
+                     options: Optional[EstimatorOptions] = None) -> MatrixReference:
+    """MC reference value of E[f(AB)] entrywise (models.cpp:177-227)."""
+    mean, se = _reference(True, model, f, count, seed, options)
+    return MatrixReference(mean.reshape(model.m, model.p), se, count)
+
+
 # -------------------------------------------------------------- sketches
 
 
