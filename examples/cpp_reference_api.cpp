@@ -16,6 +16,10 @@ int main() {
         const auto m = mlmc_matmul(gaussian_mean_matrix_model(256, 4096, 256, 0.5, -1.0, 1.0, 5), target_identity(),
                                    LevelPlan{2, 2, {64, 32, 16}, 32}, 20260823);
         std::printf("config2 value[0] %.6f cost %lld\n", m.value[0], m.total_cost_units);
+        // models.cpp:177-227: MC reference value of the deterministic product [[19, 22], [43, 50]]
+        const auto ref = reference_matmul(deterministic_matrix_model(), target_identity(), 3, 1);
+        std::printf("reference %.1f %.1f %.1f %.1f se %.1f\n", ref.value[0], ref.value[1], ref.value[2],
+                    ref.value[3], ref.std_error);
         return 0;
     } catch (const std::invalid_argument& e) {
         std::printf("invalid_argument: %s\n", e.what());

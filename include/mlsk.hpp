@@ -52,6 +52,15 @@ inline Model constant_ones_model(std::size_t n) {  // models.cpp:54-61
     m.desc.stream_mode = MLSK_STREAM_REF;
     return m;
 }
+inline Model deterministic_matrix_model() {  // models.cpp:88-97: A = [[1,2],[3,4]], B = [[5,6],[7,8]]
+    Model m;
+    m.desc.kind = MLSK_MODEL_DETERMINISTIC;
+    m.desc.m = 2;
+    m.desc.n = 2;
+    m.desc.p = 2;
+    m.desc.stream_mode = MLSK_STREAM_REF;
+    return m;
+}
 inline Model gaussian_mean_matrix_model(std::size_t m_, std::size_t n, std::size_t p, double sd, double lo, double hi,
                                         std::uint64_t data_seed) {  // BASELINE configs 2-3
     Model m;
@@ -176,6 +185,36 @@ inline EstimateReport<double> mlmc_inner(const Model& model, const TargetFunctio
     EstimateReport<double> out{value, {}, r.total_cost_units, r.wall_time_s, r.seed};
     for (std::size_t l = 0; l < levels; ++l) out.per_level.push_back({l, est[l], cnt[l], msq[l], cost[l]});
     return out;
+}
+
+// reference_inner / reference_matmul -- models.hpp:78-100 (threads ignored)
+struct ScalarReference {
+    double value;
+    double std_error;
+    std::size_t sample_count;
+};
+struct MatrixReference {
+    std::vector<double> value;  // row-major rows() x cols()
+    double std_error;
+    std::size_t sample_count;
+};
+
+inline ScalarReference reference_inner(const Model& model, const TargetFunction& f, std::size_t count,
+                                       std::uint64_t seed, const EstimatorOptions& options = {}) {
+    ScalarReference r{0.0, 0.0, count};
+    const mlsk_model_desc d = detail::desc_of(model);
+    const mlsk_exec_opts o = detail::opts_of(options);
+    check(mlsk_reference_inner(&d, f.kind, f.param, (int64_t)count, seed, &o, &r.value, &r.std_error));
+    return r;
+}
+
+inline MatrixReference reference_matmul(const Model& model, const TargetFunction& f, std::size_t count,
+                                        std::uint64_t seed, const EstimatorOptions& options = {}) {
+    MatrixReference r{std::vector<double>(model.rows() * model.cols()), 0.0, count};
+    const mlsk_model_desc d = detail::desc_of(model);
+    const mlsk_exec_opts o = detail::opts_of(options);
+    check(mlsk_reference_matmul(&d, f.kind, f.param, (int64_t)count, seed, &o, r.value.data(), &r.std_error));
+    return r;
 }
 
 }  // namespace mlsketch_b200

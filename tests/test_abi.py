@@ -95,3 +95,4 @@ def test_cpp_wrapper_on_device(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout
     assert r.stdout.startswith("value 37.0 level1 0.0")
+    assert "reference 19.0 22.0 43.0 50.0 se 0.0" in r.stdout
