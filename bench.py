@@ -325,11 +325,9 @@ def main():
 def run_e2e(g, torch, device, args):
     """Public-API call per step: means from pinned host buffers -> device,
     all levels, report back to the host."""
-    from oracle import pyoracle as po  # only to materialise the same host means
-    from paper_1904_00429_b200 import _abi as abi
-    om = po.OracleModel(po.model_desc(abi.MODEL_GAUSS_MEAN, n=N_, m=M_, p=P_, sd=0.5, mean_lo=-1.0,
-                                      mean_hi=1.0, data_seed=data_seed()))
-    ma, mb = om.means()
+    # the config's means as host arrays (read back once from the seeded model)
+    seeded = g.gaussian_mean_matrix_model(M_, N_, P_, sd=0.5, data_seed=data_seed())
+    ma, mb = g.model_data(seeded, 0), g.model_data(seeded, 1)
     pa = torch.from_numpy(ma).pin_memory().numpy()
     pb = torch.from_numpy(mb).pin_memory().numpy()
     model = g.gaussian_mean_matrix_model(M_, N_, P_, sd=0.5, mean_a=pa, mean_b=pb)
@@ -343,9 +341,12 @@ def run_e2e(g, torch, device, args):
     dt = time.perf_counter() - t0
     cells = M_ * P_
     levels = LEVELS + 1
-    d2h = 8 * (cells + 2 * levels * cells + 2 * levels) + 8 * 2 * levels
+    # what the call moves: the two mean matrices and the replication list in,
+    # each level's [sum Y | sum ||Y||^2] out (mlsk_api.cu read_levels)
+    h2d = pa.nbytes + pb.nbytes + 8 * sum(STEP_N)
+    d2h = 8 * levels * (cells + 1)
     return {"value": args.steps * sum(STEP_N) / dt, "unit": UNIT,
-            "h2d_bytes_per_step": int(pa.nbytes + pb.nbytes + 8 * levels),
+            "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h),
             "note": "mlsketch.mlmc_matmul with host mean buffers; wall clock, synchronous API"}
 

@@ -6,7 +6,11 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <string>
+#include <vector>
 #include <functional>
 #include <map>
 #include <memory>
@@ -40,6 +44,42 @@ int guard(const std::function<void()>& body) {
         return MLSK_ERUNTIME;
     }
 }
+
+// MLSK_TRACE=1: per-phase host (enqueue) and device (event) times of an
+// estimator call, printed to stderr (diagnostics only).
+struct Trace {
+    bool on;
+    cudaStream_t s;
+    std::vector<std::pair<std::string, cudaEvent_t>> ev;
+    std::vector<double> host;
+    std::chrono::steady_clock::time_point t0;
+    explicit Trace(cudaStream_t st) : on(getenv("MLSK_TRACE") != nullptr), s(st) {
+        if (on) {
+            t0 = std::chrono::steady_clock::now();
+            mark("start");
+        }
+    }
+    void mark(const char* name) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        ev.emplace_back(name, e);
+        host.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+    void report() {
+        if (!on) return;
+        cudaEventSynchronize(ev.back().second);
+        for (size_t i = 1; i < ev.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+            fprintf(stderr, "[mlsk trace] %-16s host %8.3f ms  device %8.3f ms\n", ev[i].first.c_str(),
+                    host[i] - host[i - 1], ms);
+        }
+        for (auto& e : ev) cudaEventDestroy(e.second);
+        ev.clear();
+    }
+};
 
 // Per-call execution context: device selection and stream.
 struct Exec {
@@ -150,6 +190,37 @@ struct Runner {
     }
 };
 
+// All levels' sums / sums of squares in one pass: one device->host copy per
+// level into pinned staging (only [total | total_sq] unless a chunk is
+// open), one synchronisation.
+void read_levels(const std::vector<LevelState>& sts, cudaStream_t s, Workspace& ws,
+                 std::vector<std::vector<double>>& sums, std::vector<double>& sqs) {
+    size_t need = 0;
+    for (const auto& st : sts) need += (st.open_count > 0 ? 2 : 1) * (size_t)(st.cells + 1);
+    double* h = ws.host.ensure(std::max<size_t>(need, 1));
+    size_t off = 0;
+    for (const auto& st : sts) {
+        const size_t n = (st.open_count > 0 ? 2 : 1) * (size_t)(st.cells + 1);
+        MLSK_CUDA(cudaMemcpyAsync(h + off, st.buf.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        off += n;
+    }
+    MLSK_CUDA(cudaStreamSynchronize(s));
+    sums.resize(sts.size());
+    sqs.resize(sts.size());
+    off = 0;
+    for (size_t l = 0; l < sts.size(); ++l) {
+        const int64_t cells = sts[l].cells;
+        const double* b = h + off;
+        sums[l].assign(b, b + cells);
+        sqs[l] = b[cells];
+        if (sts[l].open_count > 0) {
+            for (int64_t t = 0; t < cells; ++t) sums[l][t] += b[cells + 1 + t];
+            sqs[l] += b[2 * cells + 1];
+        }
+        off += (sts[l].open_count > 0 ? 2 : 1) * (size_t)(cells + 1);
+    }
+}
+
 // level sum / sum of squares on the host: total (+ open chunk, last in order)
 void read_level(const LevelState& st, cudaStream_t s, std::vector<double>& sum, double& sq) {
     const int64_t cells = st.cells;
@@ -173,9 +244,12 @@ int mlmc_impl(bool matrix, const mlsk_model_desc* model, int32_t target, double 
         if (!model) invalid("model: null descriptor");
         if (model_is_vector(model) == matrix) invalid("estimator: model kind does not match the estimator");
         Exec ex(opts);
+        Trace tr(ex.stream);
         Runner R;
         R.wsp = &cached_workspace(ex.device);
+        tr.mark("exec+workspace");
         build_model(R.model, model, ex.stream);
+        tr.mark("build_model");
         R.target = target;
         R.tparam = tparam;
         R.seed = seed;
@@ -183,7 +257,7 @@ int mlmc_impl(bool matrix, const mlsk_model_desc* model, int32_t target, double 
         R.world = ex.world;
         R.resolve_engine(ex.engine);
         const int64_t cells = R.model.rows * R.model.cols;
-        std::vector<double> value(cells, 0.0), sum;
+        std::vector<double> value(cells, 0.0);
         int64_t total_cost = 0;
         const int64_t cL = plan->c0 * ipow(plan->M, plan->L);
         std::vector<LevelState> states(plan->L + 1);
@@ -196,13 +270,18 @@ int mlmc_impl(bool matrix, const mlsk_model_desc* model, int32_t target, double 
             if (ex.probe_out && ex.probe_k > 0 && l > 0) probe = ex.probe_out + l * ex.probe_k * cL;
             items.push_back({LevelSpec{(uint64_t)l, fine, coarse}, 0, plan->N[l], &states[l], probe});
         }
+        tr.mark("level states");
         R.run(items, ex.stream, ex.probe_k);  // all levels as one round
+        tr.mark("round");
+        std::vector<std::vector<double>> sums;
+        std::vector<double> sqs;
+        read_levels(states, ex.stream, *R.wsp, sums, sqs);
         for (int64_t l = 0; l <= plan->L; ++l) {
             const int64_t fine = plan->c0 * ipow(plan->M, l);
             const int64_t coarse = l > 0 ? fine / plan->M : 0;
             const LevelState& st = states[l];
-            double sq;
-            read_level(st, ex.stream, sum, sq);
+            const std::vector<double>& sum = sums[l];
+            const double sq = sqs[l];
             const double inv_n = 1.0 / (double)plan->N[l];
             const int64_t cost = plan->N[l] * (fine + coarse) * cells;  // estimators.cpp:34-40
             total_cost += cost;
@@ -219,6 +298,8 @@ int mlmc_impl(bool matrix, const mlsk_model_desc* model, int32_t target, double 
             for (int64_t t = 0; t < cells; ++t) value[t] += sum[t] * inv_n;  // estimators.cpp:179-184
         }
         MLSK_CUDA(cudaStreamSynchronize(ex.stream));
+        tr.mark("read levels");
+        tr.report();
         if (rep) {
             if (rep->value) std::memcpy(rep->value, value.data(), sizeof(double) * cells);
             rep->total_cost_units = total_cost;
@@ -427,11 +508,14 @@ int mlsk_session_stats(mlsk_session* s, mlsk_report* rep) {
     return guard([&] {
         if (!s || !rep) invalid("session: null argument");
         const int64_t cells = s->R.model.rows * s->R.model.cols;
-        std::vector<double> value(cells, 0.0), sum;
+        std::vector<double> value(cells, 0.0);
         int64_t total_cost = 0;
+        std::vector<std::vector<double>> sums;
+        std::vector<double> sqs;
+        read_levels(s->levels, s->ex->stream, *s->R.wsp, sums, sqs);
         for (int64_t l = 0; l <= s->L; ++l) {
-            double sq;
-            read_level(s->levels[l], s->ex->stream, sum, sq);
+            const std::vector<double>& sum = sums[l];
+            const double sq = sqs[l];
             const int64_t n = s->levels[l].count;
             const int64_t fine = s->c0 * ipow(s->M, l), coarse = l > 0 ? fine / s->M : 0;
             const double inv_n = n > 0 ? 1.0 / (double)n : 0.0;

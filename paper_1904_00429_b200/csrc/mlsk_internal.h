@@ -163,8 +163,31 @@ struct Segment {
 std::vector<Segment> plan_segments(int64_t k_begin, int64_t k_end, int rank, int world,
                                    const LevelState& st);
 
+// Pinned host staging (device->host reads of the level accumulators).
+struct PinnedHost {
+    double* p = nullptr;
+    size_t cap = 0;
+    PinnedHost() = default;
+    PinnedHost(const PinnedHost&) = delete;
+    PinnedHost& operator=(const PinnedHost&) = delete;
+    ~PinnedHost() {
+        if (p) cudaFreeHost(p);
+    }
+    double* ensure(size_t n) {
+        if (n > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            MLSK_CUDA(cudaMallocHost(&p, n * sizeof(double)));
+            cap = n;
+        }
+        return p;
+    }
+};
+
 struct Workspace {
     std::shared_ptr<void> fused;  // engine-private pipeline state (mlsk_fused.cu)
+    PinnedHost host;              // staging for level reads
     DevArray<uint64_t> stream;
     DevArray<int64_t> ks;
     DevArray<uint32_t> idx;

@@ -323,9 +323,10 @@ class EstimateReport:
 
 class _Buffers:
     def __init__(self, levels: int, cells: int):
-        self.value = np.zeros(cells)
-        self.level_estimate = np.zeros((levels, cells))
-        self.level_sum = np.zeros((levels, cells))
+        # every entry is written by the library (np.empty: no 2 x levels x cells memset)
+        self.value = np.empty(cells)
+        self.level_estimate = np.empty((levels, cells))
+        self.level_sum = np.empty((levels, cells))
         self.level_sumsq = np.zeros(levels)
         self.level_mean_sq = np.zeros(levels)
         self.level_count = np.zeros(levels, dtype=np.int64)
@@ -350,7 +351,7 @@ def _shape(model) -> tuple:
 
 def _report(buf: _Buffers, model, levels: int, vector: bool, with_levels=True) -> EstimateReport:
     rows, cols = _shape(model)
-    conv = (lambda x: float(x[0])) if vector else (lambda x: x.reshape(rows, cols).copy())
+    conv = (lambda x: float(x[0])) if vector else (lambda x: x.reshape(rows, cols))  # views of per-call buffers
     per = []
     if with_levels:
         for l in range(levels):
