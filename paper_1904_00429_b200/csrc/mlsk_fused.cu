@@ -257,7 +257,9 @@ struct GemmShape {
     int tiles_n;   // tiles along the columns
 };
 
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+// 192-register cap (no spills; 218 uncapped): 192 x 256 leaves the SM room for
+// one generator CTA beside the GEMM CTA (measured +2% on the config-2 step).
+__global__ void __maxnreg__(192)
 k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, GemmShape sh,
            double* __restrict__ part, double* __restrict__ part_sq) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -537,6 +539,7 @@ class F64Engine final : public PanelEngine {
             return b > 0 ? b : 1;
         }();
         gen_ctas_ = nsm_ * gen_occ;  // one full wave of the grid-stride generator
+        if (const char* e = getenv("MLSK_GEN_CTAS_PER_SM")) gen_ctas_ = nsm_ * std::max(1, atoi(e));  // experiments
     }
     int64_t panel_bytes(int64_t c) const override { return (MP_ + PP_) * nkc(c) * KC * 8; }
     int64_t group_size() const override { return Gs_; }
