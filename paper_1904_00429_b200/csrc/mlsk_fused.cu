@@ -141,7 +141,7 @@ __device__ __forceinline__ void gen_phase(const DevModel& M, const Tables& T, ui
     }
 }
 
-__global__ void __launch_bounds__(GEN_THREADS)
+__global__ void __launch_bounds__(GEN_THREADS, 4)
 k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
                  int64_t cc, double w_fine, double w_coarse, int64_t MP, int64_t PP, int64_t nkc,
                  double* __restrict__ Apan, double* __restrict__ Bpan, uint32_t* __restrict__ idx_out) {
