@@ -58,6 +58,12 @@ __device__ __forceinline__ void load_tables(double2* s_sc, double2* s_lg, const 
     for (int i = threadIdx.x; i < 128; i += blockDim.x) s_lg[i] = reinterpret_cast<const double2*>(T.log_d)[i];
 }
 
+// full-circle (1024-entry) sincos table, see sincos_iv_full
+__device__ __forceinline__ void load_tables_full(double2* s_sc1024, double2* s_lg, const Tables& T) {
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_sc1024[i] = full_circle_entry(i, T.sincos_d);
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) s_lg[i] = reinterpret_cast<const double2*>(T.log_d)[i];
+}
+
 // --------------------------------------------------------- panel generator
 
 // grid-stride over work items (b, kc); each item produces the A chunk
@@ -66,6 +72,7 @@ __device__ __forceinline__ void load_tables(double2* s_sc, double2* s_lg, const 
 // phase (row pairs share one Philox block) while the previous phase's tile is
 // streamed out with coalesced 16-byte stores.
 constexpr int GROWS = 128;
+constexpr int GEN_DYN_SMEM = 2 * GROWS * KC * 8;  // the two staging tiles
 
 // One phase: 128 rows of A (IS_A) or 128 columns of B, 16 sampled columns.
 // Thread (rp = tid % 64, tq = tid / 64) owns row pair rp of chunk columns
@@ -97,7 +104,7 @@ __device__ __forceinline__ void gen_phase(const DevModel& M, const Tables& T, ui
         for (int u = 0; u < U; ++u) {
             const u32x4 r = philox((uint32_t)jj[u], rowpair, 0, IS_A ? MLSK_CTR_A : MLSK_CTR_B, key);
             double z0, z1;
-            box_muller(lo64(r), hi64(r), z0, z1, T);
+            box_muller<true>(lo64(r), hi64(r), z0, z1, T);
             double a = __dadd_rn(mv[u].x, __dmul_rn(sd, z0));
             double b = __dadd_rn(mv[u].y, __dmul_rn(sd, z1));
             if (!IS_A) {
@@ -126,7 +133,7 @@ __device__ __forceinline__ void gen_phase(const DevModel& M, const Tables& T, ui
                 const double m0 = __ldg(mp), m1 = pair ? __ldg(mp + 1) : 0.0;
                 const u32x4 r = philox((uint32_t)j, rowpair, 0, IS_A ? MLSK_CTR_A : MLSK_CTR_B, key);
                 double z0, z1;
-                box_muller(lo64(r), hi64(r), z0, z1, T);
+                box_muller<true>(lo64(r), hi64(r), z0, z1, T);
                 a = __dadd_rn(m0, __dmul_rn(sd, z0));
                 if (pair) b = __dadd_rn(m1, __dmul_rn(sd, z1));
                 if (!IS_A) {
@@ -145,12 +152,13 @@ __global__ void __launch_bounds__(GEN_THREADS, 4)
 k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
                  int64_t cc, double w_fine, double w_coarse, int64_t MP, int64_t PP, int64_t nkc,
                  double* __restrict__ Apan, double* __restrict__ Bpan, uint32_t* __restrict__ idx_out) {
-    __shared__ __align__(16) double2 s_sc[256];
+    __shared__ __align__(16) double2 s_sc[1024];
     __shared__ __align__(16) double2 s_lg[128];
-    __shared__ __align__(16) double tile[2][GROWS * KC];
+    extern __shared__ __align__(16) double gen_dyn[];  // 2 x GROWS x KC tiles (past the 48 KB static limit)
+    double* const tile[2] = {gen_dyn, gen_dyn + GROWS * KC};
     __shared__ int s_j[KC];
     __shared__ double s_w[KC];
-    load_tables(s_sc, s_lg, M.tab);
+    load_tables_full(s_sc, s_lg, M.tab);
     Tables T = M.tab;
     T.sincos_d = reinterpret_cast<const double*>(s_sc);
     T.log_d = reinterpret_cast<const double*>(s_lg);
@@ -534,8 +542,10 @@ class F64Engine final : public PanelEngine {
         }
         ws_.partial.ensure((size_t)T_ * Gs_ * (BM * BN) + (size_t)T_ * Gs_);
         static int gen_occ = [] {
+            MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_f64, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           GEN_DYN_SMEM));
             int b = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_gen_panels_f64, GEN_THREADS, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_gen_panels_f64, GEN_THREADS, GEN_DYN_SMEM);
             return b > 0 ? b : 1;
         }();
         gen_ctas_ = nsm_ * gen_occ;  // one full wave of the grid-stride generator
@@ -549,7 +559,7 @@ class F64Engine final : public PanelEngine {
         double* Apan = static_cast<double*>(panels);
         double* Bpan = Apan + (size_t)nb * k * MP_ * KC;
         Prof p("gen_panels_f64", s);
-        k_gen_panels_f64<<<(int)std::min<int64_t>((int64_t)nb * k, (int64_t)gen_ctas_), GEN_THREADS, 0, s>>>(
+        k_gen_panels_f64<<<(int)std::min<int64_t>((int64_t)nb * k, (int64_t)gen_ctas_), GEN_THREADS, GEN_DYN_SMEM, s>>>(
             M_.dm, seed, tag, ks, nb, c, cc, w_fine, w_coarse, MP_, PP_, k, Apan, Bpan, idx);
         launched();
     }
