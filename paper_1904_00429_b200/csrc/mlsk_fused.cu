@@ -112,8 +112,10 @@ __device__ __forceinline__ void gen_phase(const DevModel& M, const Tables& T, ui
                 a = __dmul_rn(w, a);
                 b = __dmul_rn(w, b);
             }
-            v0[u] = jj[u] < 0 ? 0.0 : a;
-            v1[u] = jj[u] < 0 ? 0.0 : b;
+            // padding columns (j < 0, only when KC does not divide c): A holds a
+            // finite draw of column 0, B is 0 * x = 0 (s_w = 0), so the product is 0
+            v0[u] = a;
+            v1[u] = b;
         }
         // chunk columns k and k + 4 share one 16-byte granule: 128-bit stores
 #pragma unroll
