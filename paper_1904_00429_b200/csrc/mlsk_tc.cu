@@ -12,14 +12,18 @@
 //                     (gauss f32, Student-t or random-Fourier features,
 //                     generated on the fly), written as hi / lo K-chunks in the
 //                     UMMA canonical K-major SWIZZLE_128B layout.
-//  k_gemm_tf32x3      persistent CTAs, one 128 x 128 output tile per CTA over a
+//  k_gemm_tf32x3      persistent CTAs, one 128 x 256 output tile per CTA over a
 //                     strided set of samples.  warp 0: cp.async.bulk producer
-//                     (3-stage mbarrier ring, 64 KB per stage); warp 1: TMEM
-//                     allocation + single-thread tcgen05.mma issue into two
-//                     128-column TMEM accumulators (double-buffered across
-//                     samples); warps 2-5: epilogue (tcgen05.ld, Y^2 into fp64,
-//                     running sum in 128 registers per thread, flushed to an
-//                     fp64 per-CTA partial every 32 samples).
+//                     (2-stage mbarrier ring, 96 KB per stage); warp 1: TMEM
+//                     allocation + single-thread tcgen05.mma (M128 N256 K8)
+//                     issue into two 256-column TMEM accumulators (all 512
+//                     columns, double-buffered across samples); warps 2-9:
+//                     epilogue, two warps per TMEM lane quadrant taking 128
+//                     columns each (tcgen05.ld, Y^2 into fp64, running sum in
+//                     128 registers per thread, flushed to an fp64 per-CTA
+//                     partial every 32 samples).  N = 256 cuts the operand
+//                     bytes per flop that cross L2 -> SMEM by a quarter vs
+//                     128 x 128 tiles.
 #include <algorithm>
 #include <cstring>
 
@@ -29,13 +33,16 @@ namespace mlsk {
 
 namespace {
 
-constexpr int TBM = 128, TBN = 128, TBK = 32;       // TBK tf32 = 128 bytes per row
-constexpr int TSTAGES = 3;
-constexpr int TTILE = TBM * TBK * 4;                // 16 KB
-constexpr int TSTAGE_BYTES = 4 * TTILE;             // A_hi, A_lo, B_hi, B_lo
-constexpr int TC_THREADS = 192;                     // producer, MMA, 4 epilogue warps
+constexpr int TBM = 128, TBN = 256, TBK = 16;       // TBK tf32 = 64 bytes per row (SWIZZLE_64B)
+constexpr int ROWB = TBK * 4;                       // bytes per K-chunk row
+constexpr int TSTAGES = 4;
+constexpr int TTILE = TBM * TBK * 4;                // 8 KB: one 128-row K-chunk (A tile, half a B tile)
+constexpr int TA_BYTES = TTILE, TB_BYTES = 2 * TTILE;
+constexpr int TSTAGE_BYTES = 2 * TA_BYTES + 2 * TB_BYTES;  // A_hi, A_lo, B_hi, B_lo: 48 KB
+constexpr int EPI_WARPS = 16;                       // four per TMEM lane quadrant (64-column quarters)
+constexpr int TC_THREADS = 64 + 32 * EPI_WARPS;     // producer, MMA, epilogue warps
 constexpr int FLUSH = 32;                           // samples per fp32 running-sum flush
-constexpr uint32_t TMEM_COLS = 2 * TBN;             // two accumulators
+constexpr uint32_t TMEM_COLS = 2 * TBN;             // two accumulators: all 512 columns
 constexpr int GEN_T = 256;
 
 // ----------------------------------------------------------------- PTX
@@ -99,14 +106,28 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// UMMA shared-memory descriptor, K-major, SWIZZLE_128B: 8-row groups 1024 B
-// apart (SBO), version 1 (sm_100), layout type 2.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+// 32 lanes x 16 consecutive 32-bit columns
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_64B (ROWB = 64) or
+// SWIZZLE_128B (ROWB = 128): 8-row groups 8 * ROWB bytes apart (SBO), version
+// 1 (sm_100), layout type 4 / 2.
+__device__ __forceinline__ uint64_t sw_desc(uint32_t saddr) {
     uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
-    d |= (uint64_t)1 << 16;              // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;    // SBO
-    d |= (uint64_t)1 << 46;              // descriptor version (sm_100)
-    d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+    d |= (uint64_t)1 << 16;                  // LBO (unused for swizzled K-major)
+    d |= (uint64_t)((8 * ROWB) >> 4) << 32;  // SBO
+    d |= (uint64_t)1 << 46;                  // descriptor version (sm_100)
+    d |= (uint64_t)(ROWB == 128 ? 2 : 4) << 61;
     return d;
 }
 
@@ -115,9 +136,10 @@ __host__ __device__ constexpr uint32_t tf32_idesc(int M, int N) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-// byte offset of element (r, k) in a 128-row x 32-tf32 SW128 K-major tile
-__device__ __forceinline__ int sw128_off(int r, int k) {
-    return r * 128 + ((((k >> 2) ^ (r & 7)) << 4) | ((k & 3) << 2));
+// byte offset of element (r, k) in a 128-row x TBK-tf32 swizzled K-major tile:
+// the 16-byte chunk index XOR address bits [7, 7 + log2(ROWB / 16))
+__device__ __forceinline__ int sw_off(int r, int k) {
+    return r * ROWB + ((((k >> 2) ^ ((r * ROWB >> 7) & (ROWB / 16 - 1))) << 4) | ((k & 3) << 2));
 }
 
 // ---------------------------------------------------------------- entries
@@ -178,7 +200,7 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
     T.log_f = reinterpret_cast<const float*>(s_lg);
     const int tid = threadIdx.x;
     const int64_t items = (int64_t)nb * nkc;
-    const int a_ph = (int)(MP / TBM), b_ph = (int)(PP / TBN);
+    const int a_ph = (int)(MP / TBM), b_ph = (int)(PP / TBM);  // 128-row phases (a B tile is two)
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const int b = (int)(it / nkc);
         const int64_t kc = it - (int64_t)b * nkc;
@@ -241,8 +263,8 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                     }
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        *reinterpret_cast<float*>(thi + sw128_off(r0 + e, tt)) = v[e];
-                        *reinterpret_cast<float*>(tlo + sw128_off(r0 + e, tt)) = tf32_lo(v[e]);
+                        *reinterpret_cast<float*>(thi + sw_off(r0 + e, tt)) = v[e];
+                        *reinterpret_cast<float*>(tlo + sw_off(r0 + e, tt)) = tf32_lo(v[e]);
                     }
                 }
             } else {
@@ -256,8 +278,8 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                         else x = rff_entry(M, j, rb + rr);  // RFF: B = A^T
                         v = isA ? x : __fmul_rn(s_w[tt], x);
                     }
-                    *reinterpret_cast<float*>(thi + sw128_off(rr, tt)) = v;
-                    *reinterpret_cast<float*>(tlo + sw128_off(rr, tt)) = tf32_lo(v);
+                    *reinterpret_cast<float*>(thi + sw_off(rr, tt)) = v;
+                    *reinterpret_cast<float*>(tlo + sw_off(rr, tt)) = tf32_lo(v);
                 }
             }
             __syncthreads();
@@ -281,30 +303,33 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
 // The 128 x 32 dot products of a row block run from shared memory (X tile
 // transposed for conflict-free reads, W columns broadcast).
 constexpr int RFF_DMAX = 64;
+constexpr int RFF_COLS = 32;               // sampled columns per work item (X tile reuse)
+constexpr int RFF_CH = RFF_COLS / TBK;     // K-chunk tiles per work item
 
 __global__ void __launch_bounds__(GEN_T)
 k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
-                 int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t nkc, float* __restrict__ Ahi,
+                 int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc, float* __restrict__ Ahi,
                  float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
                  uint32_t* __restrict__ idx_out) {
     extern __shared__ __align__(1024) unsigned char rsm[];
-    unsigned char* tiles = rsm;                                      // 4 x 16 KB: A hi, A lo, B hi, B lo
-    float* xs = reinterpret_cast<float*>(rsm + 4 * TTILE);           // [D][128]
-    float* wsm = xs + RFF_DMAX * TBM;                                // [D][32]
-    __shared__ int s_j[TBK];
-    __shared__ float s_w[TBK], s_b[TBK];
+    unsigned char* tiles = rsm;                                      // [q][ch] K-chunk tiles, q = A hi, A lo, B hi, B lo
+    float* xs = reinterpret_cast<float*>(rsm + 4 * RFF_CH * TTILE);  // [D][128]
+    float* wsm = xs + RFF_DMAX * TBM;                                // [D][RFF_COLS]
+    __shared__ int s_j[RFF_COLS];
+    __shared__ float s_w[RFF_COLS], s_b[RFF_COLS];
     const DevModel& M = S.M;
     const int D = (int)M.rff_dim;
     const int tid = threadIdx.x;
     const float scale = (float)M.rff_scale;
-    const int64_t items = (int64_t)nb * nkc;
+    const int64_t ngrp = (nkc + RFF_CH - 1) / RFF_CH;  // column groups of RFF_CH K-chunks
+    const int64_t items = (int64_t)nb * ngrp;
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int b = (int)(it / nkc);
-        const int64_t kc = it - (int64_t)b * nkc;
+        const int b = (int)(it / ngrp);
+        const int64_t kc0 = (it - (int64_t)b * ngrp) * RFF_CH;
         const uint64_t key = derive_seed(seed, tag, (uint64_t)ks[b]);
         __syncthreads();
-        if (tid < TBK) {
-            const int64_t t = kc * TBK + tid;
+        if (tid < RFF_COLS) {
+            const int64_t t = kc0 * TBK + tid;
             int j = -1;
             float w = 0.f;
             if (t < c) {
@@ -319,51 +344,59 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
             s_b[tid] = j >= 0 ? M.rff_b[j] : 0.f;
         }
         __syncthreads();
-        for (int e = tid; e < D * TBK; e += GEN_T) {
-            const int d = e / TBK, t = e - d * TBK;
+        for (int e = tid; e < D * RFF_COLS; e += GEN_T) {
+            const int d = e / RFF_COLS, t = e - d * RFF_COLS;
             const int j = s_j[t];
-            wsm[d * TBK + t] = j >= 0 ? M.rff_w[(int64_t)d * M.n + j] : 0.f;
+            wsm[d * RFF_COLS + t] = j >= 0 ? M.rff_w[(int64_t)d * M.n + j] : 0.f;
         }
-        for (int64_t rb = 0; rb < MP; rb += TBM) {
+        for (int64_t rb = 0; rb < (MP > PP ? MP : PP); rb += TBM) {  // A rows / B columns (m == p)
             const int64_t lim = M.m - rb;
             for (int e = tid; e < TBM * D; e += GEN_T) {
                 const int r = e / D, d = e - r * D;
                 xs[d * TBM + r] = r < lim ? M.rff_x[(rb + r) * D + d] : 0.f;
             }
             __syncthreads();
-            // lane = column t (W reads conflict-free, stores conflict-free), warp = 16 rows
-            // (X reads broadcast)
-            const int t = tid & (TBK - 1), r0 = (tid >> 5) * 16;
-            float acc[16];
+            // lane = column t (W reads conflict-free), warp = RPT consecutive rows (X reads broadcast)
+            constexpr int RPT = TBM * RFF_COLS / GEN_T;
+            const int t = tid % RFF_COLS, r0 = (tid / RFF_COLS) * RPT;
+            float acc[RPT];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+            for (int i = 0; i < RPT; ++i) acc[i] = 0.f;
             for (int d = 0; d < D; ++d) {
-                const float w = wsm[d * TBK + t];
+                const float w = wsm[d * RFF_COLS + t];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) acc[i] = __fmaf_rn(xs[d * TBM + r0 + i], w, acc[i]);
+                for (int i = 0; i < RPT; ++i) acc[i] = __fmaf_rn(xs[d * TBM + r0 + i], w, acc[i]);
             }
             const bool valid = s_j[t] >= 0;
             const float bt = s_b[t], wt = s_w[t];
+            const int ch = t / TBK, tt = t % TBK;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
+            for (int i = 0; i < RPT; ++i) {
                 const int r = r0 + i;
                 float z = 0.f;
                 if (valid && r < lim) z = scale * cosf(acc[i] + bt);
                 const float v = __fmul_rn(wt, z);
-                const int off = sw128_off(r, t);
+                const int off = ch * TTILE + sw_off(r, tt);
                 *reinterpret_cast<float*>(tiles + off) = z;
-                *reinterpret_cast<float*>(tiles + TTILE + off) = tf32_lo(z);
-                *reinterpret_cast<float*>(tiles + 2 * TTILE + off) = v;
-                *reinterpret_cast<float*>(tiles + 3 * TTILE + off) = tf32_lo(v);
+                *reinterpret_cast<float*>(tiles + RFF_CH * TTILE + off) = tf32_lo(z);
+                *reinterpret_cast<float*>(tiles + 2 * RFF_CH * TTILE + off) = v;
+                *reinterpret_cast<float*>(tiles + 3 * RFF_CH * TTILE + off) = tf32_lo(v);
             }
             __syncthreads();
-            const int64_t o = (((int64_t)b * nkc + kc) * MP + rb) * TBK;  // PP == MP for RFF
-            float* dst[4] = {Ahi + o, Alo + o, Bhi + o, Blo + o};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                float4* dq = reinterpret_cast<float4*>(dst[q]);
-                const float4* sq = reinterpret_cast<const float4*>(tiles + q * TTILE);
-                for (int i = tid; i < TTILE / 16; i += GEN_T) dq[i] = sq[i];
+            for (int ch2 = 0; ch2 < RFF_CH; ++ch2) {
+                const int64_t kc = kc0 + ch2;
+                if (kc >= nkc) break;
+                const int64_t oa = (((int64_t)b * nkc + kc) * MP + rb) * TBK;
+                const int64_t ob = (((int64_t)b * nkc + kc) * PP + rb) * TBK;  // B panels are padded to 256
+                float* dst[4] = {Ahi + oa, Alo + oa, Bhi + ob, Blo + ob};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if ((q < 2 ? MP : PP) <= rb) continue;
+                    float4* dq = reinterpret_cast<float4*>(dst[q]);
+                    const float4* sq = reinterpret_cast<const float4*>(tiles + (q * RFF_CH + ch2) * TTILE);
+                    for (int i = tid; i < TTILE / 16; i += GEN_T) dq[i] = sq[i];
+                }
             }
             __syncthreads();
         }
@@ -387,7 +420,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
     unsigned char* ring = dsm + ((1024 - (smem_addr(dsm) & 1023)) & 1023);
     __shared__ __align__(8) uint64_t bars[2 * TSTAGES + 4];  // full, empty, tmem_full[2], tmem_empty[2]
     __shared__ uint32_t s_tmem;
-    __shared__ double s_sq[4];
+    __shared__ double s_sq[EPI_WARPS];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = blockIdx.x;
@@ -405,7 +438,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
         }
         for (int a = 0; a < 2; ++a) {
             bar_init(tfull0 + 8 * a, 1);
-            bar_init(tempty0 + 8 * a, 4);
+            bar_init(tempty0 + 8 * a, EPI_WARPS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -432,10 +465,10 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 const int64_t oa = ((b * sh.nkc + kc) * sh.MP + (int64_t)tm * TBM) * TBK;
                 const int64_t ob = ((b * sh.nkc + kc) * sh.PP + (int64_t)tn * TBN) * TBK;
                 const uint32_t st = smem_addr(ring + s * TSTAGE_BYTES);
-                bulk_load(st, Ahi + oa, TTILE, full);
-                bulk_load(st + TTILE, Alo + oa, TTILE, full);
-                bulk_load(st + 2 * TTILE, Bhi + ob, TTILE, full);
-                bulk_load(st + 3 * TTILE, Blo + ob, TTILE, full);
+                bulk_load(st, Ahi + oa, TA_BYTES, full);
+                bulk_load(st + TA_BYTES, Alo + oa, TA_BYTES, full);
+                bulk_load(st + 2 * TA_BYTES, Bhi + ob, TB_BYTES, full);
+                bulk_load(st + 2 * TA_BYTES + TB_BYTES, Blo + ob, TB_BYTES, full);
                 if (++s == TSTAGES) { s = 0; ph ^= 1; }
                 if (++kc == sh.nkc) { kc = 0; b += sh.Gs; }
             }
@@ -448,10 +481,10 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             uint32_t ph = 0;
             int64_t kc = 0;
             int abuf = 0;
-            uint32_t aph[2] = {0, 0};
+            uint32_t aph = 0;  // bit a = phase of accumulator a (no indexed local array)
             for (int64_t it = 0; it < iters; ++it) {
                 if (kc == 0) {
-                    bar_wait(tempty0 + 8 * abuf, aph[abuf] ^ 1);  // epilogue released this accumulator
+                    bar_wait(tempty0 + 8 * abuf, ((aph >> abuf) & 1u) ^ 1u);  // epilogue released this accumulator
                     tc_fence_after();
                 }
                 bar_wait(full0 + 8 * s, ph);
@@ -460,8 +493,9 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 const uint32_t dcol = tmem + (uint32_t)abuf * TBN;
 #pragma unroll
                 for (int kk = 0; kk < TBK / 8; ++kk) {
-                    const uint64_t ah = sw128_desc(st + kk * 32), al = sw128_desc(st + TTILE + kk * 32);
-                    const uint64_t bh = sw128_desc(st + 2 * TTILE + kk * 32), bl = sw128_desc(st + 3 * TTILE + kk * 32);
+                    const uint64_t ah = sw_desc(st + kk * 32), al = sw_desc(st + TA_BYTES + kk * 32);
+                    const uint64_t bh = sw_desc(st + 2 * TA_BYTES + kk * 32);
+                    const uint64_t bl = sw_desc(st + 2 * TA_BYTES + TB_BYTES + kk * 32);
                     tc_mma_tf32(dcol, ah, bh, idesc, (kc > 0 || kk > 0) ? 1u : 0u);
                     tc_mma_tf32(dcol, ah, bl, idesc, 1u);
                     tc_mma_tf32(dcol, al, bh, idesc, 1u);
@@ -471,56 +505,70 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 if (++kc == sh.nkc) {
                     kc = 0;
                     tc_commit(tfull0 + 8 * abuf);  // accumulator complete
-                    aph[abuf] ^= 1;
+                    aph ^= 1u << abuf;
                     abuf ^= 1;
                 }
             }
         }
     } else {
         // --------------------------------------------------- epilogue
-        const int q = warp & 3;               // TMEM lane quadrant of this warp
-        const int row = q * 32 + lane;        // tile row owned by this thread
-        float S[TBN];
+        const int ew = warp - 2;               // 0 .. EPI_WARPS-1
+        const int q = warp & 3;                // TMEM lane quadrant of this warp
+        const int h = ew >> 2;                 // column quarter
+        const int row = q * 32 + lane;         // tile row owned by this thread
+        constexpr int HC = TBN / (EPI_WARPS / 4);  // columns per epilogue warp
+        float S[HC];
 #pragma unroll
-        for (int i = 0; i < TBN; ++i) S[i] = 0.f;
+        for (int i = 0; i < HC; ++i) S[i] = 0.f;
         double sq = 0.0;
-        double* out = part + (int64_t)g * (TBM * TBN) + (int64_t)row * TBN;
+        double* out = part + (int64_t)g * (TBM * TBN) + (int64_t)row * TBN + h * HC;
         int abuf = 0;
-        uint32_t aph[2] = {0, 0};
+        uint32_t aph = 0;  // bit a = phase of accumulator a (no indexed local array)
         for (int smp = 0; smp < my_samples; ++smp) {
-            bar_wait(tfull0 + 8 * abuf, aph[abuf]);
+            bar_wait(tfull0 + 8 * abuf, (aph >> abuf) & 1u);
             tc_fence_after();
             float ssq = 0.f;
 #pragma unroll
-            for (int ch = 0; ch < TBN / 32; ++ch) {
-                float y[32];
-                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * TBN + ch * 32), y);
+            for (int ch = 0; ch < HC / 16; ++ch) {
+                float y[16];
+                tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * TBN + h * HC + ch * 16), y);
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
+                for (int i = 0; i < 16; ++i) {
                     ssq = __fmaf_rn(y[i], y[i], ssq);
-                    S[ch * 32 + i] = __fadd_rn(S[ch * 32 + i], y[i]);
+                    S[ch * 16 + i] = __fadd_rn(S[ch * 16 + i], y[i]);
                 }
             }
             sq += (double)ssq;
             tc_fence_before();
             __syncwarp();
             if (lane == 0) bar_arrive(tempty0 + 8 * abuf);
-            aph[abuf] ^= 1;
+            aph ^= 1u << abuf;
             abuf ^= 1;
             if ((smp + 1) % FLUSH == 0 || smp + 1 == my_samples) {
 #pragma unroll
-                for (int i = 0; i < TBN; ++i) {
-                    out[i] += (double)S[i];
-                    S[i] = 0.f;
+                for (int i0 = 0; i0 < HC; i0 += 8) {
+                    double o[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) o[i] = out[i0 + i];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        out[i0 + i] = o[i] + (double)S[i0 + i];
+                        S[i0 + i] = 0.f;
+                    }
+                    asm volatile("" ::: "memory");  // bound the live doubles: 8 at a time
                 }
             }
         }
         sq = warp_sum(sq);
-        if (lane == 0) s_sq[q] = sq;
+        if (lane == 0) s_sq[ew] = sq;
     }
     tc_fence_before();
     __syncthreads();
-    if (threadIdx.x == 0) part_sq[g] = (s_sq[0] + s_sq[1]) + (s_sq[2] + s_sq[3]);
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < EPI_WARPS; ++w) t += s_sq[w];
+        part_sq[g] = t;
+    }
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
@@ -584,7 +632,7 @@ class TcEngine final : public PanelEngine {
             attr = true;
         }
         ws_.partial.ensure((size_t)T_ * Gs_ * (TBM * TBN) + (size_t)T_ * Gs_);
-        rff_smem_ = 4 * TTILE + (RFF_DMAX * TBM + RFF_DMAX * TBK) * 4;
+        rff_smem_ = 4 * RFF_CH * TTILE + (RFF_DMAX * TBM + RFF_DMAX * RFF_COLS) * 4;
         static bool rattr = false;
         if (!rattr) {
             MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_rff, cudaFuncAttributeMaxDynamicSharedMemorySize, rff_smem_));
@@ -600,8 +648,9 @@ class TcEngine final : public PanelEngine {
         const int64_t k = nkc(c);
         Prof p("gen_panels_tf32", s);
         if (M_.dm.kind == MLSK_MODEL_RFF && M_.dm.rff_dim <= RFF_DMAX) {
-            k_gen_panels_rff<<<(int)std::min<int64_t>((int64_t)nb * k, (int64_t)nsm_ * 4), GEN_T, rff_smem_, s>>>(
-                S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, k, Ahi, Alo, Bhi, Blo, idx);
+            k_gen_panels_rff<<<(int)std::min<int64_t>((int64_t)nb * ((k + RFF_CH - 1) / RFF_CH), (int64_t)nsm_ * 4),
+                               GEN_T, rff_smem_, s>>>(
+                S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, Ahi, Alo, Bhi, Blo, idx);
         } else {
             k_gen_panels_tf32<<<(int)std::min<int64_t>((int64_t)nb * k, (int64_t)nsm_ * 8), GEN_T, 0, s>>>(
                 S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, Ahi, Alo, Bhi, Blo, idx);
