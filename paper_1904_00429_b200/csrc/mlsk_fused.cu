@@ -97,23 +97,25 @@ __device__ __forceinline__ void gen_phase(const DevModel& M, const Tables& T, ui
         double v0[U], v1[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            jj[u] = s_j[tq + 4 * u];
-            mv[u] = __ldg(reinterpret_cast<const double2*>(mrow + (int64_t)(jj[u] < 0 ? 0 : jj[u]) * dim));
+            jj[u] = s_j[tq + 4 * u];  // padding columns carry j = 0 (and B weight 0)
+            mv[u] = __ldg(reinterpret_cast<const double2*>(mrow + (int64_t)jj[u] * dim));
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+            // one Philox block per chain, interleaved by the scheduler with the
+            // previous chain's fp64 Box-Muller (integer and fp64 pipes overlap)
             const u32x4 r = philox((uint32_t)jj[u], rowpair, 0, IS_A ? MLSK_CTR_A : MLSK_CTR_B, key);
             double z0, z1;
             box_muller<true>(lo64(r), hi64(r), z0, z1, T);
             double a = __dadd_rn(mv[u].x, __dmul_rn(sd, z0));
             double b = __dadd_rn(mv[u].y, __dmul_rn(sd, z1));
             if (!IS_A) {
+                // padding columns (only when KC does not divide c): A holds a finite
+                // draw of column 0, B is 0 * x = 0 (s_w = 0), so the product is 0
                 const double w = s_w[tq + 4 * u];
                 a = __dmul_rn(w, a);
                 b = __dmul_rn(w, b);
             }
-            // padding columns (j < 0, only when KC does not divide c): A holds a
-            // finite draw of column 0, B is 0 * x = 0 (s_w = 0), so the product is 0
             v0[u] = a;
             v1[u] = b;
         }
@@ -129,7 +131,7 @@ __device__ __forceinline__ void gen_phase(const DevModel& M, const Tables& T, ui
         for (int u = 0; u < U; ++u) {
             const int j = s_j[tq + 4 * u];
             double a = 0.0, b = 0.0;
-            if (j >= 0 && r0 < lim) {
+            if (r0 < lim) {
                 const double* mp = mrow + (int64_t)j * dim;
                 const bool pair = r0 + 1 < lim;
                 const double m0 = __ldg(mp), m1 = pair ? __ldg(mp + 1) : 0.0;
@@ -157,7 +159,6 @@ k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restr
     __shared__ __align__(16) double2 s_sc[1024];
     __shared__ __align__(16) double2 s_lg[128];
     extern __shared__ __align__(16) double gen_dyn[];  // 2 x GROWS x KC tiles (past the 48 KB static limit)
-    double* const tile[2] = {gen_dyn, gen_dyn + GROWS * KC};
     __shared__ int s_j[KC];
     __shared__ double s_w[KC];
     load_tables_full(s_sc, s_lg, M.tab);
@@ -175,7 +176,7 @@ k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restr
         __syncthreads();  // previous item's readers of s_j are done
         if (tid < KC) {
             const int64_t t = kc * KC + tid;
-            int j = -1;
+            int j = 0;  // padding columns (t >= c): column 0 with weight 0
             double w = 0.0;
             if (t < c) {
                 const u32x4 r = philox((uint32_t)(t >> 1), 0, 0, MLSK_CTR_INDEX, key);
@@ -192,7 +193,7 @@ k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restr
             const bool isA = ph < a_phases;
             const int64_t rb = (int64_t)(isA ? ph : ph - a_phases) * GROWS;
             const int64_t span = isA ? MP - rb : PP - rb;     // rows / cols in the panel
-            double* tl = tile[buf];
+            double* tl = gen_dyn + buf * (GROWS * KC);
             if (isA) gen_phase<true>(M, T, key, rb, s_j, s_w, tl, tid);
             else gen_phase<false>(M, T, key, rb, s_j, s_w, tl, tid);
             __syncthreads();
