@@ -52,6 +52,11 @@ def flops_of(N):
     return sum(2.0 * M_ * P_ * C0 * 2 ** l * n for l, n in enumerate(N))
 
 
+def panel_bytes_of(N):
+    """Algorithmic bytes the GEMM reads: the sampled columns of A and rows of B (fp64)."""
+    return sum(8.0 * (M_ + P_) * C0 * 2 ** l * n for l, n in enumerate(N))
+
+
 def data_seed():
     from paper_1904_00429_b200.mlsketch import RngStream
     return RngStream.derive_seed(MASTER, 0xD47A0002, 0)
@@ -277,11 +282,15 @@ def main():
     gemm = kern.get("gemm_f64", {"launches": 0, "ms": 0.0})
     rank_flops = args.steps * flops_of(STEP_N)
     achieved = rank_flops / (gemm["ms"] * 1e-3) / 1e12 if gemm["ms"] > 0 else None
+    # dram traffic per average launch: the ratio (dram bytes / algorithmic panel
+    # bytes) of a full batch captured with ncu --set full, times this run's
+    # algorithmic bytes per launch
     traffic = None
     prof_json = os.path.join(ROOT, "profiles", "gemm_f64_traffic.json")
-    if os.path.exists(prof_json):
+    if os.path.exists(prof_json) and gemm["launches"] > 0:
         try:
-            traffic = json.load(open(prof_json)).get("dram_bytes_per_launch")
+            ratio = json.load(open(prof_json)).get("dram_over_algorithmic")
+            traffic = ratio * args.steps * panel_bytes_of(STEP_N) / gemm["launches"] if ratio else None
         except Exception:
             traffic = None
 
