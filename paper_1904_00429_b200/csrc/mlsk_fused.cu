@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "mlsk_internal.h"
 
@@ -766,6 +767,18 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
             batches.push_back({j, off, nb, job_off[j] + off});
             max_panel = std::max(max_panel, nb * per);
         }
+    }
+    {
+        // one level-sample's panels must fit a buffer (samples are not split
+        // along K); fail with a clear message instead of an opaque allocation error
+        size_t free_b = 0, total_b = 0;
+        MLSK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        size_t held = 0;
+        for (int i = 0; i < NBUF; ++i) held += P.panels[i].n * sizeof(double);
+        if ((double)NBUF * (double)max_panel > (double)(free_b + held))
+            throw Error(MLSK_ERUNTIME, "fused engine: the sampled panels of one batch (" +
+                                           std::to_string(max_panel >> 20) + " MiB x " + std::to_string(NBUF) +
+                                           " buffers) exceed free device memory; use a smaller c_l or m, p");
     }
     for (int i = 0; i < NBUF; ++i) P.panels[i].ensure((size_t)(max_panel + 7) / 8);
 
