@@ -555,10 +555,11 @@ class F64Engine final : public PanelEngine {
         gen_ctas_ = nsm_ * gen_occ;  // one full wave of the grid-stride generator
         if (const char* e = getenv("MLSK_GEN_CTAS_PER_SM")) gen_ctas_ = nsm_ * std::max(1, atoi(e));  // experiments
     }
-    int64_t panel_bytes(int64_t c) const override { return (MP_ + PP_) * nkc(c) * KC * 8; }
+    int64_t chunk_cols() const override { return KC; }
+    int64_t chunk_bytes() const override { return (MP_ + PP_) * KC * 8; }
     int64_t group_size() const override { return Gs_; }
     void gen(cudaStream_t s, uint64_t seed, uint64_t tag, const int64_t* ks, int nb, int64_t c, int64_t cc,
-             double w_fine, double w_coarse, void* panels, uint32_t* idx) override {
+             double w_fine, double w_coarse, void* panels, uint32_t* idx, const KRange&) override {
         const int64_t k = nkc(c);
         double* Apan = static_cast<double*>(panels);
         double* Bpan = Apan + (size_t)nb * k * MP_ * KC;
@@ -567,7 +568,7 @@ class F64Engine final : public PanelEngine {
             M_.dm, seed, tag, ks, nb, c, cc, w_fine, w_coarse, MP_, PP_, k, Apan, Bpan, idx);
         launched();
     }
-    void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, LevelState& st) override {
+    void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, LevelState& st, const KRange&) override {
         const int64_t k = nkc(c);
         const double* Apan = static_cast<const double*>(panels);
         const double* Bpan = Apan + (size_t)nb * k * MP_ * KC;
@@ -677,6 +678,7 @@ struct Batch {
     int64_t off;  // into the job's replication list
     int nb;
     int64_t ks_off;  // into the round's device ks array
+    KRange kr;       // K-chunk range (split samples)
 };
 
 }  // namespace
@@ -753,18 +755,38 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
     std::unique_ptr<PanelEngine> engine = tc_supported(M, a.target) ? make_tc_engine(M, ws) : make_f64_engine(M, ws);
     PanelEngine& E = *engine;
     const int64_t Gs = E.group_size();
-    const int64_t budget = int64_t(384) << 20;  // panel bytes per batch (x NBUF in flight)
+    int64_t budget = int64_t(384) << 20;  // panel bytes per batch (x NBUF in flight)
+    if (const char* e = getenv("MLSK_PANEL_BUDGET_MB"))  // tests: force K-split samples at small shapes
+        budget = std::max<int64_t>(1, atoll(e)) << 20;
 
     std::vector<Batch> batches;
     int64_t max_panel = 0;
     for (size_t j = 0; j < jobs.size(); ++j) {
         const int64_t per = E.panel_bytes(jobs[j].lv.c);
+        const int64_t total = (int64_t)jks[j].size();
+        if (per > budget && E.splits_k()) {
+            // one sample's panels exceed a batch: K-segments of one sample each,
+            // the partial Y carried between them
+            if (jobs[j].probe_host)
+                throw Error(MLSK_EINVAL, "probe: not available for level-samples split along K (panels > 384 MiB)");
+            const int64_t nk = (jobs[j].lv.c + E.chunk_cols() - 1) / E.chunk_cols();
+            const int64_t seg = std::max<int64_t>(1, budget / E.chunk_bytes());
+            for (int64_t off = 0; off < total; ++off)
+                for (int64_t k0 = 0; k0 < nk; k0 += seg) {
+                    KRange kr;
+                    kr.kc0 = k0;
+                    kr.nkc = std::min(seg, nk - k0);
+                    kr.part = nk <= seg ? 0 : (k0 == 0 ? 1 : (k0 + kr.nkc == nk ? 3 : 2));
+                    batches.push_back({j, off, 1, job_off[j] + off, kr});
+                    max_panel = std::max(max_panel, kr.nkc * E.chunk_bytes());
+                }
+            continue;
+        }
         int64_t max_nb = std::max<int64_t>(1, budget / per);
         if (max_nb > Gs) max_nb = max_nb / Gs * Gs;
-        const int64_t total = (int64_t)jks[j].size();
         for (int64_t off = 0; off < total; off += max_nb) {
             const int nb = (int)std::min<int64_t>(max_nb, total - off);
-            batches.push_back({j, off, nb, job_off[j] + off});
+            batches.push_back({j, off, nb, job_off[j] + off, KRange{}});
             max_panel = std::max(max_panel, nb * per);
         }
     }
@@ -798,11 +820,11 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         // generator: wait until the GEMM that last used this buffer is done
         if (P.used[buf]) MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.mm_done[buf], 0));
         if (serial_mode() && i > 0) MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.mm_done[(i - 1) % NBUF], 0));
-        E.gen(P.s_gen, a.seed, job.lv.tag, P.ks.p + bt.ks_off, bt.nb, c, cc, w_fine, w_coarse, panels, idx);
+        E.gen(P.s_gen, a.seed, job.lv.tag, P.ks.p + bt.ks_off, bt.nb, c, cc, w_fine, w_coarse, panels, idx, bt.kr);
         MLSK_CUDA(cudaEventRecord(P.gen_done[buf], P.s_gen));
         // GEMM + fused level epilogue + fixed-order reduction
         MLSK_CUDA(cudaStreamWaitEvent(P.s_mm, P.gen_done[buf], 0));
-        E.gemm(P.s_mm, panels, bt.nb, c, *job.st);
+        E.gemm(P.s_mm, panels, bt.nb, c, *job.st, bt.kr);
         MLSK_CUDA(cudaEventRecord(P.mm_done[buf], P.s_mm));
         P.used[buf] = true;
         if (idx) {

@@ -194,7 +194,7 @@ struct Workspace {
     DevArray<double> a_cols, b_rows, v, seg_part;
     DevArray<int64_t> seg_desc;
     DevArray<double> panel_a, panel_b, partial;
-    DevArray<float> panel_af, panel_bf;
+    DevArray<float> ypart;  // partial Y of a sample split along K (tcgen05 engine)
 };
 
 struct RunArgs {
@@ -221,13 +221,24 @@ struct FusedJob {
 };
 // A sampled-GEMM engine as seen by the pipelined batch loop (mlsk_fused.cu):
 // a panel generator and a GEMM + fused level epilogue + fixed-order reduction.
+// K-range of a batch: chunks [kc0, kc0 + nkc) of each sample's K-chunks (nkc < 0:
+// all).  part = 0: whole samples; otherwise the batch is ONE sample split along
+// K, part = 1 first / 2 middle / 3 last segment, with the partial Y carried
+// between segments in device memory (samples whose panels exceed a batch).
+struct KRange {
+    int64_t kc0 = 0, nkc = -1;
+    int part = 0;
+};
 struct PanelEngine {
     virtual ~PanelEngine() = default;
-    virtual int64_t panel_bytes(int64_t c) const = 0;  // per level-sample
-    virtual int64_t group_size() const = 0;            // samples per round of the CTA groups
+    virtual int64_t chunk_cols() const = 0;   // K columns per chunk
+    virtual int64_t chunk_bytes() const = 0;  // panel bytes of one chunk of one sample
+    int64_t panel_bytes(int64_t c) const { return (c + chunk_cols() - 1) / chunk_cols() * chunk_bytes(); }
+    virtual bool splits_k() const { return false; }
+    virtual int64_t group_size() const = 0;   // samples per round of the CTA groups
     virtual void gen(cudaStream_t s, uint64_t seed, uint64_t tag, const int64_t* ks, int nb, int64_t c, int64_t cc,
-                     double w_fine, double w_coarse, void* panels, uint32_t* idx) = 0;
-    virtual void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, LevelState& st) = 0;
+                     double w_fine, double w_coarse, void* panels, uint32_t* idx, const KRange& kr) = 0;
+    virtual void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, LevelState& st, const KRange& kr) = 0;
 };
 std::unique_ptr<PanelEngine> make_tc_engine(const Model& M, Workspace& ws);  // mlsk_tc.cu
 

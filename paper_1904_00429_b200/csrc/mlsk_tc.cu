@@ -181,7 +181,7 @@ __device__ __forceinline__ float rff_entry(const DevModel& M, int64_t col, int64
 // hi and lo tiles staged in shared memory in the SW128 layout, then copied out.
 __global__ void __launch_bounds__(GEN_T)
 k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
-                  int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc,
+                  int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kc0,
                   float* __restrict__ Ahi, float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
                   uint32_t* __restrict__ idx_out) {
     __shared__ __align__(1024) unsigned char thi[TTILE];
@@ -207,7 +207,7 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
         const uint64_t key = derive_seed(seed, tag, (uint64_t)ks[b]);
         __syncthreads();
         if (tid < TBK) {
-            const int64_t t = kc * TBK + tid;
+            const int64_t t = (kc0 + kc) * TBK + tid;  // column of the sample (kc0: first chunk of this K-range)
             int j = -1;
             float w = 0.f;
             if (t < c) {
@@ -308,7 +308,8 @@ constexpr int RFF_CH = RFF_COLS / TBK;     // K-chunk tiles per work item
 
 __global__ void __launch_bounds__(GEN_T)
 k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
-                 int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc, float* __restrict__ Ahi,
+                 int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kcg,
+                 float* __restrict__ Ahi,
                  float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
                  uint32_t* __restrict__ idx_out) {
     extern __shared__ __align__(1024) unsigned char rsm[];
@@ -329,7 +330,7 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
         const uint64_t key = derive_seed(seed, tag, (uint64_t)ks[b]);
         __syncthreads();
         if (tid < RFF_COLS) {
-            const int64_t t = kc0 * TBK + tid;
+            const int64_t t = (kcg + kc0) * TBK + tid;  // kcg: first chunk of this K-range
             int j = -1;
             float w = 0.f;
             if (t < c) {
@@ -414,7 +415,8 @@ struct TcShape {
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, const float* __restrict__ Bhi,
-              const float* __restrict__ Blo, TcShape sh, double* __restrict__ part, double* __restrict__ part_sq) {
+              const float* __restrict__ Blo, TcShape sh, double* __restrict__ part, double* __restrict__ part_sq,
+              int split_part, float* __restrict__ ypart) {
     extern __shared__ __align__(1024) unsigned char dsm[];
     // 1024-byte aligned stage ring (SW128 atoms)
     unsigned char* ring = dsm + ((1024 - (smem_addr(dsm) & 1023)) & 1023);
@@ -528,10 +530,29 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             bar_wait(tfull0 + 8 * abuf, (aph >> abuf) & 1u);
             tc_fence_after();
             float ssq = 0.f;
+            // split sample (one sample per launch): the partial Y of earlier K-segments
+            float4* yp = split_part ? reinterpret_cast<float4*>(ypart + (int64_t)tile * (TBM * TBN) +
+                                                                (int64_t)row * TBN + h * HC)
+                                    : nullptr;
 #pragma unroll
             for (int ch = 0; ch < HC / 16; ++ch) {
                 float y[16];
                 tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * TBN + h * HC + ch * 16), y);
+                if (split_part >= 2) {  // middle / last segment: add the carried partial
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const float4 pv = yp[ch * 4 + v];
+                        y[4 * v] = __fadd_rn(pv.x, y[4 * v]);
+                        y[4 * v + 1] = __fadd_rn(pv.y, y[4 * v + 1]);
+                        y[4 * v + 2] = __fadd_rn(pv.z, y[4 * v + 2]);
+                        y[4 * v + 3] = __fadd_rn(pv.w, y[4 * v + 3]);
+                    }
+                }
+                if (split_part == 1 || split_part == 2) {  // not the last segment: carry Y on
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) yp[ch * 4 + v] = make_float4(y[4 * v], y[4 * v + 1], y[4 * v + 2], y[4 * v + 3]);
+                    continue;
+                }
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     ssq = __fmaf_rn(y[i], y[i], ssq);
@@ -639,34 +660,49 @@ class TcEngine final : public PanelEngine {
             rattr = true;
         }
     }
-    int64_t panel_bytes(int64_t c) const override { return (MP_ + PP_) * nkc(c) * TBK * 8; }  // hi + lo
+    int64_t chunk_cols() const override { return TBK; }
+    int64_t chunk_bytes() const override { return (MP_ + PP_) * TBK * 8; }  // hi + lo
+    bool splits_k() const override { return true; }
     int64_t group_size() const override { return Gs_; }
     void gen(cudaStream_t s, uint64_t seed, uint64_t tag, const int64_t* ks, int nb, int64_t c, int64_t cc,
-             double w_fine, double w_coarse, void* panels, uint32_t* idx) override {
+             double w_fine, double w_coarse, void* panels, uint32_t* idx, const KRange& kr) override {
+        const int64_t k = kr.nkc >= 0 ? kr.nkc : nkc(c);
         float *Ahi, *Alo, *Bhi, *Blo;
-        split(panels, nb, c, Ahi, Alo, Bhi, Blo);
-        const int64_t k = nkc(c);
+        split(panels, nb, k, Ahi, Alo, Bhi, Blo);
         Prof p("gen_panels_tf32", s);
         if (M_.dm.kind == MLSK_MODEL_RFF && M_.dm.rff_dim <= RFF_DMAX) {
             k_gen_panels_rff<<<(int)std::min<int64_t>((int64_t)nb * ((k + RFF_CH - 1) / RFF_CH), (int64_t)nsm_ * 4),
                                GEN_T, rff_smem_, s>>>(
-                S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, Ahi, Alo, Bhi, Blo, idx);
+                S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi, Blo,
+                idx);
         } else {
             k_gen_panels_tf32<<<(int)std::min<int64_t>((int64_t)nb * k, (int64_t)nsm_ * 8), GEN_T, 0, s>>>(
-                S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, Ahi, Alo, Bhi, Blo, idx);
+                S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi, Blo,
+                idx);
         }
         launched();
     }
-    void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, LevelState& st) override {
+    void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, LevelState& st, const KRange& kr) override {
+        const int64_t k = kr.nkc >= 0 ? kr.nkc : nkc(c);
         float *Ahi, *Alo, *Bhi, *Blo;
-        split(const_cast<void*>(panels), nb, c, Ahi, Alo, Bhi, Blo);
+        split(const_cast<void*>(panels), nb, k, Ahi, Alo, Bhi, Blo);
         double* part = ws_.partial.p;
         double* part_sq = part + (size_t)T_ * Gs_ * (TBM * TBN);
-        MLSK_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * (size_t)T_ * Gs_ * (TBM * TBN), s));
-        TcShape sh{nb, nkc(c), MP_, PP_, T_, Gs_, tiles_n_};
+        const bool finishes = kr.part == 0 || kr.part == 3;  // samples complete in this launch
+        if (finishes) MLSK_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * (size_t)T_ * Gs_ * (TBM * TBN), s));
+        float* ypart = nullptr;
+        if (kr.part != 0) {
+            ws_.ypart.ensure((size_t)T_ * TBM * TBN);  // the carried partial Y of a split sample
+            ypart = ws_.ypart.p;
+        }
+        TcShape sh{nb, k, MP_, PP_, T_, Gs_, tiles_n_};
         {
             Prof p("gemm_tf32x3", s);
-            k_gemm_tf32x3<<<T_ * Gs_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq);
+            k_gemm_tf32x3<<<T_ * Gs_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq, kr.part, ypart);
+        }
+        if (!finishes) {
+            launched();
+            return;
         }
         {
             Prof p("reduce_tiles_tc", s);
@@ -679,8 +715,9 @@ class TcEngine final : public PanelEngine {
 
    private:
     static int64_t nkc(int64_t c) { return (c + TBK - 1) / TBK; }
-    void split(void* panels, int nb, int64_t c, float*& Ahi, float*& Alo, float*& Bhi, float*& Blo) const {
-        const size_t na = (size_t)nb * nkc(c) * MP_ * TBK, nbp = (size_t)nb * nkc(c) * PP_ * TBK;
+    // panels of nb samples x k K-chunks: A hi, A lo, B hi, B lo
+    void split(void* panels, int nb, int64_t k, float*& Ahi, float*& Alo, float*& Bhi, float*& Blo) const {
+        const size_t na = (size_t)nb * k * MP_ * TBK, nbp = (size_t)nb * k * PP_ * TBK;
         Ahi = static_cast<float*>(panels);
         Alo = Ahi + na;
         Bhi = Alo + na;

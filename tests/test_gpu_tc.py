@@ -59,3 +59,18 @@ def test_tc_probe_indices_match_exact(gpu):
         gpu.mlmc_matmul(model, gpu.target_identity(), plan, 5,
                         gpu.EstimatorOptions(engine=eng, probe=lambda l, k, f, c, e=eng: seen[e].append((l, k, f))))
     assert seen["fused"] == seen["exact"] and len(seen["fused"]) == 3
+
+
+@pytest.mark.parametrize("name", ["gauss_f32", "student_t", "rff"])
+def test_tc_samples_split_along_k(gpu, name, monkeypatch):
+    """Level-samples whose panels exceed a batch run as K-segments of one
+    sample with the partial Y carried in device memory (BASELINE config 5's
+    deep levels: one sample of c = 262144 is 34 GB of panels).  A 1 MiB batch
+    budget forces the split at test shapes; the result must match the exact
+    engine like the unsplit one does."""
+    model = models(gpu)[name]
+    plan = gpu.LevelPlan(2, 2, [5, 3, 2], c0=256)  # c = 256, 512, 1024 -> 1 .. 8 segments per sample
+    re_ = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="exact"))
+    monkeypatch.setenv("MLSK_PANEL_BUDGET_MB", "1")
+    rs = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
+    check(rs, re_)

@@ -45,6 +45,11 @@ def configs():
         5: dict(model=g.student_t_matrix_model(8192, 2 ** 20, 8192, data_seed=ds(5)),
                 c0=256, N=[8, 4, 2, 1, 1], m=8192, p=8192,
                 desc="8192x2^20x8192 fp32 Student-t(3), c0=256, levels 0-4 (c <= 4096) of L=10, N_l = 8,4,2,1,1"),
+        # config 5's whole hierarchy: levels 5-10 (c = 8192 .. 262144, up to 34 GB of panels per sample) run as
+        # K-segments of one sample with the partial Y carried in device memory
+        6: dict(model=g.student_t_matrix_model(8192, 2 ** 20, 8192, data_seed=ds(5)),
+                c0=256, N=[8, 4, 2, 1, 1, 1, 1, 1, 1, 1, 1], m=8192, p=8192,
+                desc="config 5, all levels 0-10 (c = 256 .. 262144), N_l = 8,4,2,1,...,1"),
     }
 
 
