@@ -155,7 +155,7 @@ __device__ __forceinline__ void gen_phase(const DevModel& M, const Tables& T, ui
 
 __global__ void __launch_bounds__(GEN_THREADS, 4)
 k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
-                 int64_t cc, double w_fine, double w_coarse, int64_t MP, int64_t PP, int64_t nkc,
+                 int64_t cc, double w_fine, double w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kc0,
                  double* __restrict__ Apan, double* __restrict__ Bpan, uint32_t* __restrict__ idx_out) {
     __shared__ __align__(16) double2 s_sc[1024];
     __shared__ __align__(16) double2 s_lg[128];
@@ -176,7 +176,7 @@ k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restr
         const uint64_t key = derive_seed(seed, tag, (uint64_t)ks[b]);
         __syncthreads();  // previous item's readers of s_j are done
         if (tid < KC) {
-            const int64_t t = kc * KC + tid;
+            const int64_t t = (kc0 + kc) * KC + tid;  // column of the sample (kc0: first chunk of this K-range)
             int j = 0;  // padding columns (t >= c): column 0 with weight 0
             double w = 0.0;
             if (t < c) {
@@ -271,9 +271,12 @@ struct GemmShape {
 
 // 192-register cap (no spills; 218 uncapped): 192 x 256 leaves the SM room for
 // one generator CTA beside the GEMM CTA (measured +2% on the config-2 step).
+// SPLIT: one sample split along K per launch (split_part 1 first, 2 middle,
+// 3 last); a separate instantiation keeps the common path's registers intact.
+template <bool SPLIT>
 __global__ void __maxnreg__(192)
 k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, GemmShape sh,
-           double* __restrict__ part, double* __restrict__ part_sq) {
+           double* __restrict__ part, double* __restrict__ part_sq, int split_part, double* __restrict__ ypart) {
     extern __shared__ __align__(1024) unsigned char smem[];
     double* sA = reinterpret_cast<double*>(smem);
     double* sB = reinterpret_cast<double*>(smem + STAGES * A_STAGE_BYTES);
@@ -386,6 +389,27 @@ k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, Gem
         }
         if (++kc == sh.nkc) {
             kc = 0;
+            if (SPLIT) {
+                // one sample split along K (one sample per launch): carry the partial Y
+                double* yp = ypart + (int64_t)tile * (BM * BN);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        double2* q2 = reinterpret_cast<double2*>(yp + (wi * 32 + 8 * i + gid) * BN + wj * 32 + 8 * j +
+                                                                 2 * tig);
+                        if (split_part >= 2) {
+                            const double2 pv = *q2;
+                            acc[i][j][0] = __dadd_rn(pv.x, acc[i][j][0]);
+                            acc[i][j][1] = __dadd_rn(pv.y, acc[i][j][1]);
+                        }
+                        if (split_part <= 2) {
+                            *q2 = make_double2(acc[i][j][0], acc[i][j][1]);
+                            acc[i][j][0] = acc[i][j][1] = 0.0;
+                        }
+                    }
+                if (split_part <= 2) continue;  // not the last segment: no epilogue yet
+            }
             // sample boundary: fused level epilogue (Y^2 and running sum)
 #pragma unroll
             for (int i = 0; i < 4; ++i)
@@ -541,7 +565,8 @@ class F64Engine final : public PanelEngine {
         smem_ = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 2 * STAGES * 8;
         static bool attr = false;
         if (!attr) {
-            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_f64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_f64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
             attr = true;
         }
         ws_.partial.ensure((size_t)T_ * Gs_ * (BM * BN) + (size_t)T_ * Gs_);
@@ -557,27 +582,40 @@ class F64Engine final : public PanelEngine {
     }
     int64_t chunk_cols() const override { return KC; }
     int64_t chunk_bytes() const override { return (MP_ + PP_) * KC * 8; }
+    bool splits_k() const override { return true; }
     int64_t group_size() const override { return Gs_; }
     void gen(cudaStream_t s, uint64_t seed, uint64_t tag, const int64_t* ks, int nb, int64_t c, int64_t cc,
-             double w_fine, double w_coarse, void* panels, uint32_t* idx, const KRange&) override {
-        const int64_t k = nkc(c);
+             double w_fine, double w_coarse, void* panels, uint32_t* idx, const KRange& kr) override {
+        const int64_t k = kr.nkc >= 0 ? kr.nkc : nkc(c);
         double* Apan = static_cast<double*>(panels);
         double* Bpan = Apan + (size_t)nb * k * MP_ * KC;
         Prof p("gen_panels_f64", s);
         k_gen_panels_f64<<<(int)std::min<int64_t>((int64_t)nb * k, (int64_t)gen_ctas_), GEN_THREADS, GEN_DYN_SMEM, s>>>(
-            M_.dm, seed, tag, ks, nb, c, cc, w_fine, w_coarse, MP_, PP_, k, Apan, Bpan, idx);
+            M_.dm, seed, tag, ks, nb, c, cc, w_fine, w_coarse, MP_, PP_, k, kr.kc0, Apan, Bpan, idx);
         launched();
     }
-    void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, LevelState& st, const KRange&) override {
-        const int64_t k = nkc(c);
+    void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, LevelState& st, const KRange& kr) override {
+        const int64_t k = kr.nkc >= 0 ? kr.nkc : nkc(c);
         const double* Apan = static_cast<const double*>(panels);
         const double* Bpan = Apan + (size_t)nb * k * MP_ * KC;
         double* part = ws_.partial.p;
         double* part_sq = part + (size_t)T_ * Gs_ * (BM * BN);
+        double* ypart = nullptr;
+        if (kr.part != 0) {
+            ws_.ypart64.ensure((size_t)T_ * BM * BN);  // the carried partial Y of a split sample
+            ypart = ws_.ypart64.p;
+        }
         GemmShape sh{nb, k, MP_, PP_, T_, Gs_, tiles_n_};
         {
             Prof p("gemm_f64", s);
-            k_gemm_f64<<<T_ * Gs_, GEMM_THREADS, smem_, s>>>(Apan, Bpan, sh, part, part_sq);
+            if (kr.part == 0)
+                k_gemm_f64<false><<<T_ * Gs_, GEMM_THREADS, smem_, s>>>(Apan, Bpan, sh, part, part_sq, 0, nullptr);
+            else
+                k_gemm_f64<true><<<T_ * Gs_, GEMM_THREADS, smem_, s>>>(Apan, Bpan, sh, part, part_sq, kr.part, ypart);
+        }
+        if (kr.part == 1 || kr.part == 2) {  // the sample completes in a later launch
+            launched();
+            return;
         }
         const int64_t cells = M_.rows * M_.cols;
         {

@@ -194,7 +194,8 @@ struct Workspace {
     DevArray<double> a_cols, b_rows, v, seg_part;
     DevArray<int64_t> seg_desc;
     DevArray<double> panel_a, panel_b, partial;
-    DevArray<float> ypart;  // partial Y of a sample split along K (tcgen05 engine)
+    DevArray<float> ypart;     // partial Y of a sample split along K (tcgen05 engine)
+    DevArray<double> ypart64;  // same, fp64 engine
 };
 
 struct RunArgs {

@@ -105,3 +105,14 @@ def test_session_rounds_equal_single_run(gpu):
     r2 = gpu.mlmc_matmul(model, gpu.target_identity(), gpu.LevelPlan(2, 2, [160, 80, 33], c0=32), MASTER)
     compare_reports(r1, r2, tol=1e-13)
     sess.close()
+
+
+def test_fused_f64_samples_split_along_k(gpu, monkeypatch):
+    """fp64 level-samples larger than a panel batch run as K-segments with the
+    partial Y carried in device memory; forced here by a 1 MiB batch budget."""
+    model = gpu.gaussian_mean_matrix_model(256, 4096, 192, sd=0.5, data_seed=21)
+    plan = gpu.LevelPlan(2, 2, [5, 3, 2], c0=256)  # per-sample panels 2 .. 8 MiB
+    re_ = gpu.mlmc_matmul(model, gpu.target_identity(), plan, 13, gpu.EstimatorOptions(engine="exact"))
+    monkeypatch.setenv("MLSK_PANEL_BUDGET_MB", "1")
+    rs = gpu.mlmc_matmul(model, gpu.target_identity(), plan, 13, gpu.EstimatorOptions(engine="fused"))
+    compare_reports(rs, re_)
