@@ -193,8 +193,8 @@ struct Runner {
 // All levels' sums / sums of squares in one pass: one device->host copy per
 // level into pinned staging (only [total | total_sq] unless a chunk is
 // open), one synchronisation.
-void read_levels(const std::vector<LevelState>& sts, cudaStream_t s, Workspace& ws,
-                 std::vector<std::vector<double>>& sums, std::vector<double>& sqs) {
+void read_levels(const std::vector<LevelState>& sts, cudaStream_t s, Workspace& ws, std::vector<const double*>& sums,
+                 std::vector<double>& sqs) {
     size_t need = 0;
     for (const auto& st : sts) need += (st.open_count > 0 ? 2 : 1) * (size_t)(st.cells + 1);
     double* h = ws.host.ensure(std::max<size_t>(need, 1));
@@ -210,13 +210,13 @@ void read_levels(const std::vector<LevelState>& sts, cudaStream_t s, Workspace& 
     off = 0;
     for (size_t l = 0; l < sts.size(); ++l) {
         const int64_t cells = sts[l].cells;
-        const double* b = h + off;
-        sums[l].assign(b, b + cells);
-        sqs[l] = b[cells];
-        if (sts[l].open_count > 0) {
-            for (int64_t t = 0; t < cells; ++t) sums[l][t] += b[cells + 1 + t];
-            sqs[l] += b[2 * cells + 1];
+        double* b = h + off;  // the level's sums, read in place from the staging buffer
+        if (sts[l].open_count > 0) {  // fold the open chunk in (last in order)
+            for (int64_t t = 0; t < cells; ++t) b[t] += b[cells + 1 + t];
+            b[cells] += b[2 * cells + 1];
         }
+        sums[l] = b;
+        sqs[l] = b[cells];
         off += (sts[l].open_count > 0 ? 2 : 1) * (size_t)(cells + 1);
     }
 }
@@ -273,23 +273,25 @@ int mlmc_impl(bool matrix, const mlsk_model_desc* model, int32_t target, double 
         tr.mark("level states");
         R.run(items, ex.stream, ex.probe_k);  // all levels as one round
         tr.mark("round");
-        std::vector<std::vector<double>> sums;
+        std::vector<const double*> sums;
         std::vector<double> sqs;
         read_levels(states, ex.stream, *R.wsp, sums, sqs);
+        tr.mark("level d2h");
+        double* const lsum = rep ? rep->level_sum : nullptr;
+        double* const lest = rep ? rep->level_estimate : nullptr;
         for (int64_t l = 0; l <= plan->L; ++l) {
             const int64_t fine = plan->c0 * ipow(plan->M, l);
             const int64_t coarse = l > 0 ? fine / plan->M : 0;
             const LevelState& st = states[l];
-            const std::vector<double>& sum = sums[l];
+            const double* sum = sums[l];
             const double sq = sqs[l];
             const double inv_n = 1.0 / (double)plan->N[l];
             const int64_t cost = plan->N[l] * (fine + coarse) * cells;  // estimators.cpp:34-40
             total_cost += cost;
+            if (lsum) std::memcpy(lsum + l * cells, sum, sizeof(double) * cells);
+            if (lest)
+                for (int64_t t = 0; t < cells; ++t) lest[l * cells + t] = sum[t] * inv_n;
             if (rep) {
-                for (int64_t t = 0; t < cells; ++t) {
-                    if (rep->level_sum) rep->level_sum[l * cells + t] = sum[t];
-                    if (rep->level_estimate) rep->level_estimate[l * cells + t] = sum[t] * inv_n;
-                }
                 if (rep->level_sumsq) rep->level_sumsq[l] = sq;
                 if (rep->level_mean_sq) rep->level_mean_sq[l] = sq * inv_n;
                 if (rep->level_count) rep->level_count[l] = st.count;
@@ -510,22 +512,21 @@ int mlsk_session_stats(mlsk_session* s, mlsk_report* rep) {
         const int64_t cells = s->R.model.rows * s->R.model.cols;
         std::vector<double> value(cells, 0.0);
         int64_t total_cost = 0;
-        std::vector<std::vector<double>> sums;
+        std::vector<const double*> sums;
         std::vector<double> sqs;
         read_levels(s->levels, s->ex->stream, *s->R.wsp, sums, sqs);
         for (int64_t l = 0; l <= s->L; ++l) {
-            const std::vector<double>& sum = sums[l];
+            const double* sum = sums[l];
             const double sq = sqs[l];
             const int64_t n = s->levels[l].count;
             const int64_t fine = s->c0 * ipow(s->M, l), coarse = l > 0 ? fine / s->M : 0;
             const double inv_n = n > 0 ? 1.0 / (double)n : 0.0;
             const int64_t cost = n * (fine + coarse) * cells;
             total_cost += cost;
-            for (int64_t t = 0; t < cells; ++t) {
-                if (rep->level_sum) rep->level_sum[l * cells + t] = sum[t];
-                if (rep->level_estimate) rep->level_estimate[l * cells + t] = sum[t] * inv_n;
-                value[t] += sum[t] * inv_n;
-            }
+            if (rep->level_sum) std::memcpy(rep->level_sum + l * cells, sum, sizeof(double) * cells);
+            if (rep->level_estimate)
+                for (int64_t t = 0; t < cells; ++t) rep->level_estimate[l * cells + t] = sum[t] * inv_n;
+            for (int64_t t = 0; t < cells; ++t) value[t] += sum[t] * inv_n;
             if (rep->level_sumsq) rep->level_sumsq[l] = sq;
             if (rep->level_mean_sq) rep->level_mean_sq[l] = sq * inv_n;
             if (rep->level_count) rep->level_count[l] = n;

@@ -413,6 +413,9 @@ struct TcShape {
     int T, Gs, tiles_n;
 };
 
+// SPLIT: one sample split along K per launch (split_part 1 first, 2 middle,
+// 3 last, partial Y in ypart); a separate instantiation for the common path.
+template <bool SPLIT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, const float* __restrict__ Bhi,
               const float* __restrict__ Blo, TcShape sh, double* __restrict__ part, double* __restrict__ part_sq,
@@ -531,14 +534,14 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             tc_fence_after();
             float ssq = 0.f;
             // split sample (one sample per launch): the partial Y of earlier K-segments
-            float4* yp = split_part ? reinterpret_cast<float4*>(ypart + (int64_t)tile * (TBM * TBN) +
-                                                                (int64_t)row * TBN + h * HC)
-                                    : nullptr;
+            float4* yp = SPLIT ? reinterpret_cast<float4*>(ypart + (int64_t)tile * (TBM * TBN) +
+                                                           (int64_t)row * TBN + h * HC)
+                               : nullptr;
 #pragma unroll
             for (int ch = 0; ch < HC / 16; ++ch) {
                 float y[16];
                 tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * TBN + h * HC + ch * 16), y);
-                if (split_part >= 2) {  // middle / last segment: add the carried partial
+                if (SPLIT && split_part >= 2) {  // middle / last segment: add the carried partial
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
                         const float4 pv = yp[ch * 4 + v];
@@ -548,7 +551,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                         y[4 * v + 3] = __fadd_rn(pv.w, y[4 * v + 3]);
                     }
                 }
-                if (split_part == 1 || split_part == 2) {  // not the last segment: carry Y on
+                if (SPLIT && split_part <= 2) {  // not the last segment: carry Y on
 #pragma unroll
                     for (int v = 0; v < 4; ++v) yp[ch * 4 + v] = make_float4(y[4 * v], y[4 * v + 1], y[4 * v + 2], y[4 * v + 3]);
                     continue;
@@ -649,7 +652,8 @@ class TcEngine final : public PanelEngine {
         smem_ = TSTAGES * TSTAGE_BYTES + 1024;
         static bool attr = false;
         if (!attr) {
-            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
+            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
             attr = true;
         }
         ws_.partial.ensure((size_t)T_ * Gs_ * (TBM * TBN) + (size_t)T_ * Gs_);
@@ -698,7 +702,12 @@ class TcEngine final : public PanelEngine {
         TcShape sh{nb, k, MP_, PP_, T_, Gs_, tiles_n_};
         {
             Prof p("gemm_tf32x3", s);
-            k_gemm_tf32x3<<<T_ * Gs_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq, kr.part, ypart);
+            if (kr.part == 0)
+                k_gemm_tf32x3<false><<<T_ * Gs_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq, 0,
+                                                                         nullptr);
+            else
+                k_gemm_tf32x3<true><<<T_ * Gs_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq,
+                                                                        kr.part, ypart);
         }
         if (!finishes) {
             launched();

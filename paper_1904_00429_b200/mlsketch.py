@@ -301,15 +301,40 @@ class EstimatorOptions:
                             _ptr(probe_buf, _u32p) if probe_buf is not None else None)
 
 
-@dataclass
 class LevelStatistic:
-    level: int
-    estimate: object
-    replication_count: int
-    sample_mean_of_squares: float
-    cost_units: int
-    sum: object = None
-    sum_of_squares: float = 0.0
+    """estimators.hpp:20-27.  `estimate` = sum * (1 / replication_count), the
+    library's own arithmetic, formed on first access (the per-level sums are
+    what crosses the C-ABI; materialising every level's estimate matrix on
+    every call would double the report's host memory traffic)."""
+
+    __slots__ = ("level", "_estimate", "replication_count", "sample_mean_of_squares", "cost_units", "sum",
+                 "sum_of_squares", "_scalar", "_divisor")
+
+    def __init__(self, level, estimate, replication_count, sample_mean_of_squares, cost_units, sum=None,
+                 sum_of_squares=0.0, scalar=False, divisor=None):
+        self.level = level
+        self._estimate = estimate
+        self.replication_count = replication_count
+        self.sample_mean_of_squares = sample_mean_of_squares
+        self.cost_units = cost_units
+        self.sum = sum
+        self.sum_of_squares = sum_of_squares
+        self._scalar = scalar
+        # the plan's N_l for estimators (ranks hold partial sums of the global
+        # level), the accumulated count for sessions
+        self._divisor = replication_count if divisor is None else divisor
+
+    @property
+    def estimate(self):
+        if self._estimate is None:
+            inv = 1.0 / self._divisor if self._divisor > 0 else 0.0
+            e = np.asarray(self.sum, dtype=np.float64) * inv
+            self._estimate = float(e) if self._scalar else e
+        return self._estimate
+
+    def __repr__(self):
+        return (f"LevelStatistic(level={self.level}, replication_count={self.replication_count}, "
+                f"sample_mean_of_squares={self.sample_mean_of_squares}, cost_units={self.cost_units})")
 
 
 @dataclass
@@ -323,15 +348,16 @@ class EstimateReport:
 
 class _Buffers:
     def __init__(self, levels: int, cells: int):
-        # every entry is written by the library (np.empty: no 2 x levels x cells memset)
+        # every entry is written by the library (np.empty: no memset); the
+        # per-level estimates are derived from the sums on access
         self.value = np.empty(cells)
-        self.level_estimate = np.empty((levels, cells))
+        self.level_estimate = None
         self.level_sum = np.empty((levels, cells))
         self.level_sumsq = np.zeros(levels)
         self.level_mean_sq = np.zeros(levels)
         self.level_count = np.zeros(levels, dtype=np.int64)
         self.cost_units = np.zeros(levels, dtype=np.int64)
-        self.c = abi.Report(_ptr(self.value, _f64p), _ptr(self.level_estimate, _f64p),
+        self.c = abi.Report(_ptr(self.value, _f64p), None,
                             _ptr(self.level_sum, _f64p), _ptr(self.level_sumsq, _f64p),
                             _ptr(self.level_mean_sq, _f64p), _ptr(self.level_count, _i64p),
                             _ptr(self.cost_units, _i64p), 0, 0.0, 0)
@@ -349,15 +375,15 @@ def _shape(model) -> tuple:
     return (model.m, model.p)
 
 
-def _report(buf: _Buffers, model, levels: int, vector: bool, with_levels=True) -> EstimateReport:
+def _report(buf: _Buffers, model, levels: int, vector: bool, with_levels=True, divisors=None) -> EstimateReport:
     rows, cols = _shape(model)
     conv = (lambda x: float(x[0])) if vector else (lambda x: x.reshape(rows, cols))  # views of per-call buffers
     per = []
     if with_levels:
         for l in range(levels):
-            per.append(LevelStatistic(l, conv(buf.level_estimate[l]), int(buf.level_count[l]),
-                                      float(buf.level_mean_sq[l]), int(buf.cost_units[l]),
-                                      conv(buf.level_sum[l]), float(buf.level_sumsq[l])))
+            per.append(LevelStatistic(l, None, int(buf.level_count[l]), float(buf.level_mean_sq[l]),
+                                      int(buf.cost_units[l]), conv(buf.level_sum[l]), float(buf.level_sumsq[l]),
+                                      scalar=vector, divisor=None if divisors is None else int(divisors[l])))
     return EstimateReport(conv(buf.value), per, int(buf.c.total_cost_units),
                           float(buf.c.wall_time_s), int(buf.c.seed))
 
@@ -387,7 +413,7 @@ def _mlmc(matrix: bool, model, f: TargetFunction, plan: LevelPlan, seed: int,
             for k in range(min(probe_k, plan.N[l])):
                 fine = [int(x) for x in probe_buf[l, k, :c]]
                 options.probe(l, k, fine, fine[: c // plan.M])
-    return _report(buf, model, plan.L + 1, not matrix)
+    return _report(buf, model, plan.L + 1, not matrix, divisors=plan.N)
 
 
 def mlmc_inner(model: VectorPairModel, f: TargetFunction, plan: LevelPlan, seed: int,
