@@ -532,13 +532,10 @@ __global__ void k_reduce_inner(const double* __restrict__ y, int nb, double* tot
 }
 
 int sm_count() {
-    static int n = [] {
-        int dev = 0, v = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v;
-    }();
-    return n;
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
 }
 
 }  // namespace
@@ -563,20 +560,17 @@ class F64Engine final : public PanelEngine {
         T_ = (int)(MP_ / BM) * tiles_n_;
         Gs_ = std::max(1, nsm_ / T_);
         smem_ = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 2 * STAGES * 8;
-        static bool attr = false;
-        if (!attr) {
-            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_f64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
-            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_f64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
-            attr = true;
-        }
-        ws_.partial.ensure((size_t)T_ * Gs_ * (BM * BN) + (size_t)T_ * Gs_);
-        static int gen_occ = [] {
+        const int smem = smem_;
+        once_per_device((const void*)&k_gemm_f64<false>, [smem] {
+            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_f64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_f64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_f64, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            GEN_DYN_SMEM));
-            int b = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_gen_panels_f64, GEN_THREADS, GEN_DYN_SMEM);
-            return b > 0 ? b : 1;
-        }();
+        });
+        ws_.partial.ensure((size_t)T_ * Gs_ * (BM * BN) + (size_t)T_ * Gs_);
+        int gen_occ = 0;
+        MLSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&gen_occ, k_gen_panels_f64, GEN_THREADS, GEN_DYN_SMEM));
+        gen_occ = std::max(gen_occ, 1);
         gen_ctas_ = nsm_ * gen_occ;  // one full wave of the grid-stride generator
         if (const char* e = getenv("MLSK_GEN_CTAS_PER_SM")) gen_ctas_ = nsm_ * std::max(1, atoi(e));  // experiments
     }

@@ -4,7 +4,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <memory>
+#include <mutex>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -102,6 +105,21 @@ inline int log2_exact(int64_t n) { int k = 0; while ((int64_t(1) << k) < n) ++k;
 inline int64_t ipow(int64_t M, int64_t l) { int64_t r = 1; while (l-- > 0) r *= M; return r; }
 
 // A model uploaded / generated on the device (models.cpp:12-97 as descriptors).
+// Runs f once per (tag, current device): kernel attributes such as the dynamic
+// shared-memory limit are set per device context; a process may drive several
+// devices (mlsk_exec_opts.device).
+template <class F>
+void once_per_device(const void* tag, F&& f) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count({tag, dev})) return;
+    f();
+    done.insert({tag, dev});
+}
+
 struct Model {
     mlsk_model_desc desc{};
     DevModel dm{};

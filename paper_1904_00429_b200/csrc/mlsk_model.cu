@@ -27,16 +27,22 @@ void configure_mempool() {
 }
 
 Tables device_tables() {
-    static Tables t = [] {
-        Tables r{};
-        void* p;
-        MLSK_CUDA(cudaGetSymbolAddress(&p, g_sincos_d)); r.sincos_d = (const double*)p;
-        MLSK_CUDA(cudaGetSymbolAddress(&p, g_log_d)); r.log_d = (const double*)p;
-        MLSK_CUDA(cudaGetSymbolAddress(&p, g_sincos_f)); r.sincos_f = (const float*)p;
-        MLSK_CUDA(cudaGetSymbolAddress(&p, g_log_f)); r.log_f = (const float*)p;
-        return r;
-    }();
-    return t;
+    // symbol addresses are per device (one module per device context)
+    static std::mutex mu;
+    static std::map<int, Tables> per_dev;
+    int dev = 0;
+    MLSK_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
+    auto it = per_dev.find(dev);
+    if (it != per_dev.end()) return it->second;
+    Tables r{};
+    void* p;
+    MLSK_CUDA(cudaGetSymbolAddress(&p, g_sincos_d)); r.sincos_d = (const double*)p;
+    MLSK_CUDA(cudaGetSymbolAddress(&p, g_log_d)); r.log_d = (const double*)p;
+    MLSK_CUDA(cudaGetSymbolAddress(&p, g_sincos_f)); r.sincos_f = (const float*)p;
+    MLSK_CUDA(cudaGetSymbolAddress(&p, g_log_f)); r.log_f = (const float*)p;
+    per_dev[dev] = r;
+    return r;
 }
 
 namespace {

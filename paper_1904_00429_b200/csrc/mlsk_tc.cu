@@ -620,13 +620,10 @@ __global__ void k_reduce_tiles_tc(const double* __restrict__ part, const double*
 }
 
 int sms() {
-    static int n = [] {
-        int dev = 0, v = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v;
-    }();
-    return n;
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
 }
 
 }  // namespace
@@ -650,19 +647,14 @@ class TcEngine final : public PanelEngine {
         Gs_ = std::max(1, nsm_ / T_);
         S_.M = M.dm;
         smem_ = TSTAGES * TSTAGE_BYTES + 1024;
-        static bool attr = false;
-        if (!attr) {
-            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
-            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_));
-            attr = true;
-        }
         ws_.partial.ensure((size_t)T_ * Gs_ * (TBM * TBN) + (size_t)T_ * Gs_);
         rff_smem_ = 4 * RFF_CH * TTILE + (RFF_DMAX * TBM + RFF_DMAX * RFF_COLS) * 4;
-        static bool rattr = false;
-        if (!rattr) {
-            MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_rff, cudaFuncAttributeMaxDynamicSharedMemorySize, rff_smem_));
-            rattr = true;
-        }
+        const int smem = smem_, rsmem = rff_smem_;
+        once_per_device((const void*)&k_gemm_tf32x3<false>, [smem, rsmem] {
+            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_rff, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem));
+        });
     }
     int64_t chunk_cols() const override { return TBK; }
     int64_t chunk_bytes() const override { return (MP_ + PP_) * TBK * 8; }  // hi + lo
