@@ -531,6 +531,101 @@ __global__ void k_reduce_inner(const double* __restrict__ y, int nb, double* tot
     }
 }
 
+// All levels of a round in one launch (config 1 is launch-bound: c = 8 .. 256).
+// A part = one level's slice of the round; 8 threads per replication, lanes
+// over index pairs, reduced within the 8-lane group.
+constexpr int INNER_MAX_PARTS = 16;
+constexpr int INNER_G = 8;
+struct InnerPart {
+    uint64_t tag;
+    int64_t c, cc;
+    double w_fine, w_coarse;
+    int64_t ks_off;  // into the round's replication list
+    int64_t y_off;   // first output slot (parts are contiguous)
+    int64_t nb;
+    double* total;
+    double* total_sq;
+};
+struct InnerParts {
+    int n;
+    InnerPart p[INNER_MAX_PARTS];
+};
+
+__global__ void __launch_bounds__(256)
+k_fused_inner_multi(DevModel M, uint64_t seed, const int64_t* __restrict__ ks, InnerParts P, int64_t total,
+                    double* __restrict__ y_out) {
+    __shared__ __align__(16) double2 s_sc[256];
+    __shared__ __align__(16) double2 s_lg[128];
+    load_tables(s_sc, s_lg, M.tab);
+    __syncthreads();
+    Tables T = M.tab;
+    T.sincos_d = reinterpret_cast<const double*>(s_sc);
+    T.log_d = reinterpret_cast<const double*>(s_lg);
+    const int gl = threadIdx.x & (INNER_G - 1);
+    const int64_t groups = ((int64_t)gridDim.x * blockDim.x) / INNER_G;
+    // the whole warp iterates together (uniform trip count for the shuffles):
+    // base = its first group, lane / INNER_G selects the group
+    const int64_t warp_first = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / INNER_G;
+    for (int64_t base = warp_first; base < total; base += groups) {
+        const int64_t sidx = base + (threadIdx.x & 31) / INNER_G;
+        const bool live = sidx < total;
+        int pi = 0;
+        if (live)
+            while (pi + 1 < P.n && sidx >= P.p[pi + 1].y_off) ++pi;
+        const InnerPart& q = P.p[pi];
+        double acc = 0.0;
+        if (live) {
+            const int64_t b = sidx - q.y_off;
+            const uint64_t key = derive_seed(seed, q.tag, (uint64_t)ks[q.ks_off + b]);
+            for (int64_t tp = gl; 2 * tp < q.c; tp += INNER_G) {
+                const u32x4 ri = philox((uint32_t)tp, 0, 0, MLSK_CTR_INDEX, key);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int64_t t = 2 * tp + h;
+                    if (t >= q.c) break;
+                    const uint32_t ix = index_from_u64(h ? hi64(ri) : lo64(ri), M.n, M.log2n, M.cum);
+                    const int64_t j = (int64_t)ix - 1;
+                    const u32x4 r = philox((uint32_t)j, 0, 0, MLSK_CTR_A, key);
+                    double z0, z1;
+                    box_muller(lo64(r), hi64(r), z0, z1, T);
+                    const double a = __dadd_rn(M.mean_a[j], __dmul_rn(M.sd, z0));
+                    const double bb = __dadd_rn(M.mean_b[j], __dmul_rn(M.sd, z1));
+                    acc = __fma_rn(__dmul_rn(a, bb), t < q.cc ? q.w_coarse : q.w_fine, acc);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = INNER_G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (live && gl == 0) y_out[sidx] = acc;
+    }
+}
+
+// one block per part: total += sum y, total_sq += sum y^2 (fixed order)
+__global__ void k_reduce_inner_multi(const double* __restrict__ y, InnerParts P) {
+    __shared__ double s1[256], s2[256];
+    const InnerPart& q = P.p[blockIdx.x];
+    double a = 0.0, r = 0.0;
+    for (int64_t b = threadIdx.x; b < q.nb; b += blockDim.x) {
+        const double v = y[q.y_off + b];
+        a += v;
+        r = __fma_rn(v, v, r);
+    }
+    s1[threadIdx.x] = a;
+    s2[threadIdx.x] = r;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+        if (threadIdx.x < st) {
+            s1[threadIdx.x] += s1[threadIdx.x + st];
+            s2[threadIdx.x] += s2[threadIdx.x + st];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *q.total += s1[0];
+        *q.total_sq += s2[0];
+    }
+}
+
 int sm_count() {
     int dev = 0, v = 148;
     cudaGetDevice(&dev);
@@ -738,8 +833,54 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
     MLSK_CUDA(cudaStreamWaitEvent(P.s_mm, P.start, 0));
     P.stage_ks(all, P.s_gen);
 
+    bool any_probe = false;
+    for (const auto& job : jobs) any_probe = any_probe || job.probe_host;
+    if (M.vector && !any_probe) {
+        // config-1 shape: every level of the round in one launch (+ one reduction
+        // launch), in slices of at most 4M replications / INNER_MAX_PARTS parts
+        const int64_t max_slice = int64_t(1) << 22;
+        InnerParts parts{};
+        int64_t filled = 0;
+        auto flush = [&]() {
+            if (parts.n == 0) return;
+            ws.v.ensure((size_t)filled);
+            const int64_t grid = std::min<int64_t>((filled * INNER_G + 255) / 256, (int64_t)sms * 16);
+            {
+                Prof p("fused_inner_f64", P.s_gen);
+                k_fused_inner_multi<<<(int)std::max<int64_t>(grid, 1), 256, 0, P.s_gen>>>(M.dm, a.seed, P.ks.p, parts,
+                                                                                         filled, ws.v.p);
+            }
+            {
+                Prof p("reduce_inner", P.s_gen);
+                k_reduce_inner_multi<<<parts.n, 256, 0, P.s_gen>>>(ws.v.p, parts);
+            }
+            launched(2);
+            parts = InnerParts{};
+            filled = 0;
+        };
+        for (size_t j = 0; j < jobs.size(); ++j) {
+            FusedJob& job = jobs[j];
+            const int64_t c = job.lv.c, cc = job.lv.cc;
+            const double w_fine = n / (double)c;
+            const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;
+            const int64_t total = (int64_t)jks[j].size();
+            for (int64_t off = 0; off < total;) {
+                if (parts.n == INNER_MAX_PARTS || filled == max_slice) flush();
+                const int64_t take = std::min(total - off, max_slice - filled);
+                parts.p[parts.n++] = InnerPart{job.lv.tag, c, cc, w_fine, w_coarse, job_off[j] + off, filled, take,
+                                               job.st->total(), job.st->total_sq()};
+                filled += take;
+                off += take;
+            }
+            job.st->count += total;
+        }
+        flush();
+        MLSK_CUDA(cudaEventRecord(P.end, P.s_gen));
+        MLSK_CUDA(cudaStreamWaitEvent(a.stream, P.end, 0));
+        return;
+    }
     if (M.vector) {
-        // config-1 shape: one warp per replication, no panels
+        // config-1 shape with the coupling probe: one warp per replication, per level
         for (size_t j = 0; j < jobs.size(); ++j) {
             FusedJob& job = jobs[j];
             const int64_t c = job.lv.c, cc = job.lv.cc;
