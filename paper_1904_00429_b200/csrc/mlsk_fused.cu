@@ -929,21 +929,25 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
     PanelEngine& E = *engine;
     const int64_t Gs = E.group_size();
     int64_t budget = int64_t(384) << 20;  // panel bytes per batch (x NBUF in flight)
-    if (const char* e = getenv("MLSK_PANEL_BUDGET_MB"))  // tests: force K-split samples at small shapes
-        budget = std::max<int64_t>(1, atoll(e)) << 20;
+    if (const char* e = getenv("MLSK_PANEL_BUDGET_MB")) budget = std::max<int64_t>(1, atoll(e)) << 20;
+    // samples up to split_limit take one batch of their own (a K-split costs the
+    // partial-Y traffic and shorter launches); larger ones run as K-segments
+    int64_t split_limit = int64_t(8) << 30;
+    if (const char* e = getenv("MLSK_SPLIT_MB"))  // tests: force K-split samples at small shapes
+        split_limit = std::max<int64_t>(1, atoll(e)) << 20;
 
     std::vector<Batch> batches;
     int64_t max_panel = 0;
     for (size_t j = 0; j < jobs.size(); ++j) {
         const int64_t per = E.panel_bytes(jobs[j].lv.c);
         const int64_t total = (int64_t)jks[j].size();
-        if (per > budget && E.splits_k()) {
+        if (per > split_limit && E.splits_k()) {
             // one sample's panels exceed a batch: K-segments of one sample each,
             // the partial Y carried between them
             if (jobs[j].probe_host)
                 throw Error(MLSK_EINVAL, "probe: not available for level-samples split along K (panels > 384 MiB)");
             const int64_t nk = (jobs[j].lv.c + E.chunk_cols() - 1) / E.chunk_cols();
-            const int64_t seg = std::max<int64_t>(1, budget / E.chunk_bytes());
+            const int64_t seg = std::max<int64_t>(1, split_limit / E.chunk_bytes());  // few, large segments
             for (int64_t off = 0; off < total; ++off)
                 for (int64_t k0 = 0; k0 < nk; k0 += seg) {
                     KRange kr;

@@ -177,6 +177,79 @@ __device__ __forceinline__ float rff_entry(const DevModel& M, int64_t col, int64
 
 // ------------------------------------------------------------ generator
 
+// Gauss fp32 phase: 128 rows of A (IS_A) or 128 columns of B for the 16 chunk
+// columns.  Thread = (row quad qq, column pair cp): one float4 mean load and
+// one Philox block (4 normals) per column, 64-bit stores of the column pair
+// per row (hi and lo tiles).  Padding columns carry j = 0 and B weight 0.
+static_assert(GEN_T == 256 && TBK == 16 && TBM == 128, "gauss_phase_f32 thread map: 8 column pairs x 32 row quads");
+template <bool IS_A>
+__device__ __forceinline__ void gauss_phase_f32(const DevModel& M, const Tables& T, uint64_t key, int64_t rb,
+                                                const int* s_j, const float* s_w, unsigned char* thi,
+                                                unsigned char* tlo, int tid) {
+    const int cp = tid & 7, qq = tid >> 3;
+    const int r0 = 4 * qq;
+    const int64_t dim = IS_A ? M.m : M.p;
+    const int64_t lim = dim - rb;
+    const float* mbase = (IS_A ? M.mean_at_f : M.mean_b_f) + rb + r0;
+    const uint32_t rowq = (uint32_t)((rb + r0) >> 2);
+    const float sd = (float)M.sd;
+    float v[2][4];
+    if (r0 + 3 < lim && (dim & 3) == 0) {
+        int jj[2];
+        float4 mv[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            jj[u] = s_j[2 * cp + u];
+            mv[u] = __ldg(reinterpret_cast<const float4*>(mbase + (int64_t)jj[u] * dim));
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const u32x4 r = philox((uint32_t)jj[u], rowq, 0, IS_A ? MLSK_CTR_A : MLSK_CTR_B, key);
+            float z[4];
+            box_muller_f(r.x, r.y, z[0], z[1], T);
+            box_muller_f(r.z, r.w, z[2], z[3], T);
+            const float m4[4] = {mv[u].x, mv[u].y, mv[u].z, mv[u].w};
+            const float w = IS_A ? 1.0f : s_w[2 * cp + u];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float x = __fadd_rn(m4[e], __fmul_rn(sd, z[e]));
+                v[u][e] = IS_A ? x : __fmul_rn(w, x);
+            }
+        }
+    } else {
+        // ragged edge: rows past the matrix are zero
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int j = s_j[2 * cp + u];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[u][e] = 0.f;
+            if (r0 < lim) {
+                const float* mp = mbase + (int64_t)j * dim;
+                float mv[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) mv[e] = r0 + e < lim ? __ldg(mp + e) : 0.f;
+                const u32x4 r = philox((uint32_t)j, rowq, 0, IS_A ? MLSK_CTR_A : MLSK_CTR_B, key);
+                float z[4];
+                box_muller_f(r.x, r.y, z[0], z[1], T);
+                box_muller_f(r.z, r.w, z[2], z[3], T);
+                const float w = IS_A ? 1.0f : s_w[2 * cp + u];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (r0 + e < lim) {
+                        const float x = __fadd_rn(mv[e], __fmul_rn(sd, z[e]));
+                        v[u][e] = IS_A ? x : __fmul_rn(w, x);
+                    }
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int off = sw_off(r0 + e, 2 * cp);  // chunk columns 2cp, 2cp+1: adjacent words
+        *reinterpret_cast<float2*>(thi + off) = make_float2(v[0][e], v[1][e]);
+        *reinterpret_cast<float2*>(tlo + off) = make_float2(tf32_lo(v[0][e]), tf32_lo(v[1][e]));
+    }
+}
+
 // work item (b, kc): 32 sampled columns; phases of 128 rows of A / cols of B;
 // hi and lo tiles staged in shared memory in the SW128 layout, then copied out.
 __global__ void __launch_bounds__(GEN_T)
@@ -208,7 +281,7 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
         __syncthreads();
         if (tid < TBK) {
             const int64_t t = (kc0 + kc) * TBK + tid;  // column of the sample (kc0: first chunk of this K-range)
-            int j = -1;
+            int j = 0;  // padding columns (t >= c): column 0 with weight 0 (B = 0)
             float w = 0.f;
             if (t < c) {
                 const u32x4 r = philox((uint32_t)(t >> 1), 0, 0, MLSK_CTR_INDEX, key);
@@ -225,54 +298,15 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
             const bool isA = ph < a_ph;
             const int64_t rb = (int64_t)(isA ? ph : ph - a_ph) * TBM;
             const int64_t lim = isA ? M.m - rb : M.p - rb;
-            const bool quad_aligned = ((isA ? M.m : M.p) & 3) == 0;
             if (M.kind == MLSK_MODEL_GAUSS_MEAN) {
-                // one Philox block -> 4 normals for rows 4q..4q+3 of one column
-                // lanes span the 32 columns of a row quad: conflict-free SW128 stores
-                for (int item = tid; item < (TBM / 4) * TBK; item += GEN_T) {
-                    const int tt = item & (TBK - 1), qd = item / TBK;
-                    const int r0 = 4 * qd;
-                    const int j = s_j[tt];
-                    float v[4] = {0.f, 0.f, 0.f, 0.f};
-                    if (j >= 0 && r0 < lim) {
-                        // mean quad first (vector load when aligned) so its latency hides behind the RNG
-                        const float* mp = isA ? M.mean_at_f + (int64_t)j * M.m + rb + r0
-                                              : M.mean_b_f + (int64_t)j * M.p + rb + r0;
-                        float mv[4];
-                        if (quad_aligned && r0 + 3 < lim) {
-                            const float4 q4 = __ldg(reinterpret_cast<const float4*>(mp));
-                            mv[0] = q4.x; mv[1] = q4.y; mv[2] = q4.z; mv[3] = q4.w;
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) mv[e] = r0 + e < lim ? __ldg(mp + e) : 0.f;
-                        }
-                        const u32x4 r = philox((uint32_t)j, (uint32_t)((rb + r0) >> 2), 0,
-                                               isA ? MLSK_CTR_A : MLSK_CTR_B, key);
-                        float z[4];
-                        box_muller_f(r.x, r.y, z[0], z[1], T);
-                        box_muller_f(r.z, r.w, z[2], z[3], T);
-                        const float sd = (float)M.sd;
-                        const float w = isA ? 1.0f : s_w[tt];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            if (r0 + e < lim) {
-                                const float x = __fadd_rn(mv[e], __fmul_rn(sd, z[e]));
-                                v[e] = isA ? x : __fmul_rn(w, x);
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        *reinterpret_cast<float*>(thi + sw_off(r0 + e, tt)) = v[e];
-                        *reinterpret_cast<float*>(tlo + sw_off(r0 + e, tt)) = tf32_lo(v[e]);
-                    }
-                }
+                if (isA) gauss_phase_f32<true>(M, T, key, rb, s_j, s_w, thi, tlo, tid);
+                else gauss_phase_f32<false>(M, T, key, rb, s_j, s_w, thi, tlo, tid);
             } else {
                 for (int item = tid; item < TBM * TBK; item += GEN_T) {
                     const int tt = item & (TBK - 1), rr = item / TBK;
                     const int j = s_j[tt];
                     float v = 0.f;
-                    if (j >= 0 && rr < lim) {
+                    if (rr < lim) {
                         float x;
                         if (M.kind == MLSK_MODEL_STUDENT_T) x = student_t_entry(S, key, j, rb + rr, isA ? 0 : 1, T);
                         else x = rff_entry(M, j, rb + rr);  // RFF: B = A^T

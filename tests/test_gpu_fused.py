@@ -114,5 +114,6 @@ def test_fused_f64_samples_split_along_k(gpu, monkeypatch):
     plan = gpu.LevelPlan(2, 2, [5, 3, 2], c0=256)  # per-sample panels 2 .. 8 MiB
     re_ = gpu.mlmc_matmul(model, gpu.target_identity(), plan, 13, gpu.EstimatorOptions(engine="exact"))
     monkeypatch.setenv("MLSK_PANEL_BUDGET_MB", "1")
+    monkeypatch.setenv("MLSK_SPLIT_MB", "1")
     rs = gpu.mlmc_matmul(model, gpu.target_identity(), plan, 13, gpu.EstimatorOptions(engine="fused"))
     compare_reports(rs, re_)

@@ -72,5 +72,6 @@ def test_tc_samples_split_along_k(gpu, name, monkeypatch):
     plan = gpu.LevelPlan(2, 2, [5, 3, 2], c0=256)  # c = 256, 512, 1024 -> 1 .. 8 segments per sample
     re_ = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="exact"))
     monkeypatch.setenv("MLSK_PANEL_BUDGET_MB", "1")
+    monkeypatch.setenv("MLSK_SPLIT_MB", "1")
     rs = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
     check(rs, re_)
