@@ -85,7 +85,35 @@ class ClockSampler:
         self._t = None
 
     def __enter__(self):
-        def run():
+        # NVML (microseconds per query) at ~20 ms intervals; nvidia-smi (100+ ms
+        # per call) only when pynvml is unavailable
+        nv = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = [getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+                    getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+                    getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+                    getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4)]
+        except Exception:
+            nv = None
+
+        def run_nvml():
+            while not self._stop.is_set():
+                try:
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    try:
+                        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    except Exception:
+                        r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                    self.rows.append([str(sm), str(mx), "", ""] + ["Active" if r & b else "Not Active" for b in bits])
+                except Exception:
+                    pass
+                self._stop.wait(0.1)  # sparse: NVML queries contend with the launching thread
+
+        def run_smi():
             while not self._stop.is_set():
                 try:
                     out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
@@ -96,7 +124,7 @@ class ClockSampler:
                 except Exception:
                     pass
                 self._stop.wait(0.2)
-        self._t = threading.Thread(target=run, daemon=True)
+        self._t = threading.Thread(target=run_nvml if nv is not None else run_smi, daemon=True)
         self._t.start()
         return self
 
