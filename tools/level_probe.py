@@ -1,0 +1,42 @@
+"""Per-level kernel times of the config-2 round (diagnostics): each level of the
+bench step alone, serialised generator / GEMM, event-timed per kernel."""
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_1904_00429_b200 import mlsketch as g  # noqa: E402
+from paper_1904_00429_b200._lib import lib  # noqa: E402
+
+L = lib()
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)
+opts = g.EstimatorOptions(stream=stream.cuda_stream, engine="fused")
+model = g.gaussian_mean_matrix_model(256, 4096, 256, sd=0.5, data_seed=bench.data_seed())
+name = C.create_string_buffer(64)
+nl, ms = C.c_int64(), C.c_double()
+for lvl in range(7):
+    N = [0] * 7
+    N[lvl] = bench.STEP_N[lvl]
+    sess = g.MlmcSession(model, g.target_identity(), 2, 6, 1, c0=32, options=opts)
+    sess.run_round(N)
+    torch.cuda.synchronize()
+    L.mlsk_profile_reset()
+    L.mlsk_profile_enable(1)
+    for _ in range(3):
+        sess.run_round(N)
+    torch.cuda.synchronize()
+    L.mlsk_profile_enable(0)
+    out = {}
+    for i in range(L.mlsk_profile_read(0, name, 64, C.byref(nl), C.byref(ms))):
+        L.mlsk_profile_read(i, name, 64, C.byref(nl), C.byref(ms))
+        out[name.value.decode()] = round(ms.value / 3, 3)
+    c = 32 * 2 ** lvl
+    flops = 2.0 * 256 * 256 * c * N[lvl]
+    gemm = out.get("gemm_f64", 0)
+    print(f"level {lvl} c={c:5d} N={N[lvl]:6d}  " + "  ".join(f"{k} {v:.3f} ms" for k, v in out.items()) +
+          f"  gemm {flops / (gemm * 1e-3) / 1e12 if gemm else 0:.1f} TFLOP/s")
+    sess.close()
