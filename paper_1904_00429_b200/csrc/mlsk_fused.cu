@@ -99,7 +99,7 @@ __device__ __forceinline__ void gen_phase(const DevModel& M, const Tables& T, ui
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             jj[u] = s_j[tq + 4 * u];  // padding columns carry j = 0 (and B weight 0)
-            mv[u] = __ldg(reinterpret_cast<const double2*>(mrow + (int64_t)jj[u] * dim));
+            mv[u] = __ldg(reinterpret_cast<const double2*>(mrow + (uint64_t)(uint32_t)jj[u] * (uint32_t)dim));
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -190,23 +190,33 @@ k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restr
             s_w[tid] = w;
         }
         __syncthreads();
+        double* const baseA = Apan + ((int64_t)b * nkc + kc) * MP * KC;
+        double* const baseB = Bpan + ((int64_t)b * nkc + kc) * PP * KC;
         for (int ph = 0; ph < a_phases + b_phases; ++ph) {
             const bool isA = ph < a_phases;
-            const int64_t rb = (int64_t)(isA ? ph : ph - a_phases) * GROWS;
-            const int64_t span = isA ? MP - rb : PP - rb;     // rows / cols in the panel
+            const int rb = (isA ? ph : ph - a_phases) * GROWS;
+            const int span = (int)(isA ? MP : PP) - rb;  // rows / cols in the panel
             double* tl = gen_dyn + buf * (GROWS * KC);
             if (isA) gen_phase<true>(M, T, key, rb, s_j, s_w, tl, tid);
             else gen_phase<false>(M, T, key, rb, s_j, s_w, tl, tid);
+            // the tile leaves by one bulk copy (TMA engine), not by the threads
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
-            double* base = isA ? Apan + (((int64_t)b * nkc + kc) * MP + rb) * KC
-                               : Bpan + (((int64_t)b * nkc + kc) * PP + rb) * KC;
-            const int n2 = (int)((span < GROWS ? span : GROWS) * KC / 2);
-            double2* dst = reinterpret_cast<double2*>(base);
-            const double2* src = reinterpret_cast<const double2*>(tl);
-            for (int i = tid; i < n2; i += GEN_THREADS) dst[i] = src[i];
-            buf ^= 1;  // next phase writes the other tile; no second barrier needed
+            if (tid == 0) {
+                double* dst = (isA ? baseA : baseB) + (int64_t)rb * KC;
+                const uint32_t bytes = (uint32_t)((span < GROWS ? span : GROWS) * KC * 8);
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                             "r"((uint32_t)__cvta_generic_to_shared(tl)), "r"(bytes)
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                // the other tile's copy (previous phase) has finished reading
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            }
+            __syncthreads();
+            buf ^= 1;
         }
     }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------- mbarriers
