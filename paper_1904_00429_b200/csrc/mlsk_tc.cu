@@ -257,8 +257,7 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                   int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kc0,
                   float* __restrict__ Ahi, float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
                   uint32_t* __restrict__ idx_out) {
-    __shared__ __align__(1024) unsigned char thi[TTILE];
-    __shared__ __align__(1024) unsigned char tlo[TTILE];
+    __shared__ __align__(1024) unsigned char tbuf[2][2][TTILE];  // [buffer][hi / lo], double-buffered
     __shared__ __align__(16) float2 s_sc[64];
     __shared__ __align__(16) float2 s_lg[64];
     __shared__ int s_j[TBK];
@@ -274,6 +273,7 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
     const int tid = threadIdx.x;
     const int64_t items = (int64_t)nb * nkc;
     const int a_ph = (int)(MP / TBM), b_ph = (int)(PP / TBM);  // 128-row phases (a B tile is two)
+    int buf = 0;
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const int b = (int)(it / nkc);
         const int64_t kc = it - (int64_t)b * nkc;
@@ -298,6 +298,8 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
             const bool isA = ph < a_ph;
             const int64_t rb = (int64_t)(isA ? ph : ph - a_ph) * TBM;
             const int64_t lim = isA ? M.m - rb : M.p - rb;
+            unsigned char* thi = tbuf[buf][0];
+            unsigned char* tlo = tbuf[buf][1];
             if (M.kind == MLSK_MODEL_GAUSS_MEAN) {
                 if (isA) gauss_phase_f32<true>(M, T, key, rb, s_j, s_w, thi, tlo, tid);
                 else gauss_phase_f32<false>(M, T, key, rb, s_j, s_w, thi, tlo, tid);
@@ -316,19 +318,27 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                     *reinterpret_cast<float*>(tlo + sw_off(rr, tt)) = tf32_lo(v);
                 }
             }
+            // both tiles leave by bulk copies (TMA engine), not by the threads
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
-            const int64_t off = (((int64_t)b * nkc + kc) * (isA ? MP : PP) + rb) * TBK;
-            float4* dh = reinterpret_cast<float4*>((isA ? Ahi : Bhi) + off);
-            float4* dl = reinterpret_cast<float4*>((isA ? Alo : Blo) + off);
-            const float4* sh = reinterpret_cast<const float4*>(thi);
-            const float4* sl = reinterpret_cast<const float4*>(tlo);
-            for (int i = tid; i < TTILE / 16; i += GEN_T) {
-                dh[i] = sh[i];
-                dl[i] = sl[i];
+            if (tid == 0) {
+                const int64_t off = (((int64_t)b * nkc + kc) * (isA ? MP : PP) + rb) * TBK;
+                float* dh = (isA ? Ahi : Bhi) + off;
+                float* dl = (isA ? Alo : Blo) + off;
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dh),
+                             "r"((uint32_t)__cvta_generic_to_shared(thi)), "r"((uint32_t)TTILE)
+                             : "memory");
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dl),
+                             "r"((uint32_t)__cvta_generic_to_shared(tlo)), "r"((uint32_t)TTILE)
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // the other buffer is free
             }
             __syncthreads();
+            buf ^= 1;
         }
     }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // RFF features: Z[x][j] = sqrt(2/n) cos(w_j . x + b_j).  A_S = Z[:, S] and
