@@ -36,7 +36,7 @@ namespace {
 constexpr int KC = 16;        // K-chunk (indices per smem stage)
 constexpr int BM = 128;       // tile rows
 constexpr int BN = 64;        // tile cols
-constexpr int STAGES = 4;
+constexpr int STAGES = 6;
 constexpr int CONSUMERS = 8;  // consumer warps (4 x 2 of 32 x 32)
 constexpr int GEMM_THREADS = CONSUMERS * 32;  // lane 0 of warp 0 also produces
 constexpr int A_STAGE_BYTES = BM * KC * 8;
