@@ -37,8 +37,15 @@ constexpr int KC = 16;        // K-chunk (indices per smem stage)
 constexpr int BM = 128;       // tile rows
 constexpr int BN = 64;        // tile cols
 constexpr int STAGES = 6;
-constexpr int CONSUMERS = 8;  // consumer warps (4 x 2 of 32 x 32)
+#ifndef MLSK_GEMM_WN
+#define MLSK_GEMM_WN 32
+#endif
+constexpr int WN = MLSK_GEMM_WN;          // warp tile: 32 rows x WN columns
+constexpr int WARPS_N = BN / WN;
+constexpr int NJ = WN / 8;                // 8-column DMMA tiles per warp
+constexpr int CONSUMERS = (BM / 32) * WARPS_N;  // consumer warps
 constexpr int GEMM_THREADS = CONSUMERS * 32;  // lane 0 of warp 0 also produces
+constexpr int GEMM_MAXNREG = CONSUMERS == 8 ? 192 : 128;
 constexpr int A_STAGE_BYTES = BM * KC * 8;
 constexpr int B_STAGE_BYTES = BN * KC * 8;
 constexpr int GEN_THREADS = 256;
@@ -284,7 +291,7 @@ struct GemmShape {
 // SPLIT: one sample split along K per launch (split_part 1 first, 2 middle,
 // 3 last); a separate instantiation keeps the common path's registers intact.
 template <bool SPLIT>
-__global__ void __maxnreg__(192)
+__global__ void __maxnreg__(GEMM_MAXNREG)
 k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, GemmShape sh,
            double* __restrict__ part, double* __restrict__ part_sq, int split_part, double* __restrict__ ypart) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -337,13 +344,13 @@ k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, Gem
         while (p_it < iters && p_it < STAGES - 1) produce();
 
     // ---------------------------------------------------- consumer warps
-    const int wi = warp >> 1, wj = warp & 1;
+    const int wi = warp / WARPS_N, wj = warp % WARPS_N;
     const int gid = lane >> 2, tig = lane & 3;
-    double acc[4][4][2], S[4][4][2];
+    double acc[4][NJ][2], S[4][NJ][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < NJ; ++j) {
             acc[i][j][0] = acc[i][j][1] = 0.0;
             S[i][j][0] = S[i][j][1] = 0.0;
         }
@@ -353,7 +360,7 @@ k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, Gem
     const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
     // per-lane fragment offsets (bytes) inside a stage: rows wi*32 + 8i + gid,
     // cols wj*32 + 8j + gid, granules (2 tig + h) ^ gid
-    const uint32_t a_off = (uint32_t)((wi * 32 + gid) * KC * 8), b_off = (uint32_t)((wj * 32 + gid) * KC * 8);
+    const uint32_t a_off = (uint32_t)((wi * 32 + gid) * KC * 8), b_off = (uint32_t)((wj * WN + gid) * KC * 8);
     const uint32_t g0 = (uint32_t)((((2 * tig) ^ gid) << 4)), g1 = (uint32_t)((((2 * tig + 1) ^ gid) << 4));
     int s = 0;
     uint32_t ph = 0;
@@ -363,33 +370,33 @@ k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, Gem
         const uint32_t a_st = a_base + s * A_STAGE_BYTES + a_off;
         const uint32_t b_st = b_base + s * B_STAGE_BYTES + b_off;
         // all fragments of the stage first (16 x LDS.128), then 64 DMMAs
-        double2 af0[4], bf0[4], af1[4], bf1[4];
+        double2 af0[4], bf0[NJ], af1[4], bf1[NJ];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             af0[i] = lds128(a_st + i * (8 * KC * 8) + g0);
             af1[i] = lds128(a_st + i * (8 * KC * 8) + g1);
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < NJ; ++j) {
             bf0[j] = lds128(b_st + j * (8 * KC * 8) + g0);
             bf1[j] = lds128(b_st + j * (8 * KC * 8) + g1);
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af0[i].x, bf0[j].x);
+            for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], af0[i].x, bf0[j].x);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af0[i].y, bf0[j].y);
+            for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], af0[i].y, bf0[j].y);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af1[i].x, bf1[j].x);
+            for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], af1[i].x, bf1[j].x);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af1[i].y, bf1[j].y);
+            for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], af1[i].y, bf1[j].y);
         __syncwarp();
         if (lane == 0) mbar_arrive(empty0 + 8 * s);
         if (producer && p_it < iters) produce();
@@ -405,8 +412,8 @@ k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, Gem
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        double2* q2 = reinterpret_cast<double2*>(yp + (wi * 32 + 8 * i + gid) * BN + wj * 32 + 8 * j +
+                    for (int j = 0; j < NJ; ++j) {
+                        double2* q2 = reinterpret_cast<double2*>(yp + (wi * 32 + 8 * i + gid) * BN + wj * WN + 8 * j +
                                                                  2 * tig);
                         if (split_part >= 2) {
                             const double2 pv = *q2;
@@ -424,7 +431,7 @@ k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, Gem
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
+                for (int j = 0; j < NJ; ++j)
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
                         const double y = acc[i][j][e];
@@ -440,9 +447,9 @@ k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, Gem
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < NJ; ++j) {
             const int r = wi * 32 + 8 * i + gid;
-            const int q = wj * 32 + 8 * j + 2 * tig;
+            const int q = wj * WN + 8 * j + 2 * tig;
             *reinterpret_cast<double2*>(out + r * BN + q) = make_double2(S[i][j][0], S[i][j][1]);
         }
     sq = warp_sum(sq);
