@@ -29,7 +29,21 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// The caller's current device is restored on return: entry points select
+// their device (mlsk_exec_opts.device / the session's) only for the call.
+struct DeviceRestore {
+    int dev = -1;
+    DeviceRestore() {
+        if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
+    }
+    ~DeviceRestore() {
+        int now = -1;
+        if (dev >= 0 && cudaGetDevice(&now) == cudaSuccess && now != dev) cudaSetDevice(dev);
+    }
+};
+
 int guard(const std::function<void()>& body) {
+    DeviceRestore restore;
     try {
         body();
         return MLSK_OK;
@@ -509,6 +523,7 @@ int mlsk_session_run_round(mlsk_session* s, const int64_t* dN) {
 int mlsk_session_stats(mlsk_session* s, mlsk_report* rep) {
     return guard([&] {
         if (!s || !rep) invalid("session: null argument");
+        MLSK_CUDA(cudaSetDevice(s->ex->device));
         const int64_t cells = s->R.model.rows * s->R.model.cols;
         std::vector<double> value(cells, 0.0);
         int64_t total_cost = 0;
@@ -559,6 +574,7 @@ int mlsk_session_level_buffer(mlsk_session* s, void** device_ptr, int64_t* n_dou
 int mlsk_session_synchronize(mlsk_session* s) {
     return guard([&] {
         if (!s) invalid("session: null argument");
+        MLSK_CUDA(cudaSetDevice(s->ex->device));
         MLSK_CUDA(cudaStreamSynchronize(s->ex->stream));
     });
 }
@@ -566,6 +582,7 @@ int mlsk_session_synchronize(mlsk_session* s) {
 int mlsk_session_destroy(mlsk_session* s) {
     return guard([&] {
         if (!s) return;
+        cudaSetDevice(s->ex->device);
         cudaStreamSynchronize(s->ex->stream);
         delete s;
     });
