@@ -455,6 +455,10 @@ struct TcShape {
     int64_t nkc;
     int64_t MP, PP;
     int T, Gs, tiles_n;
+    // Gs == 1 (one CTA per tile): running sums go straight into the level
+    // total (rows x cols, row-major) -- no partial buffer, no reduction pass
+    double* direct;
+    int64_t rows, cols;
 };
 
 // SPLIT: one sample split along K per launch (split_part 1 first, 2 middle,
@@ -613,14 +617,18 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             aph ^= 1u << abuf;
             abuf ^= 1;
             if ((smp + 1) % FLUSH == 0 || smp + 1 == my_samples) {
+                // this thread's 64 consecutive columns: the CTA partial, or (direct,
+                // tile-aligned outputs only) the level total itself, row-major
+                double* o = sh.direct ? sh.direct + ((int64_t)tm * TBM + row) * sh.cols + (int64_t)tn * TBN + h * HC
+                                      : out;
 #pragma unroll
                 for (int i0 = 0; i0 < HC; i0 += 8) {
-                    double o[8];
+                    double ov[8];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) o[i] = out[i0 + i];
+                    for (int i = 0; i < 8; ++i) ov[i] = o[i0 + i];
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        out[i0 + i] = o[i] + (double)S[i0 + i];
+                        o[i0 + i] = ov[i] + (double)S[i0 + i];
                         S[i0 + i] = 0.f;
                     }
                     asm volatile("" ::: "memory");  // bound the live doubles: 8 at a time
@@ -729,13 +737,16 @@ class TcEngine final : public PanelEngine {
         double* part = ws_.partial.p;
         double* part_sq = part + (size_t)T_ * Gs_ * (TBM * TBN);
         const bool finishes = kr.part == 0 || kr.part == 3;  // samples complete in this launch
-        if (finishes) MLSK_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * (size_t)T_ * Gs_ * (TBM * TBN), s));
+        // one CTA per tile and a tile-aligned output: sums straight into the level total
+        const bool direct = Gs_ == 1 && M_.rows % TBM == 0 && M_.cols % TBN == 0;
+        if (finishes && !direct)
+            MLSK_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * (size_t)T_ * Gs_ * (TBM * TBN), s));
         float* ypart = nullptr;
         if (kr.part != 0) {
             ws_.ypart.ensure((size_t)T_ * TBM * TBN);  // the carried partial Y of a split sample
             ypart = ws_.ypart.p;
         }
-        TcShape sh{nb, k, MP_, PP_, T_, Gs_, tiles_n_};
+        TcShape sh{nb, k, MP_, PP_, T_, Gs_, tiles_n_, direct ? st.total() : nullptr, M_.rows, M_.cols};
         {
             Prof p("gemm_tf32x3", s);
             if (kr.part == 0)
@@ -752,8 +763,9 @@ class TcEngine final : public PanelEngine {
         {
             Prof p("reduce_tiles_tc", s);
             const int64_t cells = M_.rows * M_.cols;
-            k_reduce_tiles_tc<<<(int)std::min<int64_t>((cells + 255) / 256, (int64_t)nsm_ * 8), 256, 0, s>>>(
-                part, part_sq, sh, M_.rows, M_.cols, st.total(), st.total_sq());
+            // direct mode: only the squares are left to add (cells = 0)
+            k_reduce_tiles_tc<<<direct ? 1 : (int)std::min<int64_t>((cells + 255) / 256, (int64_t)nsm_ * 8), 256, 0,
+                                s>>>(part, part_sq, sh, direct ? 0 : M_.rows, M_.cols, st.total(), st.total_sq());
         }
         launched(2);
     }

@@ -75,3 +75,14 @@ def test_tc_samples_split_along_k(gpu, name, monkeypatch):
     monkeypatch.setenv("MLSK_SPLIT_MB", "1")
     rs = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
     check(rs, re_)
+
+
+def test_tc_direct_accumulation_one_cta_per_tile(gpu):
+    """Outputs with >= 148 tiles and tile-aligned shapes (configs 4 and 5) put
+    one CTA per tile, which adds its running sums straight into the level
+    total (no partial buffer / reduction pass)."""
+    model = gpu.gaussian_mean_matrix_model(1536, 2048, 2560, sd=1.0, data_seed=17, dtype=1)  # 12 x 10 tiles
+    plan = gpu.LevelPlan(2, 1, [6, 3], c0=32)
+    rf = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
+    re_ = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="exact"))
+    check(rf, re_)
