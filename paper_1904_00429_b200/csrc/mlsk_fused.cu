@@ -977,6 +977,9 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
             continue;
         }
         int64_t max_nb = std::max<int64_t>(1, budget / per);
+        // every CTA group needs a sample: stretch the batch (up to 4x the budget)
+        // rather than leave groups idle (config 3's deepest level: 268 MB samples)
+        if (max_nb < Gs && Gs * per <= 4 * budget) max_nb = Gs;
         if (max_nb > Gs) max_nb = max_nb / Gs * Gs;
         for (int64_t off = 0; off < total; off += max_nb) {
             const int nb = (int)std::min<int64_t>(max_nb, total - off);
