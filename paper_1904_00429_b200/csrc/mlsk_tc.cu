@@ -141,8 +141,8 @@ __device__ __forceinline__ float student_t_entry(const TcModel& S, uint64_t key,
                                                  const Tables& T) {
     const u32x4 r = philox((uint32_t)col, (uint32_t)rq, (uint32_t)which, MLSK_CTR_T, key);
     float z[4];
-    box_muller_f(r.x, r.y, z[0], z[1], T);
-    box_muller_f(r.z, r.w, z[2], z[3], T);
+    box_muller_f<true>(r.x, r.y, z[0], z[1], T);
+    box_muller_f<true>(r.z, r.w, z[2], z[3], T);
     const float v = __fadd_rn(__fadd_rn(__fmul_rn(z[1], z[1]), __fmul_rn(z[2], z[2])), __fmul_rn(z[3], z[3]));
     const float t = __fdiv_rn(z[0], __fsqrt_rn(__fdiv_rn(v, 3.0f)));
     const uint64_t e = which == 0 ? (uint64_t)rq * (uint64_t)S.M.n + (uint64_t)col
@@ -184,14 +184,14 @@ __device__ __forceinline__ void gauss_phase_f32(const DevModel& M, const Tables&
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             jj[u] = s_j[2 * cp + u];
-            mv[u] = __ldg(reinterpret_cast<const float4*>(mbase + (int64_t)jj[u] * dim));
+            mv[u] = __ldg(reinterpret_cast<const float4*>(mbase + (uint64_t)(uint32_t)jj[u] * (uint32_t)dim));
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const u32x4 r = philox((uint32_t)jj[u], rowq, 0, IS_A ? MLSK_CTR_A : MLSK_CTR_B, key);
             float z[4];
-            box_muller_f(r.x, r.y, z[0], z[1], T);
-            box_muller_f(r.z, r.w, z[2], z[3], T);
+            box_muller_f<true>(r.x, r.y, z[0], z[1], T);
+            box_muller_f<true>(r.z, r.w, z[2], z[3], T);
             const float m4[4] = {mv[u].x, mv[u].y, mv[u].z, mv[u].w};
             const float w = IS_A ? 1.0f : s_w[2 * cp + u];
 #pragma unroll
@@ -214,8 +214,8 @@ __device__ __forceinline__ void gauss_phase_f32(const DevModel& M, const Tables&
                 for (int e = 0; e < 4; ++e) mv[e] = r0 + e < lim ? __ldg(mp + e) : 0.f;
                 const u32x4 r = philox((uint32_t)j, rowq, 0, IS_A ? MLSK_CTR_A : MLSK_CTR_B, key);
                 float z[4];
-                box_muller_f(r.x, r.y, z[0], z[1], T);
-                box_muller_f(r.z, r.w, z[2], z[3], T);
+                box_muller_f<true>(r.x, r.y, z[0], z[1], T);
+                box_muller_f<true>(r.z, r.w, z[2], z[3], T);
                 const float w = IS_A ? 1.0f : s_w[2 * cp + u];
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
@@ -242,15 +242,13 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                   float* __restrict__ Ahi, float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
                   uint32_t* __restrict__ idx_out) {
     __shared__ __align__(1024) unsigned char tbuf[2][2][TTILE];  // [buffer][hi / lo], double-buffered
-    __shared__ __align__(16) float2 s_sc[64];
+    __shared__ __align__(16) float2 s_sc[256];  // full-circle sincos table
     __shared__ __align__(16) float2 s_lg[64];
     __shared__ int s_j[TBK];
     __shared__ float s_w[TBK];
     const DevModel& M = S.M;
-    for (int i = threadIdx.x; i < 64; i += blockDim.x) {
-        s_sc[i] = reinterpret_cast<const float2*>(M.tab.sincos_f)[i];
-        s_lg[i] = reinterpret_cast<const float2*>(M.tab.log_f)[i];
-    }
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_sc[i] = full_circle_entry_f(i, M.tab.sincos_f);
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) s_lg[i] = reinterpret_cast<const float2*>(M.tab.log_f)[i];
     Tables T = M.tab;
     T.sincos_f = reinterpret_cast<const float*>(s_sc);
     T.log_f = reinterpret_cast<const float*>(s_lg);
