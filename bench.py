@@ -48,7 +48,9 @@ METRIC = "MLMC level-samples/s (config 2: 256x4096x256 fp64, c_l=32*2^l, L=6, st
 UNIT = "level-samples/s"
 
 
-GPU_WARM_S = 2.5  # seconds of device warm-up (memory writes + DMMA) before the warm-up steps
+# seconds of device warm-up (memory writes + DMMA) before the warm-up steps;
+# MLSK_BENCH_WARM_S=0 for profiler passes (keeps the launch list to the steps)
+GPU_WARM_S = float(os.environ.get("MLSK_BENCH_WARM_S", "2.5"))
 
 
 def flops_of(N):
