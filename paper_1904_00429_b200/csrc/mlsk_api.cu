@@ -128,12 +128,20 @@ struct Exec {
         if (o && o->stream) {
             stream = (cudaStream_t)o->stream;
         } else {
-            MLSK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-            owns = true;
+            // one library stream per (thread, device), reused by every call: the
+            // stream-ordered pool then recycles the per-call allocations in order
+            // (a fresh stream per call made pool reuse opportunistic and call
+            // times erratic)
+            static thread_local std::map<int, cudaStream_t> streams;
+            auto it = streams.find(device);
+            if (it == streams.end()) {
+                cudaStream_t st;
+                MLSK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+                it = streams.emplace(device, st).first;
+            }
+            stream = it->second;
+            owns = true;  // library stream: calls synchronise before returning
         }
-    }
-    ~Exec() {
-        if (owns && stream) cudaStreamDestroy(stream);
     }
 };
 
