@@ -11,7 +11,9 @@ import os
 
 from . import _abi as abi
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libmlsk.so")
+# MLSK_LIB_PATH: an alternative build of the same library (A/B experiments, tools/build_variant.py)
+LIB_PATH = os.environ.get("MLSK_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                          "libmlsk.so")
 
 _P = C.POINTER
 _lib = None

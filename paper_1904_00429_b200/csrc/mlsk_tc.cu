@@ -35,13 +35,19 @@ namespace {
 
 constexpr int TBM = 128, TBN = 256, TBK = 16;       // TBK tf32 = 64 bytes per row (SWIZZLE_64B)
 constexpr int ROWB = TBK * 4;                       // bytes per K-chunk row
-constexpr int TSTAGES = 4;
+#ifndef MLSK_TC_STAGES
+#define MLSK_TC_STAGES 4
+#endif
+constexpr int TSTAGES = MLSK_TC_STAGES;             // 4 x 48 KB (3 stages: 6% slower GEMM, no gain from a co-resident generator CTA)
 constexpr int TTILE = TBM * TBK * 4;                // 8 KB: one 128-row K-chunk (A tile, half a B tile)
 constexpr int TA_BYTES = TTILE, TB_BYTES = 2 * TTILE;
 constexpr int TSTAGE_BYTES = 2 * TA_BYTES + 2 * TB_BYTES;  // A_hi, A_lo, B_hi, B_lo: 48 KB
 constexpr int EPI_WARPS = 16;                       // four per TMEM lane quadrant (64-column quarters)
 constexpr int TC_THREADS = 64 + 32 * EPI_WARPS;     // producer, MMA, epilogue warps
-constexpr int FLUSH = 32;                           // samples per fp32 running-sum flush
+#ifndef MLSK_TC_FLUSH
+#define MLSK_TC_FLUSH 32
+#endif
+constexpr int FLUSH = MLSK_TC_FLUSH;                // samples per fp32 running-sum flush
 constexpr uint32_t TMEM_COLS = 2 * TBN;             // two accumulators: all 512 columns
 constexpr int GEN_T = 256;
 
@@ -234,9 +240,13 @@ __device__ __forceinline__ void gauss_phase_f32(const DevModel& M, const Tables&
     }
 }
 
-// work item (b, kc): 32 sampled columns; phases of 128 rows of A / cols of B;
-// hi and lo tiles staged in shared memory in the SW128 layout, then copied out.
-__global__ void __launch_bounds__(GEN_T)
+// work item (b, kc): 16 sampled columns; phases of 128 rows of A / cols of B;
+// hi and lo tiles staged in shared memory in the SW64 layout, then copied out
+// by the TMA engine.
+#ifndef MLSK_GEN_TF32_MINB
+#define MLSK_GEN_TF32_MINB 1
+#endif
+__global__ void __launch_bounds__(GEN_T, MLSK_GEN_TF32_MINB)
 k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
                   int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kc0,
                   float* __restrict__ Ahi, float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
@@ -496,6 +506,9 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             for (int64_t it = 0; it < iters; ++it) {
                 bar_wait(empty0 + 8 * s, ph ^ 1);
                 const uint32_t full = full0 + 8 * s;
+#ifdef MLSK_TC_ABL_NOLD  // ablation (timing only, wrong results): no operand loads
+                bar_arrive(full);
+#else
                 bar_expect_tx(full, TSTAGE_BYTES);
                 const int64_t oa = ((b * sh.nkc + kc) * sh.MP + (int64_t)tm * TBM) * TBK;
                 const int64_t ob = ((b * sh.nkc + kc) * sh.PP + (int64_t)tn * TBN) * TBK;
@@ -504,6 +517,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 bulk_load(st + TA_BYTES, Alo + oa, TA_BYTES, full);
                 bulk_load(st + 2 * TA_BYTES, Bhi + ob, TB_BYTES, full);
                 bulk_load(st + 2 * TA_BYTES + TB_BYTES, Blo + ob, TB_BYTES, full);
+#endif
                 if (++s == TSTAGES) { s = 0; ph ^= 1; }
                 if (++kc == sh.nkc) { kc = 0; b += sh.Gs; }
             }
@@ -531,9 +545,11 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                     const uint64_t ah = sw_desc(st + kk * 32), al = sw_desc(st + TA_BYTES + kk * 32);
                     const uint64_t bh = sw_desc(st + 2 * TA_BYTES + kk * 32);
                     const uint64_t bl = sw_desc(st + 2 * TA_BYTES + TB_BYTES + kk * 32);
+#ifndef MLSK_TC_ABL_NOMMA  // ablation: no MMAs (commits only)
                     tc_mma_tf32(dcol, ah, bh, idesc, (kc > 0 || kk > 0) ? 1u : 0u);
                     tc_mma_tf32(dcol, ah, bl, idesc, 1u);
                     tc_mma_tf32(dcol, al, bh, idesc, 1u);
+#endif
                 }
                 tc_commit(empty0 + 8 * s);  // smem stage free once these MMAs complete
                 if (++s == TSTAGES) { s = 0; ph ^= 1; }
@@ -556,7 +572,11 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
 #pragma unroll
         for (int i = 0; i < HC; ++i) S[i] = 0.f;
         double sq = 0.0;
-        double* out = part + (int64_t)g * (TBM * TBN) + (int64_t)row * TBN + h * HC;
+        // per-CTA partial tile, column-major ([col][row]): for a fixed column the
+        // 32 lanes (rows) of a warp touch 256 contiguous bytes, so a flush is 2 x 64
+        // coalesced accesses per thread (row-major flushes cost 0.9 ms per config-3
+        // level 0: one 32-byte sector per 8-byte access)
+        double* out = part + (int64_t)g * (TBM * TBN) + (int64_t)(h * HC) * TBM + row;
         int abuf = 0;
         uint32_t aph = 0;  // bit a = phase of accumulator a (no indexed local array)
         for (int smp = 0; smp < my_samples; ++smp) {
@@ -570,7 +590,11 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
 #pragma unroll
             for (int ch = 0; ch < HC / 16; ++ch) {
                 float y[16];
+#ifdef MLSK_TC_ABL_NOEPI  // ablation: no accumulator reads
+                for (int i = 0; i < 16; ++i) y[i] = (float)i;
+#else
                 tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * TBN + h * HC + ch * 16), y);
+#endif
                 if (SPLIT && split_part >= 2) {  // middle / last segment: add the carried partial
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
@@ -599,21 +623,39 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             aph ^= 1u << abuf;
             abuf ^= 1;
             if ((smp + 1) % FLUSH == 0 || smp + 1 == my_samples) {
-                // this thread's 64 consecutive columns: the CTA partial, or (direct,
-                // tile-aligned outputs only) the level total itself, row-major
-                double* o = sh.direct ? sh.direct + ((int64_t)tm * TBM + row) * sh.cols + (int64_t)tn * TBN + h * HC
-                                      : out;
+                if (sh.direct) {
+                    // (tile-aligned outputs, one CTA per tile) this thread's 64
+                    // consecutive columns of the row-major level total, 16 bytes a time
+                    double2* o = reinterpret_cast<double2*>(sh.direct + ((int64_t)tm * TBM + row) * sh.cols +
+                                                            (int64_t)tn * TBN + h * HC);
 #pragma unroll
-                for (int i0 = 0; i0 < HC; i0 += 8) {
-                    double ov[8];
+                    for (int i0 = 0; i0 < HC / 2; i0 += 4) {
+                        double2 ov[4];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) ov[i] = o[i0 + i];
+                        for (int i = 0; i < 4; ++i) ov[i] = o[i0 + i];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        o[i0 + i] = ov[i] + (double)S[i0 + i];
-                        S[i0 + i] = 0.f;
+                        for (int i = 0; i < 4; ++i) {
+                            ov[i].x += (double)S[2 * (i0 + i)];
+                            ov[i].y += (double)S[2 * (i0 + i) + 1];
+                            o[i0 + i] = ov[i];
+                            S[2 * (i0 + i)] = 0.f;
+                            S[2 * (i0 + i) + 1] = 0.f;
+                        }
+                        asm volatile("" ::: "memory");  // bound the live doubles: 8 at a time
                     }
-                    asm volatile("" ::: "memory");  // bound the live doubles: 8 at a time
+                } else {
+#pragma unroll
+                    for (int i0 = 0; i0 < HC; i0 += 8) {
+                        double ov[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) ov[i] = out[(i0 + i) * TBM];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            out[(i0 + i) * TBM] = ov[i] + (double)S[i0 + i];
+                            S[i0 + i] = 0.f;
+                        }
+                        asm volatile("" ::: "memory");
+                    }
                 }
             }
         }
@@ -633,20 +675,39 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
     }
 }
 
-__global__ void k_reduce_tiles_tc(const double* __restrict__ part, const double* __restrict__ part_sq, TcShape sh,
-                                  int64_t rows, int64_t cols, double* __restrict__ total,
-                                  double* __restrict__ total_sq) {
-    const int64_t cells = rows * cols;
-    for (int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cell < cells;
-         cell += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = cell / cols, q = cell - r * cols;
-        const int tile = (int)((r / TBM) * sh.tiles_n + q / TBN);
-        const int64_t off = (r % TBM) * TBN + (q % TBN);
-        double acc = 0.0;
-        for (int grp = 0; grp < sh.Gs; ++grp) acc += part[(int64_t)(grp * sh.T + tile) * (TBM * TBN) + off];
-        total[cell] += acc;
+// level total (row-major rows x cols) += sum over the Gs group partials of
+// each tile (column-major [col][row] per CTA); 32 x 32 cell blocks through
+// shared memory so both the partial reads and the total updates coalesce.
+// Block (32, 8); grid covers the cell blocks (grid-stride).
+__global__ void __launch_bounds__(256) k_reduce_tiles_tc(const double* __restrict__ part,
+                                                         const double* __restrict__ part_sq, TcShape sh,
+                                                         int64_t rows, int64_t cols, double* __restrict__ total,
+                                                         double* __restrict__ total_sq) {
+    __shared__ double blk[32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t brows = (rows + 31) / 32, bcols = (cols + 31) / 32;
+    for (int64_t bi = blockIdx.x; bi < brows * bcols; bi += gridDim.x) {
+        const int64_t r0 = (bi / bcols) * 32, q0 = (bi % bcols) * 32;
+        // read: lane = row (contiguous in the column-major partial)
+        for (int k = ty; k < 32; k += 8) {
+            const int64_t r = r0 + tx, q = q0 + k;
+            double acc = 0.0;
+            if (r < rows && q < cols) {
+                const int tile = (int)((r / TBM) * sh.tiles_n + q / TBN);
+                const int64_t off = (q % TBN) * TBM + (r % TBM);
+                for (int grp = 0; grp < sh.Gs; ++grp) acc += part[(int64_t)(grp * sh.T + tile) * (TBM * TBN) + off];
+            }
+            blk[tx][k] = acc;
+        }
+        __syncthreads();
+        // write: lane = column (contiguous in the row-major total)
+        for (int k = ty; k < 32; k += 8) {
+            const int64_t r = r0 + k, q = q0 + tx;
+            if (r < rows && q < cols) total[r * cols + q] += blk[k][tx];
+        }
+        __syncthreads();
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (blockIdx.x == 0 && tx == 0 && ty == 0) {
         double acc = 0.0;
         for (int g = 0; g < sh.T * sh.Gs; ++g) acc += part_sq[g];
         *total_sq += acc;
@@ -682,12 +743,20 @@ class TcEngine final : public PanelEngine {
         S_.M = M.dm;
         smem_ = TSTAGES * TSTAGE_BYTES + 1024;
         ws_.partial.ensure((size_t)T_ * Gs_ * (TBM * TBN) + (size_t)T_ * Gs_);
+        // generator grid cap (CTAs; grid-stride beyond it).  MLSK_TC_GEN_CTAS_PER_SM
+        // (experiments): 0 = one work item per CTA
+        gen_cap_ = (int64_t)nsm_ * 8;
         rff_smem_ = 4 * RFF_CH * TTILE + (RFF_DMAX * TBM + RFF_DMAX * RFF_COLS) * 4;
         const int smem = smem_, rsmem = rff_smem_;
         once_per_device((const void*)&k_gemm_tf32x3<false>, [smem, rsmem] {
             MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_rff, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem));
+            // full shared-memory carveout for every kernel of the pipeline, so a
+            // generator CTA never leaves an SM configured too small for a GEMM CTA
+            MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_tf32, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         });
     }
     int64_t chunk_cols() const override { return TBK; }
@@ -706,7 +775,7 @@ class TcEngine final : public PanelEngine {
                 S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi, Blo,
                 idx);
         } else {
-            k_gen_panels_tf32<<<(int)std::min<int64_t>((int64_t)nb * k, (int64_t)nsm_ * 8), GEN_T, 0, s>>>(
+            k_gen_panels_tf32<<<(int)std::min<int64_t>((int64_t)nb * k, gen_cap_), GEN_T, 0, s>>>(
                 S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi, Blo,
                 idx);
         }
@@ -746,8 +815,9 @@ class TcEngine final : public PanelEngine {
             Prof p("reduce_tiles_tc", s);
             const int64_t cells = M_.rows * M_.cols;
             // direct mode: only the squares are left to add (cells = 0)
-            k_reduce_tiles_tc<<<direct ? 1 : (int)std::min<int64_t>((cells + 255) / 256, (int64_t)nsm_ * 8), 256, 0,
-                                s>>>(part, part_sq, sh, direct ? 0 : M_.rows, M_.cols, st.total(), st.total_sq());
+            k_reduce_tiles_tc<<<direct ? 1 : (int)std::min<int64_t>((cells + 1023) / 1024, (int64_t)nsm_ * 8),
+                                dim3(32, 8), 0, s>>>(part, part_sq, sh, direct ? 0 : M_.rows, M_.cols, st.total(),
+                                                     st.total_sq());
         }
         launched(2);
     }
@@ -766,6 +836,7 @@ class TcEngine final : public PanelEngine {
     Workspace& ws_;
     TcModel S_{};
     int nsm_, T_, Gs_, tiles_n_, smem_, rff_smem_;
+    int64_t gen_cap_;
     int64_t MP_, PP_;
 };
 

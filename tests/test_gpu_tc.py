@@ -27,12 +27,15 @@ def models(g):
     return {
         "gauss_f32": g.gaussian_mean_matrix_model(256, 4096, 384, sd=1.0, mean_lo=-1.0, mean_hi=1.0, data_seed=7,
                                                   dtype=f32),
+        # m % 128 == 0 and p % 256 == 0: the generator's mean-prefetch path
+        "gauss_f32_aligned": g.gaussian_mean_matrix_model(256, 4096, 512, sd=1.0, mean_lo=-1.0, mean_hi=1.0,
+                                                          data_seed=8, dtype=f32),
         "student_t": g.student_t_matrix_model(256, 8192, 128, data_seed=9),
         "rff": g.rff_gram_model(256, 4096, dim=64, sigma=4.0, data_seed=11),
     }
 
 
-@pytest.mark.parametrize("name", ["gauss_f32", "student_t", "rff"])
+@pytest.mark.parametrize("name", ["gauss_f32", "gauss_f32_aligned", "student_t", "rff"])
 def test_tc_engine_vs_exact(gpu, name):
     model = models(gpu)[name]
     plan = gpu.LevelPlan(2, 2, [37, 20, 9], c0=64)
@@ -61,7 +64,7 @@ def test_tc_probe_indices_match_exact(gpu):
     assert seen["fused"] == seen["exact"] and len(seen["fused"]) == 3
 
 
-@pytest.mark.parametrize("name", ["gauss_f32", "student_t", "rff"])
+@pytest.mark.parametrize("name", ["gauss_f32", "gauss_f32_aligned", "student_t", "rff"])
 def test_tc_samples_split_along_k(gpu, name, monkeypatch):
     """Level-samples whose panels exceed a batch run as K-segments of one
     sample with the partial Y carried in device memory (BASELINE config 5's

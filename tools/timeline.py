@@ -13,14 +13,20 @@ L = lib()
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 opts = g.EstimatorOptions(stream=stream.cuda_stream, engine="fused")
-model = g.gaussian_mean_matrix_model(256, 4096, 256, sd=0.5, data_seed=bench.data_seed())
-sess = g.MlmcSession(model, g.target_identity(), 2, 6, 1, c0=32, options=opts)
+if len(sys.argv) > 1 and sys.argv[1] == "3":  # config 3 (fp32, 3xTF32 engine)
+    model = g.gaussian_mean_matrix_model(1024, 16384, 1024, sd=1.0, data_seed=3, dtype=1)
+    sess = g.MlmcSession(model, g.target_identity(), 2, 8, 1, c0=64, options=opts)
+    STEP = [8 * 2 ** (8 - l) for l in range(9)]
+else:
+    model = g.gaussian_mean_matrix_model(256, 4096, 256, sd=0.5, data_seed=bench.data_seed())
+    sess = g.MlmcSession(model, g.target_identity(), 2, 6, 1, c0=32, options=opts)
+    STEP = bench.STEP_N
 for _ in range(3):
-    sess.run_round(bench.STEP_N)
+    sess.run_round(STEP)
 torch.cuda.synchronize()
 L.mlsk_profile_reset()
 L.mlsk_profile_enable(1)
-sess.run_round(bench.STEP_N)
+sess.run_round(STEP)
 torch.cuda.synchronize()
 L.mlsk_profile_enable(0)
 name = C.create_string_buffer(64)
