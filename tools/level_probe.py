@@ -14,7 +14,7 @@ from paper_1904_00429_b200._lib import lib  # noqa: E402
 import argparse  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--config", type=int, default=2, choices=[2, 3])
+ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5])
 args = ap.parse_args()
 L = lib()
 stream = torch.cuda.Stream()
@@ -25,10 +25,16 @@ if args.config == 2:
     m = p = 256
     c0, LV, STEP = 32, 6, bench.STEP_N
     gemm_name = "gemm_f64"
-else:
+elif args.config == 3:
     model = g.gaussian_mean_matrix_model(1024, 16384, 1024, sd=1.0, data_seed=3, dtype=1)
     m = p = 1024
     c0, LV, STEP = 64, 8, [8 * 2 ** (8 - l) for l in range(9)]
+    gemm_name = "gemm_tf32x3"
+else:  # configs 4 and 5 as tools/bench_configs.py defines them
+    from tools.bench_configs import configs as _cfgs  # noqa: E402
+    cf = _cfgs()[args.config]
+    model, m, p, c0, STEP = cf["model"], cf["m"], cf["p"], cf["c0"], cf["N"]
+    LV = len(STEP) - 1
     gemm_name = "gemm_tf32x3"
 name = C.create_string_buffer(64)
 nl, ms = C.c_int64(), C.c_double()

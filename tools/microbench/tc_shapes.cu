@@ -35,7 +35,7 @@ __device__ __forceinline__ void wait_bar(uint32_t b, uint32_t ph) {
 // epi: epilogue warps read the other accumulator in a loop
 template <int PAIR>
 __global__ void __launch_bounds__(THREADS, 1) k_tc(int rounds, int rowb, int pattern, int epi, int stages,
-                                                   uint32_t* sink) {
+                                                   int N, uint32_t* sink) {
     extern __shared__ __align__(1024) unsigned char sm[];
     unsigned char* base = sm + ((1024 - (sa(sm) & 1023)) & 1023);
     __shared__ __align__(8) uint64_t bar[2];
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_tc(int rounds, int rowb, int pat
     if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
     // per-CTA stage: A hi / lo (128 rows) + B hi / lo (N rows held by this CTA)
     const int kchunk = rowb / 4;                     // tf32 per row
-    const int nrows_b = PAIR ? 128 : 256;            // B rows held in this CTA's smem
+    const int nrows_b = PAIR ? N / 2 : N;            // B rows held in this CTA's smem
     const int a_bytes = 128 * rowb, b_bytes = nrows_b * rowb;
     const int stage_bytes = 2 * a_bytes + 2 * b_bytes;
     for (int i = threadIdx.x; i < stages * stage_bytes / 4; i += blockDim.x) {
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_tc(int rounds, int rowb, int pat
     const uint32_t tmem = s_tmem;
     if (warp == 1 && threadIdx.x == 32 && rank == 0) {
         const uint32_t s0 = sa(base);
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) |
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
                                ((uint32_t)((PAIR ? 256 : 128) >> 4) << 24);
         uint32_t ph[2] = {0, 0};
         int s = 0;
@@ -139,6 +139,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_tc(int rounds, int rowb, int pat
         }
         for (int i = ngrp >= 2 ? ngrp - 2 : 0; i < ngrp; ++i) { wait_bar(sa(&bar[i & 1]), ph[i & 1]); ph[i & 1] ^= 1; }
         s_stop = 1;
+        if (PAIR) {  // the peer's epilogue warps stop too
+            uint32_t remote;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 1;" : "=r"(remote) : "r"(sa((const void*)&s_stop)));
+            asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(remote), "r"(1) : "memory");
+        }
     }
     if (warp >= 2 && epi) {
         // read the other accumulator (columns 256..511) until the MMA thread is done
@@ -183,7 +188,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_tc(int rounds, int rowb, int pat
 }
 
 template <int PAIR>
-float run(int sms, int rounds, int rowb, int pattern, int epi, int stages, uint32_t* sink, int smem) {
+float run(int sms, int rounds, int rowb, int pattern, int epi, int stages, int N, uint32_t* sink, int smem) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(PAIR ? (sms / 2) * 2 : sms);
     cfg.blockDim = dim3(THREADS);
@@ -198,12 +203,12 @@ float run(int sms, int rounds, int rowb, int pattern, int epi, int stages, uint3
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    cudaLaunchKernelEx(&cfg, k_tc<PAIR>, 2, rowb, pattern, epi, stages, sink);
+    cudaLaunchKernelEx(&cfg, k_tc<PAIR>, 2, rowb, pattern, epi, stages, N, sink);
     cudaDeviceSynchronize();
     float best = 1e30f;
     for (int r = 0; r < 3; ++r) {
         cudaEventRecord(e0);
-        cudaLaunchKernelEx(&cfg, k_tc<PAIR>, rounds, rowb, pattern, epi, stages, sink);
+        cudaLaunchKernelEx(&cfg, k_tc<PAIR>, rounds, rowb, pattern, epi, stages, N, sink);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
@@ -224,26 +229,24 @@ int main() {
     cudaFuncSetAttribute(k_tc<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     int rnd = 1;
     cudaMemcpyToSymbol(g_random, &rnd, sizeof(int));
-    for (int pair = 0; pair < 1; ++pair)
-        for (int rowb : {64, 128})
-            for (int pattern : {0, 1})
-                for (int epi : {0, 1}) {
-                    if (!pattern) continue;
-                    const int stage_bytes = 2 * 128 * rowb + 2 * (pair ? 128 : 256) * rowb;
-                    int stages = (192 * 1024) / stage_bytes;
-                    if (stages > 4) stages = 4;
-                    const int rounds = 4000;
-                    float ms = pair ? run<1>(sms, rounds, rowb, pattern, epi, stages, sink, smem)
-                                    : run<0>(sms, rounds, rowb, pattern, epi, stages, sink, smem);
-                    const int ctas = pair ? (sms / 2) * 2 : sms;
-                    const double per_round = (double)(rowb / 4 / 8) * (pattern ? 3 : 1);  // MMAs per round
-                    // flops per MMA: 2 * M * N * K, M = 128 per CTA (pair: 256 per leader = 128 per CTA)
-                    const double flops = (double)ctas * rounds * per_round * 2.0 * 128 * 256 * 8;
-                    printf("{\"random\": 1, \"pair\": %d, \"rowb\": %d, \"pattern\": \"%s\", \"epi\": %d, \"stages\": %d, \"tflops\": %.1f, "
-                           "\"err\": \"%s\"}\n",
-                           pair, rowb, pattern ? "3xtf32" : "single", epi, stages, flops / (ms * 1e-3) / 1e12,
-                           cudaGetErrorString(cudaGetLastError()));
-                    fflush(stdout);
-                }
+    const int cases[4][2] = {{0, 256}, {0, 128}, {1, 256}, {1, 128}};  // (pair, N)
+    for (const auto& cs : cases)
+        for (int epi : {0, 1}) {
+            const int pair = cs[0], N = cs[1], rowb = 64, pattern = 1;
+            const int stage_bytes = 2 * 128 * rowb + 2 * (pair ? N / 2 : N) * rowb;
+            int stages = (192 * 1024) / stage_bytes;
+            if (stages > 4) stages = 4;
+            const int rounds = 4000;
+            float ms = pair ? run<1>(sms, rounds, rowb, pattern, epi, stages, N, sink, smem)
+                            : run<0>(sms, rounds, rowb, pattern, epi, stages, N, sink, smem);
+            const int ctas = pair ? (sms / 2) * 2 : sms;
+            const double per_round = (double)(rowb / 4 / 8) * 3;  // MMAs per round
+            // flops per CTA per MMA: 2 * 128 * N * 8 (pair: M = 256 over two CTAs)
+            const double flops = (double)ctas * rounds * per_round * 2.0 * 128 * N * 8;
+            printf("{\"random\": 1, \"pair\": %d, \"N\": %d, \"rowb\": %d, \"epi\": %d, \"stages\": %d, "
+                   "\"tflops\": %.1f, \"err\": \"%s\"}\n",
+                   pair, N, rowb, epi, stages, flops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+            fflush(stdout);
+        }
     return 0;
 }
