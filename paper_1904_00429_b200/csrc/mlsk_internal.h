@@ -127,7 +127,7 @@ struct Model {
     int64_t rows = 1, cols = 1;
     int64_t ref_u64 = 0;  // u64 the reference draw consumes before the indices
     DevArray<double> cum, mean_a, mean_b, mean_at, paper_b;
-    DevArray<float> mean_a_f, mean_b_f, mean_at_f, rff_x, rff_w, rff_b;
+    DevArray<float> mean_a_f, mean_b_f, mean_at_f, rff_x, rff_xt, rff_w, rff_b;
 };
 
 // Validates the descriptor (the reference's constructor checks) and builds it.

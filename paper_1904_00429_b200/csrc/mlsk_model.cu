@@ -285,6 +285,9 @@ void build_model(Model& M, const mlsk_model_desc* d, cudaStream_t st) {
         k_phases_f32<<<grid_for(D.n), 256, 0, st>>>(M.rff_b.p, D.n, derive_seed(D.data_seed, MLSK_TAG_DATA, 4));
         launched(3);
         dm.rff_x = M.rff_x.p;
+        M.rff_xt.alloc_on(D.m * Dd, st);
+        transpose<float>(M.rff_x.p, M.rff_xt.p, D.m, Dd, st);
+        dm.rff_xt = M.rff_xt.p;
         dm.rff_w = M.rff_w.p;
         dm.rff_b = M.rff_b.p;
         dm.rff_dim = Dd;

@@ -388,21 +388,39 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
         }
         for (int64_t rb = 0; rb < (MP > PP ? MP : PP); rb += TBM) {  // A rows / B columns (m == p)
             const int64_t lim = M.m - rb;
-            for (int e = tid; e < TBM * D; e += GEN_T) {
-                const int r = e / D, d = e - r * D;
-                xs[d * TBM + r] = r < lim ? M.rff_x[(rb + r) * D + d] : 0.f;
+            // X tile from the transposed copy: rows contiguous per dimension, so
+            // the global reads coalesce and the shared stores are conflict-free
+            if (lim >= TBM && (M.m & 3) == 0) {
+                for (int e = tid; e < TBM / 4 * D; e += GEN_T) {
+                    const int d = e / (TBM / 4), r4 = e - d * (TBM / 4);
+                    reinterpret_cast<float4*>(xs + d * TBM)[r4] =
+                        __ldg(reinterpret_cast<const float4*>(M.rff_xt + (int64_t)d * M.m + rb) + r4);
+                }
+            } else {
+                for (int e = tid; e < TBM * D; e += GEN_T) {
+                    const int d = e / TBM, r = e - d * TBM;
+                    xs[d * TBM + r] = r < lim ? M.rff_xt[(int64_t)d * M.m + rb + r] : 0.f;
+                }
             }
             __syncthreads();
-            // lane = column t (W reads conflict-free), warp = RPT consecutive rows (X reads broadcast)
+            // lane = column t (W reads conflict-free), warp = RPT consecutive rows (X reads broadcast, 16 bytes)
             constexpr int RPT = TBM * RFF_COLS / GEN_T;
+            static_assert(RPT % 4 == 0, "float4 X reads");
             const int t = tid % RFF_COLS, r0 = (tid / RFF_COLS) * RPT;
             float acc[RPT];
 #pragma unroll
             for (int i = 0; i < RPT; ++i) acc[i] = 0.f;
             for (int d = 0; d < D; ++d) {
                 const float w = wsm[d * RFF_COLS + t];
+                const float4* xr = reinterpret_cast<const float4*>(xs + d * TBM + r0);
 #pragma unroll
-                for (int i = 0; i < RPT; ++i) acc[i] = __fmaf_rn(xs[d * TBM + r0 + i], w, acc[i]);
+                for (int i4 = 0; i4 < RPT / 4; ++i4) {
+                    const float4 xv = xr[i4];
+                    acc[4 * i4] = __fmaf_rn(xv.x, w, acc[4 * i4]);
+                    acc[4 * i4 + 1] = __fmaf_rn(xv.y, w, acc[4 * i4 + 1]);
+                    acc[4 * i4 + 2] = __fmaf_rn(xv.z, w, acc[4 * i4 + 2]);
+                    acc[4 * i4 + 3] = __fmaf_rn(xv.w, w, acc[4 * i4 + 3]);
+                }
             }
             const bool valid = s_j[t] >= 0;
             const float bt = s_b[t], wt = s_w[t];
