@@ -240,13 +240,47 @@ __device__ __forceinline__ void gauss_phase_f32(const DevModel& M, const Tables&
     }
 }
 
+// Student-t(3) phase (config 5): same thread map as the gauss phase (a row
+// quad x a chunk-column pair per thread, 64-bit stores of the pair per row);
+// the eight entries are independent (two Philox blocks each: the t draw and
+// the on-the-fly mean), so the unrolled loop keeps many chains in flight.
+template <bool IS_A>
+__device__ __forceinline__ void student_t_phase_f32(const TcModel& S, const Tables& T, uint64_t key, int64_t rb,
+                                                    const int* s_j, const float* s_w, unsigned char* thi,
+                                                    unsigned char* tlo, int tid) {
+    const int cp = tid & 7, qq = tid >> 3;
+    const int r0 = 4 * qq;
+    const int64_t lim = (IS_A ? S.M.m : S.M.p) - rb;
+    float v[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const int j = s_j[2 * cp + u];
+        const float w = IS_A ? 1.0f : s_w[2 * cp + u];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            float x = 0.f;
+            if (r0 + e < lim) {
+                x = student_t_entry(S, key, j, rb + r0 + e, IS_A ? 0 : 1, T);
+                if (!IS_A) x = __fmul_rn(w, x);
+            }
+            v[u][e] = x;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int off = sw_off(r0 + e, 2 * cp);
+        *reinterpret_cast<float2*>(thi + off) = make_float2(v[0][e], v[1][e]);
+        *reinterpret_cast<float2*>(tlo + off) = make_float2(tf32_lo(v[0][e]), tf32_lo(v[1][e]));
+    }
+}
+
 // work item (b, kc): 16 sampled columns; phases of 128 rows of A / cols of B;
 // hi and lo tiles staged in shared memory in the SW64 layout, then copied out
 // by the TMA engine.
-#ifndef MLSK_GEN_TF32_MINB
-#define MLSK_GEN_TF32_MINB 1
-#endif
-__global__ void __launch_bounds__(GEN_T, MLSK_GEN_TF32_MINB)
+// KIND: GK_GAUSS, GK_STUDENT_T, or GK_GENERIC (per-entry loop: RFF with D > 64)
+constexpr int GK_GAUSS = 0, GK_STUDENT_T = 1, GK_GENERIC = 2;
+template <int KIND>
+__global__ void __launch_bounds__(GEN_T, KIND == GK_GAUSS ? 5 : KIND == GK_STUDENT_T ? 3 : 1)
 k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
                   int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kc0,
                   float* __restrict__ Ahi, float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
@@ -292,9 +326,12 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
             const int64_t lim = isA ? M.m - rb : M.p - rb;
             unsigned char* thi = tbuf[buf][0];
             unsigned char* tlo = tbuf[buf][1];
-            if (M.kind == MLSK_MODEL_GAUSS_MEAN) {
+            if (KIND == GK_GAUSS) {
                 if (isA) gauss_phase_f32<true>(M, T, key, rb, s_j, s_w, thi, tlo, tid);
                 else gauss_phase_f32<false>(M, T, key, rb, s_j, s_w, thi, tlo, tid);
+            } else if (KIND == GK_STUDENT_T) {
+                if (isA) student_t_phase_f32<true>(S, T, key, rb, s_j, s_w, thi, tlo, tid);
+                else student_t_phase_f32<false>(S, T, key, rb, s_j, s_w, thi, tlo, tid);
             } else {
                 for (int item = tid; item < TBM * TBK; item += GEN_T) {
                     const int tt = item & (TBK - 1), rr = item / TBK;
@@ -303,7 +340,7 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                     if (rr < lim) {
                         float x;
                         if (M.kind == MLSK_MODEL_STUDENT_T) x = student_t_entry(S, key, j, rb + rr, isA ? 0 : 1, T);
-                        else x = rff_entry(M, j, rb + rr);  // RFF: B = A^T
+                        else x = rff_entry(M, j, rb + rr);  // RFF (D > 64): B = A^T
                         v = isA ? x : __fmul_rn(s_w[tt], x);
                     }
                     *reinterpret_cast<float*>(thi + sw_off(rr, tt)) = v;
@@ -772,7 +809,9 @@ class TcEngine final : public PanelEngine {
             MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_rff, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem));
             // full shared-memory carveout for every kernel of the pipeline, so a
             // generator CTA never leaves an SM configured too small for a GEMM CTA
-            MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_tf32, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_tf32<GK_GAUSS>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_tf32<GK_STUDENT_T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_tf32<GK_GENERIC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
             MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
             MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         });
@@ -793,9 +832,19 @@ class TcEngine final : public PanelEngine {
                 S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi, Blo,
                 idx);
         } else {
-            k_gen_panels_tf32<<<(int)std::min<int64_t>((int64_t)nb * k, gen_cap_), GEN_T, 0, s>>>(
-                S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi, Blo,
-                idx);
+            const int grid = (int)std::min<int64_t>((int64_t)nb * k, gen_cap_);
+            if (M_.dm.kind == MLSK_MODEL_GAUSS_MEAN)
+                k_gen_panels_tf32<GK_GAUSS><<<grid, GEN_T, 0, s>>>(S_, seed, tag, ks, nb, c, cc, (float)w_fine,
+                                                                  (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi,
+                                                                  Blo, idx);
+            else if (M_.dm.kind == MLSK_MODEL_STUDENT_T)
+                k_gen_panels_tf32<GK_STUDENT_T><<<grid, GEN_T, 0, s>>>(S_, seed, tag, ks, nb, c, cc, (float)w_fine,
+                                                                      (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo,
+                                                                      Bhi, Blo, idx);
+            else
+                k_gen_panels_tf32<GK_GENERIC><<<grid, GEN_T, 0, s>>>(S_, seed, tag, ks, nb, c, cc, (float)w_fine,
+                                                                    (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi,
+                                                                    Blo, idx);
         }
         launched();
     }
