@@ -583,10 +583,9 @@ __global__ void k_reduce_tiles(const double* __restrict__ part, const double* __
         for (int grp = 0; grp < sh.Gs; ++grp) acc += part[(int64_t)(grp * sh.T + tile) * (RBM * RBN) + off];
         total[cell] += acc;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        double acc = 0.0;
-        for (int g = 0; g < sh.T * sh.Gs; ++g) acc += part_sq[g];
-        *total_sq += acc;
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        const double acc = warp_sum_array(part_sq, sh.T * sh.Gs, threadIdx.x);
+        if (threadIdx.x == 0) *total_sq += acc;
     }
 }
 

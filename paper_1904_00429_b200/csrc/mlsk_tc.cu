@@ -762,10 +762,9 @@ __global__ void __launch_bounds__(256) k_reduce_tiles_tc(const double* __restric
         }
         __syncthreads();
     }
-    if (blockIdx.x == 0 && tx == 0 && ty == 0) {
-        double acc = 0.0;
-        for (int g = 0; g < sh.T * sh.Gs; ++g) acc += part_sq[g];
-        *total_sq += acc;
+    if (blockIdx.x == 0 && ty == 0) {
+        const double acc = warp_sum_array(part_sq, sh.T * sh.Gs, tx);
+        if (tx == 0) *total_sq += acc;
     }
 }
 
