@@ -21,6 +21,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch  # noqa: E402
 
+import bench  # noqa: E402
 from paper_1904_00429_b200 import mlsketch as g  # noqa: E402
 from paper_1904_00429_b200._lib import lib  # noqa: E402
 
@@ -87,13 +88,14 @@ def main():
         L.mlsk_profile_reset()
         L.mlsk_profile_enable(1)
         times = []
-        for _ in range(args.reps):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            sess.run_round(c["N"])
-            e1.record(stream)
-            e1.synchronize()
-            times.append(e0.elapsed_time(e1))
+        with bench.ClockSampler(0) as clk:  # SM clocks / throttle reasons while the timed rounds run
+            for _ in range(args.reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                sess.run_round(c["N"])
+                e1.record(stream)
+                e1.synchronize()
+                times.append(e0.elapsed_time(e1))
         L.mlsk_profile_enable(0)
         kern = profile_read(L)
         ms = sum(times) / len(times)
@@ -110,6 +112,7 @@ def main():
             "dominant_kernel": dom[0], "dominant_achieved_tflops": dom_rate,
             "peak_tflops": peak, "peak_kind": "3xTF32 = measured dense TF32 / 3" if f32 else "measured fp64 DMMA",
             "frac_of_peak_step": flops / (ms * 1e-3) / 1e12 / peak if peak > 0 else None,
+            "clocks": clk.summary(),
         }), flush=True)
         sess.close()
 
