@@ -440,39 +440,44 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                 }
             }
             __syncthreads();
-            // lane = column t (W reads conflict-free), warp = RPT consecutive rows (X reads broadcast, 16 bytes)
-            constexpr int RPT = TBM * RFF_COLS / GEN_T;
-            static_assert(RPT % 4 == 0, "float4 X reads");
-            const int t = tid % RFF_COLS, r0 = (tid / RFF_COLS) * RPT;
-            float acc[RPT];
+            // thread = 4 consecutive columns x 4 consecutive rows: per dimension one
+            // 16-byte W read and one 16-byte X read (both broadcast within the warp)
+            // feed 16 FMAs; each entry still sums over d in order (rff_entry)
+            static_assert(RFF_COLS == 32 && TBM == 128 && GEN_T == 256, "4 x 4 thread tile map");
+            const int t0 = 4 * (tid & 7), r0 = 4 * (tid >> 3);
+            float acc[4][4];
 #pragma unroll
-            for (int i = 0; i < RPT; ++i) acc[i] = 0.f;
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[i][c] = 0.f;
+#pragma unroll 4
             for (int d = 0; d < D; ++d) {
-                const float w = wsm[d * RFF_COLS + t];
-                const float4* xr = reinterpret_cast<const float4*>(xs + d * TBM + r0);
+                const float4 wv = *reinterpret_cast<const float4*>(wsm + d * RFF_COLS + t0);
+                const float4 xv = *reinterpret_cast<const float4*>(xs + d * TBM + r0);
+                const float xa[4] = {xv.x, xv.y, xv.z, xv.w}, wa[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
-                for (int i4 = 0; i4 < RPT / 4; ++i4) {
-                    const float4 xv = xr[i4];
-                    acc[4 * i4] = __fmaf_rn(xv.x, w, acc[4 * i4]);
-                    acc[4 * i4 + 1] = __fmaf_rn(xv.y, w, acc[4 * i4 + 1]);
-                    acc[4 * i4 + 2] = __fmaf_rn(xv.z, w, acc[4 * i4 + 2]);
-                    acc[4 * i4 + 3] = __fmaf_rn(xv.w, w, acc[4 * i4 + 3]);
-                }
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[i][c] = __fmaf_rn(xa[i], wa[c], acc[i][c]);
             }
-            const bool valid = s_j[t] >= 0;
-            const float bt = s_b[t], wt = s_w[t];
-            const int ch = t / TBK, tt = t % TBK;
+            const int ch = t0 / TBK, tt = t0 % TBK;
 #pragma unroll
-            for (int i = 0; i < RPT; ++i) {
+            for (int i = 0; i < 4; ++i) {
                 const int r = r0 + i;
-                float z = 0.f;
-                if (valid && r < lim) z = scale * cosf(acc[i] + bt);
-                const float v = __fmul_rn(wt, z);
+                float z[4], v[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    z[c] = 0.f;
+                    if (s_j[t0 + c] >= 0 && r < lim) z[c] = scale * cosf(acc[i][c] + s_b[t0 + c]);
+                    v[c] = __fmul_rn(s_w[t0 + c], z[c]);
+                }
                 const int off = ch * TTILE + sw_off(r, tt);
-                *reinterpret_cast<float*>(tiles + off) = z;
-                *reinterpret_cast<float*>(tiles + RFF_CH * TTILE + off) = tf32_lo(z);
-                *reinterpret_cast<float*>(tiles + 2 * RFF_CH * TTILE + off) = v;
-                *reinterpret_cast<float*>(tiles + 3 * RFF_CH * TTILE + off) = tf32_lo(v);
+                *reinterpret_cast<float4*>(tiles + off) = make_float4(z[0], z[1], z[2], z[3]);
+                *reinterpret_cast<float4*>(tiles + RFF_CH * TTILE + off) =
+                    make_float4(tf32_lo(z[0]), tf32_lo(z[1]), tf32_lo(z[2]), tf32_lo(z[3]));
+                *reinterpret_cast<float4*>(tiles + 2 * RFF_CH * TTILE + off) = make_float4(v[0], v[1], v[2], v[3]);
+                *reinterpret_cast<float4*>(tiles + 3 * RFF_CH * TTILE + off) =
+                    make_float4(tf32_lo(v[0]), tf32_lo(v[1]), tf32_lo(v[2]), tf32_lo(v[3]));
             }
             __syncthreads();
 #pragma unroll
