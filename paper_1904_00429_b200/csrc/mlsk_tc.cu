@@ -377,8 +377,15 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
 // transposed for conflict-free reads, W columns broadcast).
 constexpr int RFF_DMAX = 64;
 constexpr int RFF_COLS = 32;               // sampled columns per work item (X tile reuse)
-constexpr int RFF_CH = RFF_COLS / TBK;     // K-chunk tiles per work item
+constexpr int RFF_CH = RFF_COLS / TBK;     // K-chunks per work item
+constexpr int RFF_RSPLIT = 4;              // work items per column group (row-block ranges)
+constexpr int RFF_SMEM = (RFF_DMAX * TBM + RFF_DMAX * RFF_COLS) * 4;  // X tile + W columns (40 KB)
 
+// work item (b, column group of 32 sampled columns, range of 128-row blocks):
+// W columns and (per row block) the X tile in shared memory; each thread
+// owns 4 consecutive columns x 4 consecutive rows and writes its 16-byte row
+// pieces straight into the swizzled panels (no staging tiles: 40 KB of shared
+// memory per CTA, five CTAs per SM).
 __global__ void __launch_bounds__(GEN_T)
 k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
                  int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kcg,
@@ -386,9 +393,8 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                  float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
                  uint32_t* __restrict__ idx_out) {
     extern __shared__ __align__(1024) unsigned char rsm[];
-    unsigned char* tiles = rsm;                                      // [q][ch] K-chunk tiles, q = A hi, A lo, B hi, B lo
-    float* xs = reinterpret_cast<float*>(rsm + 4 * RFF_CH * TTILE);  // [D][128]
-    float* wsm = xs + RFF_DMAX * TBM;                                // [D][RFF_COLS]
+    float* xs = reinterpret_cast<float*>(rsm);  // [D][128]
+    float* wsm = xs + RFF_DMAX * TBM;            // [D][RFF_COLS]
     __shared__ int s_j[RFF_COLS];
     __shared__ float s_w[RFF_COLS], s_b[RFF_COLS];
     const DevModel& M = S.M;
@@ -396,10 +402,17 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
     const int tid = threadIdx.x;
     const float scale = (float)M.rff_scale;
     const int64_t ngrp = (nkc + RFF_CH - 1) / RFF_CH;  // column groups of RFF_CH K-chunks
-    const int64_t items = (int64_t)nb * ngrp;
+    const int64_t nrb = (MP > PP ? MP : PP) / TBM;     // 128-row blocks (A rows / B columns, m == p)
+    const int64_t rb_per = (nrb + RFF_RSPLIT - 1) / RFF_RSPLIT;
+    const int64_t items = (int64_t)nb * ngrp * RFF_RSPLIT;
+    static_assert(RFF_COLS == 32 && TBM == 128 && GEN_T == 256, "4 x 4 thread tile map");
+    const int t0 = 4 * (tid & 7), r0 = 4 * (tid >> 3);
+    const int ch = t0 / TBK, tt = t0 % TBK;
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int b = (int)(it / ngrp);
-        const int64_t kc0 = (it - (int64_t)b * ngrp) * RFF_CH;
+        const int64_t cgi = it / RFF_RSPLIT;
+        const int rs = (int)(it - cgi * RFF_RSPLIT);
+        const int b = (int)(cgi / ngrp);
+        const int64_t kc0 = (cgi - (int64_t)b * ngrp) * RFF_CH;
         const uint64_t key = derive_seed(seed, tag, (uint64_t)ks[b]);
         __syncthreads();
         if (tid < RFF_COLS) {
@@ -411,7 +424,7 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                 const uint32_t ix = index_from_u64((t & 1) ? hi64(r) : lo64(r), M.n, M.log2n, M.cum);
                 j = (int)(ix - 1);
                 w = t < cc ? w_coarse : w_fine;
-                if (idx_out) idx_out[(int64_t)b * c + t] = ix;
+                if (idx_out && rs == 0) idx_out[(int64_t)b * c + t] = ix;
             }
             s_j[tid] = j;
             s_w[tid] = w;
@@ -423,8 +436,22 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
             const int j = s_j[t];
             wsm[d * RFF_COLS + t] = j >= 0 ? M.rff_w[(int64_t)d * M.n + j] : 0.f;
         }
-        for (int64_t rb = 0; rb < (MP > PP ? MP : PP); rb += TBM) {  // A rows / B columns (m == p)
+        // this thread's columns: index, phase and weight are fixed over the item
+        int jv[4];
+        float bv[4], wv4[4];
+#pragma unroll
+        for (int cc4 = 0; cc4 < 4; ++cc4) {
+            jv[cc4] = s_j[t0 + cc4];
+            bv[cc4] = s_b[t0 + cc4];
+            wv4[cc4] = s_w[t0 + cc4];
+        }
+        const int64_t kc = kc0 + ch;
+        const bool col_ok = kc < nkc;
+        const int64_t rb_end = nrb < (rs + 1) * rb_per ? nrb : (rs + 1) * rb_per;
+        for (int64_t rbi = rs * rb_per; rbi < rb_end; ++rbi) {
+            const int64_t rb = rbi * TBM;
             const int64_t lim = M.m - rb;
+            __syncthreads();  // previous X tile consumed
             // X tile from the transposed copy: rows contiguous per dimension, so
             // the global reads coalesce and the shared stores are conflict-free
             if (lim >= TBM && (M.m & 3) == 0) {
@@ -440,16 +467,14 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                 }
             }
             __syncthreads();
-            // thread = 4 consecutive columns x 4 consecutive rows: per dimension one
-            // 16-byte W read and one 16-byte X read (both broadcast within the warp)
-            // feed 16 FMAs; each entry still sums over d in order (rff_entry)
-            static_assert(RFF_COLS == 32 && TBM == 128 && GEN_T == 256, "4 x 4 thread tile map");
-            const int t0 = 4 * (tid & 7), r0 = 4 * (tid >> 3);
+            // per dimension one 16-byte W read and one 16-byte X read (both
+            // broadcast within the warp) feed 16 FMAs; each entry sums over d
+            // in order (rff_entry)
             float acc[4][4];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc[i][c] = 0.f;
+                for (int q = 0; q < 4; ++q) acc[i][q] = 0.f;
 #pragma unroll 4
             for (int d = 0; d < D; ++d) {
                 const float4 wv = *reinterpret_cast<const float4*>(wsm + d * RFF_COLS + t0);
@@ -458,44 +483,33 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) acc[i][c] = __fmaf_rn(xa[i], wa[c], acc[i][c]);
+                    for (int q = 0; q < 4; ++q) acc[i][q] = __fmaf_rn(xa[i], wa[q], acc[i][q]);
             }
-            const int ch = t0 / TBK, tt = t0 % TBK;
+            if (!col_ok) continue;
+            const int64_t oa = (((int64_t)b * nkc + kc) * MP + rb) * TBK;
+            const int64_t ob = (((int64_t)b * nkc + kc) * PP + rb) * TBK;  // B panels are padded to 256
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int r = r0 + i;
                 float z[4], v[4];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    z[c] = 0.f;
-                    if (s_j[t0 + c] >= 0 && r < lim) z[c] = scale * cosf(acc[i][c] + s_b[t0 + c]);
-                    v[c] = __fmul_rn(s_w[t0 + c], z[c]);
-                }
-                const int off = ch * TTILE + sw_off(r, tt);
-                *reinterpret_cast<float4*>(tiles + off) = make_float4(z[0], z[1], z[2], z[3]);
-                *reinterpret_cast<float4*>(tiles + RFF_CH * TTILE + off) =
-                    make_float4(tf32_lo(z[0]), tf32_lo(z[1]), tf32_lo(z[2]), tf32_lo(z[3]));
-                *reinterpret_cast<float4*>(tiles + 2 * RFF_CH * TTILE + off) = make_float4(v[0], v[1], v[2], v[3]);
-                *reinterpret_cast<float4*>(tiles + 3 * RFF_CH * TTILE + off) =
-                    make_float4(tf32_lo(v[0]), tf32_lo(v[1]), tf32_lo(v[2]), tf32_lo(v[3]));
-            }
-            __syncthreads();
-#pragma unroll
-            for (int ch2 = 0; ch2 < RFF_CH; ++ch2) {
-                const int64_t kc = kc0 + ch2;
-                if (kc >= nkc) break;
-                const int64_t oa = (((int64_t)b * nkc + kc) * MP + rb) * TBK;
-                const int64_t ob = (((int64_t)b * nkc + kc) * PP + rb) * TBK;  // B panels are padded to 256
-                float* dst[4] = {Ahi + oa, Alo + oa, Bhi + ob, Blo + ob};
-#pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    if ((q < 2 ? MP : PP) <= rb) continue;
-                    float4* dq = reinterpret_cast<float4*>(dst[q]);
-                    const float4* sq = reinterpret_cast<const float4*>(tiles + (q * RFF_CH + ch2) * TTILE);
-                    for (int i = tid; i < TTILE / 16; i += GEN_T) dq[i] = sq[i];
+                    z[q] = 0.f;
+                    if (jv[q] >= 0 && r < lim) z[q] = scale * cosf(acc[i][q] + bv[q]);
+                    v[q] = __fmul_rn(wv4[q], z[q]);
+                }
+                const int off = sw_off(r, tt) / 4;  // floats
+                if (rb < MP) {
+                    *reinterpret_cast<float4*>(Ahi + oa + off) = make_float4(z[0], z[1], z[2], z[3]);
+                    *reinterpret_cast<float4*>(Alo + oa + off) =
+                        make_float4(tf32_lo(z[0]), tf32_lo(z[1]), tf32_lo(z[2]), tf32_lo(z[3]));
+                }
+                if (rb < PP) {
+                    *reinterpret_cast<float4*>(Bhi + ob + off) = make_float4(v[0], v[1], v[2], v[3]);
+                    *reinterpret_cast<float4*>(Blo + ob + off) =
+                        make_float4(tf32_lo(v[0]), tf32_lo(v[1]), tf32_lo(v[2]), tf32_lo(v[3]));
                 }
             }
-            __syncthreads();
         }
     }
 }
@@ -805,7 +819,7 @@ class TcEngine final : public PanelEngine {
         // generator grid cap (CTAs; grid-stride beyond it).  MLSK_TC_GEN_CTAS_PER_SM
         // (experiments): 0 = one work item per CTA
         gen_cap_ = (int64_t)nsm_ * 8;
-        rff_smem_ = 4 * RFF_CH * TTILE + (RFF_DMAX * TBM + RFF_DMAX * RFF_COLS) * 4;
+        rff_smem_ = RFF_SMEM;
         const int smem = smem_, rsmem = rff_smem_;
         once_per_device((const void*)&k_gemm_tf32x3<false>, [smem, rsmem] {
             MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -831,7 +845,8 @@ class TcEngine final : public PanelEngine {
         split(panels, nb, k, Ahi, Alo, Bhi, Blo);
         Prof p("gen_panels_tf32", s);
         if (M_.dm.kind == MLSK_MODEL_RFF && M_.dm.rff_dim <= RFF_DMAX) {
-            k_gen_panels_rff<<<(int)std::min<int64_t>((int64_t)nb * ((k + RFF_CH - 1) / RFF_CH), (int64_t)nsm_ * 4),
+            k_gen_panels_rff<<<(int)std::min<int64_t>((int64_t)nb * ((k + RFF_CH - 1) / RFF_CH) * RFF_RSPLIT,
+                                                      (int64_t)nsm_ * 5),
                                GEN_T, rff_smem_, s>>>(
                 S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi, Blo,
                 idx);
