@@ -525,6 +525,10 @@ struct TcShape {
     // total (rows x cols, row-major) -- no partial buffer, no reduction pass
     double* direct;
     int64_t rows, cols;
+    // kpar (SPLIT instantiation, one sample): group g of the T-CTA groups takes
+    // K-chunks [g * ceil(nkc / 2), ...) and stores its partial Y into its own
+    // ypart slot; k_kpar_combine forms Y, ||Y||^2 and the level total
+    int kpar;
 };
 
 // SPLIT: one sample split along K per launch (split_part 1 first, 2 middle,
@@ -545,8 +549,12 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
     const int g = blockIdx.x;
     const int tile = g % sh.T, grp = g / sh.T;
     const int tm = tile / sh.tiles_n, tn = tile % sh.tiles_n;
-    const int my_samples = grp < sh.nb ? (sh.nb - 1 - grp) / sh.Gs + 1 : 0;
-    const int64_t iters = (int64_t)my_samples * sh.nkc;
+    const bool kpar = SPLIT && sh.kpar;
+    const int my_samples = kpar ? 1 : grp < sh.nb ? (sh.nb - 1 - grp) / sh.Gs + 1 : 0;
+    const int64_t kh = (sh.nkc + 1) / 2;
+    const int64_t kb = kpar ? grp * kh : 0;                              // this CTA's K-chunk range
+    const int64_t ke = kpar ? (kb + kh < sh.nkc ? kb + kh : sh.nkc) : sh.nkc;
+    const int64_t iters = (int64_t)my_samples * (ke - kb);
 
     const uint32_t full0 = smem_addr(&bars[0]), empty0 = smem_addr(&bars[TSTAGES]);
     const uint32_t tfull0 = smem_addr(&bars[2 * TSTAGES]), tempty0 = smem_addr(&bars[2 * TSTAGES + 2]);
@@ -576,7 +584,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            int64_t b = grp, kc = 0;
+            int64_t b = kpar ? 0 : grp, kc = kb;
             for (int64_t it = 0; it < iters; ++it) {
                 bar_wait(empty0 + 8 * s, ph ^ 1);
                 const uint32_t full = full0 + 8 * s;
@@ -593,7 +601,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 bulk_load(st + 2 * TA_BYTES + TB_BYTES, Blo + ob, TB_BYTES, full);
 #endif
                 if (++s == TSTAGES) { s = 0; ph ^= 1; }
-                if (++kc == sh.nkc) { kc = 0; b += sh.Gs; }
+                if (++kc == ke) { kc = kb; b += sh.Gs; }
             }
         }
     } else if (warp == 1) {
@@ -602,7 +610,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             constexpr uint32_t idesc = tf32_idesc(TBM, TBN);
             int s = 0;
             uint32_t ph = 0;
-            int64_t kc = 0;
+            int64_t kc = kb;
             int abuf = 0;
             uint32_t aph = 0;  // bit a = phase of accumulator a (no indexed local array)
             for (int64_t it = 0; it < iters; ++it) {
@@ -620,15 +628,15 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                     const uint64_t bh = sw_desc(st + 2 * TA_BYTES + kk * 32);
                     const uint64_t bl = sw_desc(st + 2 * TA_BYTES + TB_BYTES + kk * 32);
 #ifndef MLSK_TC_ABL_NOMMA  // ablation: no MMAs (commits only)
-                    tc_mma_tf32(dcol, ah, bh, idesc, (kc > 0 || kk > 0) ? 1u : 0u);
+                    tc_mma_tf32(dcol, ah, bh, idesc, (kc > kb || kk > 0) ? 1u : 0u);
                     tc_mma_tf32(dcol, ah, bl, idesc, 1u);
                     tc_mma_tf32(dcol, al, bh, idesc, 1u);
 #endif
                 }
                 tc_commit(empty0 + 8 * s);  // smem stage free once these MMAs complete
                 if (++s == TSTAGES) { s = 0; ph ^= 1; }
-                if (++kc == sh.nkc) {
-                    kc = 0;
+                if (++kc == ke) {
+                    kc = kb;
                     tc_commit(tfull0 + 8 * abuf);  // accumulator complete
                     aph ^= 1u << abuf;
                     abuf ^= 1;
@@ -658,7 +666,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             tc_fence_after();
             float ssq = 0.f;
             // split sample (one sample per launch): the partial Y of earlier K-segments
-            float4* yp = SPLIT ? reinterpret_cast<float4*>(ypart + (int64_t)tile * (TBM * TBN) +
+            float4* yp = SPLIT ? reinterpret_cast<float4*>(ypart + (int64_t)((kpar ? grp * sh.T : 0) + tile) * (TBM * TBN) +
                                                            (int64_t)row * TBN + h * HC)
                                : nullptr;
 #pragma unroll
@@ -696,7 +704,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             if (lane == 0) bar_arrive(tempty0 + 8 * abuf);
             aph ^= 1u << abuf;
             abuf ^= 1;
-            if ((smp + 1) % FLUSH == 0 || smp + 1 == my_samples) {
+            if (!(SPLIT && split_part <= 2) && ((smp + 1) % FLUSH == 0 || smp + 1 == my_samples)) {
                 if (sh.direct) {
                     // (tile-aligned outputs, one CTA per tile) this thread's 64
                     // consecutive columns of the row-major level total, 16 bytes a time
@@ -738,7 +746,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
     }
     tc_fence_before();
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && !kpar) {  // kpar: the squares come from k_kpar_combine
         double t = 0.0;
         for (int w = 0; w < EPI_WARPS; ++w) t += s_sq[w];
         part_sq[g] = t;
@@ -785,6 +793,37 @@ __global__ void __launch_bounds__(256) k_reduce_tiles_tc(const double* __restric
         const double acc = warp_sum_array(part_sq, sh.T * sh.Gs, tx);
         if (tx == 0) *total_sq += acc;
     }
+}
+
+// kpar: Y = Y_0 + Y_1 (fp32, as a carried K-segment), level total += Y,
+// per-block sum of Y^2 in fp64 into blk_sq (then summed by one warp)
+__global__ void __launch_bounds__(256) k_kpar_combine(const float* __restrict__ yp, int T, int tiles_n, int64_t rows,
+                                                      int64_t cols, double* __restrict__ total,
+                                                      double* __restrict__ blk_sq) {
+    __shared__ double s_red[8];
+    double sq = 0.0;
+    const int64_t cells = rows * cols;
+    for (int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cell < cells;
+         cell += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = cell / cols, q = cell - r * cols;
+        const int tile = (int)((r / TBM) * tiles_n + q / TBN);
+        const int64_t off = (int64_t)tile * (TBM * TBN) + (r % TBM) * TBN + (q % TBN);
+        const float y = __fadd_rn(yp[off], yp[(int64_t)T * (TBM * TBN) + off]);
+        total[cell] += (double)y;
+        sq = __fma_rn((double)y, (double)y, sq);
+    }
+    sq = warp_sum(sq);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const double v = warp_sum(threadIdx.x < 8 ? s_red[threadIdx.x] : 0.0);
+        if (threadIdx.x == 0) blk_sq[blockIdx.x] = v;
+    }
+}
+
+__global__ void k_sum_sq(const double* __restrict__ blk_sq, int n, double* __restrict__ total_sq) {
+    const double v = warp_sum_array(blk_sq, n, threadIdx.x);
+    if (threadIdx.x == 0) *total_sq += v;
 }
 
 int sms() {
@@ -876,6 +915,27 @@ class TcEngine final : public PanelEngine {
         const bool finishes = kr.part == 0 || kr.part == 3;  // samples complete in this launch
         // one CTA per tile and a tile-aligned output: sums straight into the level total
         const bool direct = Gs_ == 1 && M_.rows % TBM == 0 && M_.cols % TBN == 0;
+        // one sample whose tiles fill the last CTA wave poorly (config 4: 512
+        // tiles = 3.5 waves): split its K range over two CTA groups, 7 waves of
+        // half the work, and combine the two partial Y afterwards
+        const int64_t w1 = (T_ + nsm_ - 1) / nsm_, w2 = (2 * T_ + nsm_ - 1) / nsm_;
+        if (kr.part == 0 && nb == 1 && direct && w2 < 2 * w1 && k >= 16) {
+            ws_.ypart.ensure((size_t)2 * T_ * TBM * TBN);
+            TcShape sh{1, k, MP_, PP_, T_, 2, tiles_n_, nullptr, M_.rows, M_.cols, 1};
+            {
+                Prof p("gemm_tf32x3", s);
+                k_gemm_tf32x3<true><<<2 * T_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq, 1,
+                                                                      ws_.ypart.p);
+            }
+            {
+                Prof p("reduce_tiles_tc", s);
+                const int blocks = nsm_ * 4;  // blk_sq scratch: the (unused) partial buffer
+                k_kpar_combine<<<blocks, 256, 0, s>>>(ws_.ypart.p, T_, tiles_n_, M_.rows, M_.cols, st.total(), part);
+                k_sum_sq<<<1, 32, 0, s>>>(part, blocks, st.total_sq());
+            }
+            launched(3);
+            return;
+        }
         if (finishes && !direct)
             MLSK_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * (size_t)T_ * Gs_ * (TBM * TBN), s));
         float* ypart = nullptr;

@@ -89,3 +89,15 @@ def test_tc_direct_accumulation_one_cta_per_tile(gpu):
     rf = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
     re_ = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="exact"))
     check(rf, re_)
+
+
+def test_tc_kparallel_single_sample(gpu):
+    """One level-sample over a direct-mode tile grid with a poorly filled last
+    CTA wave (160 tiles on 148 SMs) runs as two K-halves on two CTA groups
+    whose partial Y are combined afterwards; single-sample levels take that
+    path, the multi-sample level the ordinary one."""
+    model = gpu.gaussian_mean_matrix_model(1280, 4096, 4096, sd=1.0, data_seed=19, dtype=1)  # 10 x 16 tiles
+    plan = gpu.LevelPlan(2, 2, [3, 1, 1], c0=256)  # c = 256 (16 K-chunks), 512, 1024
+    rf = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
+    re_ = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="exact"))
+    check(rf, re_)
