@@ -339,8 +339,8 @@ def main():
             traffic = None
 
     e2e = None
-    if not args.no_e2e and rank == 0:
-        e2e = run_e2e(g, torch, device, args)
+    if not args.no_e2e:
+        e2e = run_e2e(g, torch, device, args, rank, world, dist)
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1:
@@ -377,33 +377,65 @@ def main():
     return 0
 
 
-def run_e2e(g, torch, device, args):
-    """Public-API call per step: means from pinned host buffers -> device,
-    all levels, report back to the host."""
+def run_e2e(g, torch, device, args, rank=0, world=1, dist=None):
+    """Public-API call per step on every rank: means from pinned host buffers ->
+    device, this rank's replication chunks of all levels (global counts
+    N_l * world, rank-sharded as the library's multi-GPU path does), the
+    per-level sums all-reduced across ranks, the report on the host.  Timed by
+    wall clock between barriers, max over ranks; value = all ranks' samples /
+    that time."""
+    import numpy as np
     # the config's means as host arrays (read back once from the seeded model)
     seeded = g.gaussian_mean_matrix_model(M_, N_, P_, sd=0.5, data_seed=data_seed())
     ma, mb = g.model_data(seeded, 0), g.model_data(seeded, 1)
     pa = torch.from_numpy(ma).pin_memory().numpy()
     pb = torch.from_numpy(mb).pin_memory().numpy()
     model = g.gaussian_mean_matrix_model(M_, N_, P_, sd=0.5, mean_a=pa, mean_b=pb)
-    plan = g.LevelPlan(2, LEVELS, STEP_N, c0=C0)
-    opts = g.EstimatorOptions(device=device, engine="fused")
-    for _ in range(max(1, args.warmup)):
-        g.mlmc_matmul(model, g.target_identity(), plan, MASTER, opts)
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        r = g.mlmc_matmul(model, g.target_identity(), plan, MASTER + 1 + i, opts)
-    dt = time.perf_counter() - t0
+    plan = g.LevelPlan(2, LEVELS, [n * world for n in STEP_N], c0=C0)
+    opts = g.EstimatorOptions(device=device, engine="fused", rank=rank, world=world)
     cells = M_ * P_
     levels = LEVELS + 1
-    # what the call moves: the two mean matrices and the replication list in,
-    # each level's [sum Y | sum ||Y||^2] out (mlsk_api.cu read_levels)
-    h2d = pa.nbytes + pb.nbytes + 8 * sum(STEP_N)
-    d2h = 8 * levels * (cells + 1)
-    return {"value": args.steps * sum(STEP_N) / dt, "unit": UNIT,
+    on_dev = world > 1 and dist.get_backend() == "nccl"  # gloo (multi-rank tests on one GPU): host buffer
+    red = torch.empty(levels * (cells + 1), dtype=torch.float64, device="cuda" if on_dev else "cpu") \
+        if world > 1 else None
+
+    def call(seed):
+        r = g.mlmc_matmul(model, g.target_identity(), plan, seed, opts)
+        if world > 1:  # the global level sums: one all-reduce of [sum Y | sum ||Y||^2] per level
+            host = np.concatenate([np.append(np.asarray(st.sum, dtype=np.float64).ravel(), st.sum_of_squares)
+                                   for st in r.per_level])
+            red.copy_(torch.from_numpy(host))
+            dist.all_reduce(red)
+            if on_dev:
+                red.cpu()
+        return r
+
+    for _ in range(max(1, args.warmup)):
+        call(MASTER)
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    calls = []
+    for i in range(args.steps):
+        tc = time.perf_counter()
+        call(MASTER + 1 + i)
+        calls.append(1e3 * (time.perf_counter() - tc))
+    dt = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda" if on_dev else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    # what one rank's call moves: the two mean matrices and the replication list
+    # in, each level's [sum Y | sum ||Y||^2] out (mlsk_api.cu read_levels); with
+    # world > 1 also the all-reduce buffer in and out
+    h2d = pa.nbytes + pb.nbytes + 8 * sum(STEP_N) + (8 * levels * (cells + 1) if world > 1 else 0)
+    d2h = 8 * levels * (cells + 1) * (2 if world > 1 else 1)
+    return {"value": world * args.steps * sum(STEP_N) / dt, "unit": UNIT,
             "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h),
-            "note": "mlsketch.mlmc_matmul with host mean buffers; wall clock, synchronous API"}
+            "call_ms": {"median": statistics.median(calls), "max": max(calls)},
+            "note": "mlsketch.mlmc_matmul with host mean buffers on every rank (rank-sharded global plan, "
+                    "level sums all-reduced); wall clock between barriers, max over ranks"}
 
 
 if __name__ == "__main__":

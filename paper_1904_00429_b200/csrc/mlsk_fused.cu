@@ -1439,9 +1439,11 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
             max_panel = std::max(max_panel, nb * per);
         }
     }
-    {
-        // one level-sample's panels must fit a buffer (samples are not split
-        // along K); fail with a clear message instead of an opaque allocation error
+    if ((size_t)(max_panel + 7) / 8 > P.panels[0].n) {
+        // the buffers must grow: one level-sample's panels must fit a buffer;
+        // fail with a clear message instead of an opaque allocation error
+        // (queried only when growing: cudaMemGetInfo on every round stalled
+        // the launching thread for milliseconds now and then)
         size_t free_b = 0, total_b = 0;
         MLSK_CUDA(cudaMemGetInfo(&free_b, &total_b));
         size_t held = 0;
