@@ -1269,7 +1269,14 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
             parts = InnerParts{};
             filled = 0;
         };
-        for (size_t j = 0; j < jobs.size(); ++j) {
+        // longest replications (largest c) first: the grid-stride loop hands out
+        // replications in list order, so the deep levels' long chains start at
+        // once instead of forming the kernel's tail
+        std::vector<size_t> order(jobs.size());
+        for (size_t j = 0; j < jobs.size(); ++j) order[j] = j;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](size_t x, size_t y) { return jobs[x].lv.c > jobs[y].lv.c; });
+        for (size_t j : order) {
             FusedJob& job = jobs[j];
             const int64_t c = job.lv.c, cc = job.lv.cc;
             const double w_fine = n / (double)c;
