@@ -1,4 +1,4 @@
-"""BASELINE configs 1 and 2 as full adaptive MLMC runs on one GPU: the
+"""BASELINE configs 1-4 as full adaptive MLMC runs on one GPU: the
 standard allocation for the target RMSE, then the achieved error against the
 exact product of the means (statistics check of BASELINE.json's north star).
 
@@ -26,7 +26,7 @@ MASTER = 20260823
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4])
     ap.add_argument("--eps-rel", type=float, default=1e-2)
     ap.add_argument("--repeats", type=int, default=1)
     args = ap.parse_args()
@@ -34,10 +34,19 @@ def main():
     if args.config == 1:
         model = g.gaussian_mean_model(4096, sd=1.0, mean_lo=0.0, mean_hi=1.0, data_seed=ds)
         M, c0, L = 2, 8, 5
-    else:
+    elif args.config == 2:
         model = g.gaussian_mean_matrix_model(256, 4096, 256, sd=0.5, data_seed=ds)
         M, c0, L = 2, 32, 6
-    exact = np.atleast_1d(np.asarray(g.ground_truth(model), dtype=np.float64)).ravel()
+    elif args.config == 3:  # fp32, tcgen05 3xTF32 engine
+        model = g.gaussian_mean_matrix_model(1024, 16384, 1024, sd=1.0, data_seed=ds, dtype=1)
+        M, c0, L = 2, 64, 8
+    else:  # config 4: RFF Gram, error against K_n (the n-feature Gram the sketch estimates)
+        model = g.rff_gram_model(4096, 2 ** 16, dim=64, sigma=4.0, data_seed=ds)
+        M, c0, L = 2, 128, 9
+    gt = g.ground_truth(model)
+    if isinstance(gt, tuple):  # RFF: (K_n, exact Gaussian kernel)
+        gt = gt[0]
+    exact = np.atleast_1d(np.asarray(gt, dtype=np.float64)).ravel()
     norm = float(np.linalg.norm(exact))
     eps = args.eps_rel * norm
     for rep in range(args.repeats):
