@@ -25,6 +25,7 @@
 //                     bytes per flop that cross L2 -> SMEM by a quarter vs
 //                     128 x 128 tiles.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "mlsk_internal.h"
@@ -529,7 +530,38 @@ struct TcShape {
     // K-chunks [g * ceil(nkc / 2), ...) and stores its partial Y into its own
     // ypart slot; k_kpar_combine forms Y, ||Y||^2 and the level total
     int kpar;
+    // symmetric output (RFF Gram: B = diag(w) A^T, so Y = A_S D A_S^T): the
+    // tiles cover only the 256 x 256 blocks (R, C) with R <= C, sym_nb blocks
+    // per side (0 = full tile grid).  Off-diagonal blocks count twice in
+    // ||Y||^2; k_mirror_lower fills the lower blocks of the level total.
+    int sym_nb;
 };
+
+// tile index -> (tile row of 128, tile column of 256)
+__device__ __forceinline__ void tile_coords(const TcShape& sh, int tile, int& tm, int& tn) {
+    if (sh.sym_nb == 0) {
+        tm = tile / sh.tiles_n;
+        tn = tile % sh.tiles_n;
+        return;
+    }
+    // blocks (R, C >= R) in row-major order, two 128-row tiles per block
+    const int u = tile >> 1;
+    int R = 0, start = 0;
+    while (u >= start + (sh.sym_nb - R)) {
+        start += sh.sym_nb - R;
+        ++R;
+    }
+    tm = 2 * R + (tile & 1);
+    tn = R + (u - start);
+}
+
+// (tile row, tile column) -> tile index; -1 for a block below the diagonal
+__device__ __forceinline__ int tile_index(const TcShape& sh, int tm, int tn) {
+    if (sh.sym_nb == 0) return tm * sh.tiles_n + tn;
+    const int R = tm >> 1;
+    if (R > tn) return -1;
+    return 2 * (R * sh.sym_nb - R * (R - 1) / 2 + (tn - R)) + (tm & 1);
+}
 
 // SPLIT: one sample split along K per launch (split_part 1 first, 2 middle,
 // 3 last, partial Y in ypart); a separate instantiation for the common path.
@@ -548,7 +580,8 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = blockIdx.x;
     const int tile = g % sh.T, grp = g / sh.T;
-    const int tm = tile / sh.tiles_n, tn = tile % sh.tiles_n;
+    int tm, tn;
+    tile_coords(sh, tile, tm, tn);
     const bool kpar = SPLIT && sh.kpar;
     const int my_samples = kpar ? 1 : grp < sh.nb ? (sh.nb - 1 - grp) / sh.Gs + 1 : 0;
     const int64_t kh = (sh.nkc + 1) / 2;
@@ -749,7 +782,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
     if (threadIdx.x == 0 && !kpar) {  // kpar: the squares come from k_kpar_combine
         double t = 0.0;
         for (int w = 0; w < EPI_WARPS; ++w) t += s_sq[w];
-        part_sq[g] = t;
+        part_sq[g] = sh.sym_nb && (tm >> 1) != tn ? 2.0 * t : t;  // a mirrored block counts twice
     }
     if (warp == 1) {
         tc_fence_after();
@@ -774,8 +807,8 @@ __global__ void __launch_bounds__(256) k_reduce_tiles_tc(const double* __restric
         for (int k = ty; k < 32; k += 8) {
             const int64_t r = r0 + tx, q = q0 + k;
             double acc = 0.0;
-            if (r < rows && q < cols) {
-                const int tile = (int)((r / TBM) * sh.tiles_n + q / TBN);
+            const int tile = r < rows && q < cols ? tile_index(sh, (int)(r / TBM), (int)(q / TBN)) : -1;
+            if (tile >= 0) {  // (cells of the lower blocks of a symmetric output: filled by the mirror)
                 const int64_t off = (q % TBN) * TBM + (r % TBM);
                 for (int grp = 0; grp < sh.Gs; ++grp) acc += part[(int64_t)(grp * sh.T + tile) * (TBM * TBN) + off];
             }
@@ -821,6 +854,26 @@ __global__ void __launch_bounds__(256) k_kpar_combine(const float* __restrict__ 
     }
 }
 
+// symmetric output: total[r][q] = total[q][r] for every r > q (n % 256 == 0):
+// the 256 x 256 blocks below the diagonal were not computed, and inside the
+// diagonal blocks (computed in full) the copy makes the estimate exactly
+// symmetric.  32 x 32 cell blocks through shared memory, both sides
+// coalesced.  Block (32, 8).
+__global__ void __launch_bounds__(256) k_mirror_lower(double* __restrict__ total, int64_t n) {
+    __shared__ double blk[32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t nb = n / 32;
+    for (int64_t bi = blockIdx.x; bi < nb * nb; bi += gridDim.x) {
+        const int64_t r0 = (bi / nb) * 32, q0 = (bi % nb) * 32;
+        if (r0 < q0) continue;  // above the diagonal (uniform per CTA)
+        for (int k = ty; k < 32; k += 8) blk[k][tx] = total[(q0 + k) * n + r0 + tx];
+        __syncthreads();
+        for (int k = ty; k < 32; k += 8)
+            if (r0 > q0 || k > tx) total[(r0 + k) * n + q0 + tx] = blk[tx][k];
+        __syncthreads();
+    }
+}
+
 __global__ void k_sum_sq(const double* __restrict__ blk_sq, int n, double* __restrict__ total_sq) {
     const double v = warp_sum_array(blk_sq, n, threadIdx.x);
     if (threadIdx.x == 0) *total_sq += v;
@@ -851,6 +904,13 @@ class TcEngine final : public PanelEngine {
         PP_ = (M.cols + TBN - 1) / TBN * TBN;
         tiles_n_ = (int)(PP_ / TBN);
         T_ = (int)(MP_ / TBM) * tiles_n_;
+        // RFF Gram (Y symmetric): upper-triangle blocks only (MLSK_TC_SYM=0: full grid)
+        const char* sym_env = std::getenv("MLSK_TC_SYM");
+        if (M.dm.kind == MLSK_MODEL_RFF && M.rows == M.cols && M.rows % TBN == 0 &&
+            !(sym_env && std::strcmp(sym_env, "0") == 0)) {
+            sym_nb_ = (int)(M.rows / TBN);
+            T_ = sym_nb_ * (sym_nb_ + 1);  // nb (nb + 1) / 2 blocks of two tiles
+        }
         Gs_ = std::max(1, nsm_ / T_);
         S_.M = M.dm;
         smem_ = TSTAGES * TSTAGE_BYTES + 1024;
@@ -919,9 +979,9 @@ class TcEngine final : public PanelEngine {
         // tiles = 3.5 waves): split its K range over two CTA groups, 7 waves of
         // half the work, and combine the two partial Y afterwards
         const int64_t w1 = (T_ + nsm_ - 1) / nsm_, w2 = (2 * T_ + nsm_ - 1) / nsm_;
-        if (kr.part == 0 && nb == 1 && direct && w2 < 2 * w1 && k >= 16) {
+        if (kr.part == 0 && nb == 1 && direct && w2 < 2 * w1 && k >= 16 && !sym_nb_) {
             ws_.ypart.ensure((size_t)2 * T_ * TBM * TBN);
-            TcShape sh{1, k, MP_, PP_, T_, 2, tiles_n_, nullptr, M_.rows, M_.cols, 1};
+            TcShape sh{1, k, MP_, PP_, T_, 2, tiles_n_, nullptr, M_.rows, M_.cols, 1, 0};
             {
                 Prof p("gemm_tf32x3", s);
                 k_gemm_tf32x3<true><<<2 * T_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq, 1,
@@ -943,7 +1003,7 @@ class TcEngine final : public PanelEngine {
             ws_.ypart.ensure((size_t)T_ * TBM * TBN);  // the carried partial Y of a split sample
             ypart = ws_.ypart.p;
         }
-        TcShape sh{nb, k, MP_, PP_, T_, Gs_, tiles_n_, direct ? st.total() : nullptr, M_.rows, M_.cols};
+        TcShape sh{nb, k, MP_, PP_, T_, Gs_, tiles_n_, direct ? st.total() : nullptr, M_.rows, M_.cols, 0, sym_nb_};
         {
             Prof p("gemm_tf32x3", s);
             if (kr.part == 0)
@@ -965,6 +1025,14 @@ class TcEngine final : public PanelEngine {
                                 dim3(32, 8), 0, s>>>(part, part_sq, sh, direct ? 0 : M_.rows, M_.cols, st.total(),
                                                      st.total_sq());
         }
+        if (sym_nb_) {
+            Prof p("mirror_tc", s);
+            const int64_t n = M_.rows;
+            k_mirror_lower<<<(int)std::min<int64_t>((n / 32) * (n / 32), (int64_t)nsm_ * 8), dim3(32, 8), 0, s>>>(
+                st.total(), n);
+            launched(3);
+            return;
+        }
         launched(2);
     }
 
@@ -982,6 +1050,7 @@ class TcEngine final : public PanelEngine {
     Workspace& ws_;
     TcModel S_{};
     int nsm_, T_, Gs_, tiles_n_, smem_, rff_smem_;
+    int sym_nb_ = 0;  // symmetric output: 256-blocks per side (0 = full tile grid)
     int64_t gen_cap_;
     int64_t MP_, PP_;
 };

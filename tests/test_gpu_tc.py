@@ -101,3 +101,26 @@ def test_tc_kparallel_single_sample(gpu):
     rf = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
     re_ = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="exact"))
     check(rf, re_)
+
+
+@pytest.mark.parametrize("points", [512, 2560, 384])
+def test_tc_symmetric_gram(gpu, points, monkeypatch):
+    """RFF Gram estimates are symmetric (B = diag(w) A^T): the engine runs only
+    the 256 x 256 blocks on and above the diagonal, counts the off-diagonal
+    ones twice in ||Y||^2 and mirrors the level total.  512 points: partial
+    buffer + reduction; 2560: one CTA per tile (direct); 384 (not a multiple
+    of 256): the full tile grid.  Results match the exact engine and the
+    full-grid run (MLSK_TC_SYM=0), and the level sums are exactly symmetric
+    (the mirror also copies the upper half of the diagonal blocks)."""
+    model = gpu.rff_gram_model(points, 4096, dim=64, sigma=4.0, data_seed=23)
+    plan = gpu.LevelPlan(2, 2, [9, 5, 3], c0=128)
+    rf = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
+    re_ = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="exact"))
+    check(rf, re_)
+    monkeypatch.setenv("MLSK_TC_SYM", "0")
+    rfull = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
+    check(rf, rfull, tol=1e-6)
+    if points % 256 == 0:
+        for st in rf.per_level:
+            s = np.asarray(st.sum)
+            assert np.array_equal(s, s.T)
