@@ -1083,7 +1083,8 @@ class F64Engine final : public PanelEngine {
             M_.dm, seed, tag, ks, nb, c, cc, w_fine, w_coarse, MP_, PP_, k, kr.kc0, Apan, Bpan, idx);
         launched();
     }
-    void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, LevelState& st, const KRange& kr) override {
+    void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, int64_t, double, double, LevelState& st,
+              const KRange& kr) override {
         const int64_t k = kr.nkc >= 0 ? kr.nkc : nkc(c);
         const double* Apan = static_cast<const double*>(panels);
         const double* Bpan = Apan + (size_t)nb * k * MP_ * KC;
@@ -1482,7 +1483,7 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         MLSK_CUDA(cudaEventRecord(P.gen_done[buf], P.s_gen));
         // GEMM + fused level epilogue + fixed-order reduction
         MLSK_CUDA(cudaStreamWaitEvent(P.s_mm, P.gen_done[buf], 0));
-        E.gemm(P.s_mm, panels, bt.nb, c, *job.st, bt.kr);
+        E.gemm(P.s_mm, panels, bt.nb, c, cc, w_fine, w_coarse, *job.st, bt.kr);
         MLSK_CUDA(cudaEventRecord(P.mm_done[buf], P.s_mm));
         P.used[buf] = true;
         if (idx) {

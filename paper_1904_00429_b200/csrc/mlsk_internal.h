@@ -257,7 +257,8 @@ struct PanelEngine {
     virtual int64_t group_size() const = 0;   // samples per round of the CTA groups
     virtual void gen(cudaStream_t s, uint64_t seed, uint64_t tag, const int64_t* ks, int nb, int64_t c, int64_t cc,
                      double w_fine, double w_coarse, void* panels, uint32_t* idx, const KRange& kr) = 0;
-    virtual void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, LevelState& st, const KRange& kr) = 0;
+    virtual void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, int64_t cc, double w_fine,
+                      double w_coarse, LevelState& st, const KRange& kr) = 0;
 };
 std::unique_ptr<PanelEngine> make_tc_engine(const Model& M, Workspace& ws);  // mlsk_tc.cu
 

@@ -25,6 +25,7 @@
 //                     bytes per flop that cross L2 -> SMEM by a quarter vs
 //                     128 x 128 tiles.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 
@@ -390,7 +391,7 @@ constexpr int RFF_SMEM = (RFF_DMAX * TBM + RFF_DMAX * RFF_COLS) * 4;  // X tile 
 __global__ void __launch_bounds__(GEN_T)
 k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
                  int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kcg,
-                 float* __restrict__ Ahi,
+                 int write_b, float* __restrict__ Ahi,
                  float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
                  uint32_t* __restrict__ idx_out) {
     extern __shared__ __align__(1024) unsigned char rsm[];
@@ -505,7 +506,7 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                     *reinterpret_cast<float4*>(Alo + oa + off) =
                         make_float4(tf32_lo(z[0]), tf32_lo(z[1]), tf32_lo(z[2]), tf32_lo(z[3]));
                 }
-                if (rb < PP) {
+                if (write_b && rb < PP) {
                     *reinterpret_cast<float4*>(Bhi + ob + off) = make_float4(v[0], v[1], v[2], v[3]);
                     *reinterpret_cast<float4*>(Blo + ob + off) =
                         make_float4(tf32_lo(v[0]), tf32_lo(v[1]), tf32_lo(v[2]), tf32_lo(v[3]));
@@ -535,6 +536,12 @@ struct TcShape {
     // per side (0 = full tile grid).  Off-diagonal blocks count twice in
     // ||Y||^2; k_mirror_lower fills the lower blocks of the level total.
     int sym_nb;
+    // shared panel (RFF Gram, |w| a power of two on every column): B = A^T is
+    // read from the A panel; the K-chunks below neg_kc (absolute index, kc0 =
+    // first chunk of this launch's K-range) run with the B operand negated and
+    // the epilogue scales Y by escale = |w| -- bit-identical to B = diag(w) A^T
+    int64_t neg_kc, kc0;
+    float escale;
 };
 
 // tile index -> (tile row of 128, tile column of 256)
@@ -655,15 +662,16 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 tc_fence_after();
                 const uint32_t st = smem_addr(ring + s * TSTAGE_BYTES);
                 const uint32_t dcol = tmem + (uint32_t)abuf * TBN;
+                const uint32_t id = sh.kc0 + kc < sh.neg_kc ? idesc | (1u << 14) : idesc;  // negate B
 #pragma unroll
                 for (int kk = 0; kk < TBK / 8; ++kk) {
                     const uint64_t ah = sw_desc(st + kk * 32), al = sw_desc(st + TA_BYTES + kk * 32);
                     const uint64_t bh = sw_desc(st + 2 * TA_BYTES + kk * 32);
                     const uint64_t bl = sw_desc(st + 2 * TA_BYTES + TB_BYTES + kk * 32);
 #ifndef MLSK_TC_ABL_NOMMA  // ablation: no MMAs (commits only)
-                    tc_mma_tf32(dcol, ah, bh, idesc, (kc > kb || kk > 0) ? 1u : 0u);
-                    tc_mma_tf32(dcol, ah, bl, idesc, 1u);
-                    tc_mma_tf32(dcol, al, bh, idesc, 1u);
+                    tc_mma_tf32(dcol, ah, bh, id, (kc > kb || kk > 0) ? 1u : 0u);
+                    tc_mma_tf32(dcol, ah, bl, id, 1u);
+                    tc_mma_tf32(dcol, al, bh, id, 1u);
 #endif
                 }
                 tc_commit(empty0 + 8 * s);  // smem stage free once these MMAs complete
@@ -710,6 +718,10 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
 #else
                 tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * TBN + h * HC + ch * 16), y);
 #endif
+                if (sh.escale != 1.0f) {  // shared panel: |w| (a power of two, exact)
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) y[i] = __fmul_rn(y[i], sh.escale);
+                }
                 if (SPLIT && split_part >= 2) {  // middle / last segment: add the carried partial
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
@@ -728,7 +740,9 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     ssq = __fmaf_rn(y[i], y[i], ssq);
+#ifndef MLSK_TC_ABL_NOSUM  // ablation (timing only, wrong sums): no register running sum
                     S[ch * 16 + i] = __fadd_rn(S[ch * 16 + i], y[i]);
+#endif
                 }
             }
             sq += (double)ssq;
@@ -737,7 +751,11 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             if (lane == 0) bar_arrive(tempty0 + 8 * abuf);
             aph ^= 1u << abuf;
             abuf ^= 1;
+#ifdef MLSK_TC_ABL_NOSUM
+            if (false) {
+#else
             if (!(SPLIT && split_part <= 2) && ((smp + 1) % FLUSH == 0 || smp + 1 == my_samples)) {
+#endif
                 if (sh.direct) {
                     // (tile-aligned outputs, one CTA per tile) this thread's 64
                     // consecutive columns of the row-major level total, 16 bytes a time
@@ -911,6 +929,8 @@ class TcEngine final : public PanelEngine {
             sym_nb_ = (int)(M.rows / TBN);
             T_ = sym_nb_ * (sym_nb_ + 1);  // nb (nb + 1) / 2 blocks of two tiles
         }
+        const char* sh_env = std::getenv("MLSK_TC_SHARED");
+        shared_env_ = !(sh_env && std::strcmp(sh_env, "0") == 0);
         Gs_ = std::max(1, nsm_ / T_);
         S_.M = M.dm;
         smem_ = TSTAGES * TSTAGE_BYTES + 1024;
@@ -947,8 +967,8 @@ class TcEngine final : public PanelEngine {
             k_gen_panels_rff<<<(int)std::min<int64_t>((int64_t)nb * ((k + RFF_CH - 1) / RFF_CH) * RFF_RSPLIT,
                                                       (int64_t)nsm_ * 5),
                                GEN_T, rff_smem_, s>>>(
-                S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi, Blo,
-                idx);
+                S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, kr.kc0,
+                shared_panel(c, cc, w_fine, w_coarse) ? 0 : 1, Ahi, Alo, Bhi, Blo, idx);
         } else {
             const int grid = (int)std::min<int64_t>((int64_t)nb * k, gen_cap_);
             if (M_.dm.kind == MLSK_MODEL_GAUSS_MEAN)
@@ -966,10 +986,19 @@ class TcEngine final : public PanelEngine {
         }
         launched();
     }
-    void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, LevelState& st, const KRange& kr) override {
+    void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, int64_t cc, double w_fine, double w_coarse,
+              LevelState& st, const KRange& kr) override {
         const int64_t k = kr.nkc >= 0 ? kr.nkc : nkc(c);
         float *Ahi, *Alo, *Bhi, *Blo;
         split(const_cast<void*>(panels), nb, k, Ahi, Alo, Bhi, Blo);
+        int64_t neg_kc = 0;
+        float escale = 1.0f;
+        if (shared_panel(c, cc, w_fine, w_coarse)) {  // B tiles from the A panel (MP == PP)
+            Bhi = Ahi;
+            Blo = Alo;
+            neg_kc = w_coarse < 0 ? cc / TBK : 0;
+            escale = (float)std::fabs(w_fine);
+        }
         double* part = ws_.partial.p;
         double* part_sq = part + (size_t)T_ * Gs_ * (TBM * TBN);
         const bool finishes = kr.part == 0 || kr.part == 3;  // samples complete in this launch
@@ -981,7 +1010,7 @@ class TcEngine final : public PanelEngine {
         const int64_t w1 = (T_ + nsm_ - 1) / nsm_, w2 = (2 * T_ + nsm_ - 1) / nsm_;
         if (kr.part == 0 && nb == 1 && direct && w2 < 2 * w1 && k >= 16 && !sym_nb_) {
             ws_.ypart.ensure((size_t)2 * T_ * TBM * TBN);
-            TcShape sh{1, k, MP_, PP_, T_, 2, tiles_n_, nullptr, M_.rows, M_.cols, 1, 0};
+            TcShape sh{1, k, MP_, PP_, T_, 2, tiles_n_, nullptr, M_.rows, M_.cols, 1, 0, 0, 0, 1.0f};
             {
                 Prof p("gemm_tf32x3", s);
                 k_gemm_tf32x3<true><<<2 * T_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq, 1,
@@ -1003,7 +1032,8 @@ class TcEngine final : public PanelEngine {
             ws_.ypart.ensure((size_t)T_ * TBM * TBN);  // the carried partial Y of a split sample
             ypart = ws_.ypart.p;
         }
-        TcShape sh{nb, k, MP_, PP_, T_, Gs_, tiles_n_, direct ? st.total() : nullptr, M_.rows, M_.cols, 0, sym_nb_};
+        TcShape sh{nb,      k,       MP_,     PP_,    T_,     Gs_,        tiles_n_, direct ? st.total() : nullptr,
+                   M_.rows, M_.cols, 0,       sym_nb_, neg_kc, kr.kc0, escale};
         {
             Prof p("gemm_tf32x3", s);
             if (kr.part == 0)
@@ -1038,6 +1068,18 @@ class TcEngine final : public PanelEngine {
 
    private:
     static int64_t nkc(int64_t c) { return (c + TBK - 1) / TBK; }
+    // RFF Gram with the fast generator: the B panel is diag(w) A^T.  When every
+    // |w| is the same power of two and the coarse prefix is whole K-chunks, the
+    // GEMM reads B from the A panel (negated prefix chunks, Y scaled by |w|):
+    // the products and their fp32 sums are the same bits scaled by |w|, and
+    // the generator writes half the panel bytes.  MLSK_TC_SHARED=0 disables.
+    bool shared_panel(int64_t c, int64_t cc, double w_fine, double w_coarse) const {
+        if (!sym_nb_ || M_.dm.rff_dim > RFF_DMAX || cc % TBK != 0 || c <= 0) return false;
+        if (cc > 0 && std::fabs(w_coarse) != std::fabs(w_fine)) return false;
+        int e = 0;
+        if (std::frexp(std::fabs(w_fine), &e) != 0.5 || e < -100 || e > 100) return false;
+        return shared_env_;
+    }
     // panels of nb samples x k K-chunks: A hi, A lo, B hi, B lo
     void split(void* panels, int nb, int64_t k, float*& Ahi, float*& Alo, float*& Bhi, float*& Blo) const {
         const size_t na = (size_t)nb * k * MP_ * TBK, nbp = (size_t)nb * k * PP_ * TBK;
@@ -1051,6 +1093,7 @@ class TcEngine final : public PanelEngine {
     TcModel S_{};
     int nsm_, T_, Gs_, tiles_n_, smem_, rff_smem_;
     int sym_nb_ = 0;  // symmetric output: 256-blocks per side (0 = full tile grid)
+    bool shared_env_ = true;
     int64_t gen_cap_;
     int64_t MP_, PP_;
 };

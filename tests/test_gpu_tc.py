@@ -117,6 +117,13 @@ def test_tc_symmetric_gram(gpu, points, monkeypatch):
     rf = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
     re_ = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="exact"))
     check(rf, re_)
+    # n / c a power of two: the GEMM reads B from the A panel (negated coarse
+    # prefix, Y scaled by |w|) -- the same bits as the separate B panel
+    monkeypatch.setenv("MLSK_TC_SHARED", "0")
+    rsep = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
+    for a, b in zip(rf.per_level, rsep.per_level):
+        assert np.array_equal(np.asarray(a.sum), np.asarray(b.sum))
+        assert a.sum_of_squares == b.sum_of_squares
     monkeypatch.setenv("MLSK_TC_SYM", "0")
     rfull = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
     check(rf, rfull, tol=1e-6)
