@@ -381,14 +381,21 @@ constexpr int RFF_DMAX = 64;
 constexpr int RFF_COLS = 32;               // sampled columns per work item (X tile reuse)
 constexpr int RFF_CH = RFF_COLS / TBK;     // K-chunks per work item
 constexpr int RFF_RSPLIT = 4;              // work items per column group (row-block ranges)
-constexpr int RFF_SMEM = (RFF_DMAX * TBM + RFF_DMAX * RFF_COLS) * 4;  // X tile + W columns (40 KB)
+// MLSK_RFF_SMALL (experiment): 128 threads over 64-row X tiles (24 KB, <= 72
+// registers), small enough to sit beside a GEMM CTA on the same SM
+#ifdef MLSK_RFF_SMALL
+constexpr int RFF_T = 128, RFF_RB = 64, RFF_MINB = 7;
+#else
+constexpr int RFF_T = GEN_T, RFF_RB = TBM, RFF_MINB = 1;
+#endif
+constexpr int RFF_SMEM = (RFF_DMAX * RFF_RB + RFF_DMAX * RFF_COLS) * 4;  // X tile + W columns (40 KB)
 
 // work item (b, column group of 32 sampled columns, range of 128-row blocks):
 // W columns and (per row block) the X tile in shared memory; each thread
 // owns 4 consecutive columns x 4 consecutive rows and writes its 16-byte row
 // pieces straight into the swizzled panels (no staging tiles: 40 KB of shared
 // memory per CTA, five CTAs per SM).
-__global__ void __launch_bounds__(GEN_T)
+__global__ void __launch_bounds__(RFF_T, RFF_MINB)
 k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
                  int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kcg,
                  int write_b, float* __restrict__ Ahi,
@@ -396,7 +403,7 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                  uint32_t* __restrict__ idx_out) {
     extern __shared__ __align__(1024) unsigned char rsm[];
     float* xs = reinterpret_cast<float*>(rsm);  // [D][128]
-    float* wsm = xs + RFF_DMAX * TBM;            // [D][RFF_COLS]
+    float* wsm = xs + RFF_DMAX * RFF_RB;         // [D][RFF_COLS]
     __shared__ int s_j[RFF_COLS];
     __shared__ float s_w[RFF_COLS], s_b[RFF_COLS];
     const DevModel& M = S.M;
@@ -404,10 +411,10 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
     const int tid = threadIdx.x;
     const float scale = (float)M.rff_scale;
     const int64_t ngrp = (nkc + RFF_CH - 1) / RFF_CH;  // column groups of RFF_CH K-chunks
-    const int64_t nrb = (MP > PP ? MP : PP) / TBM;     // 128-row blocks (A rows / B columns, m == p)
+    const int64_t nrb = (MP > PP ? MP : PP) / RFF_RB;  // row blocks (A rows / B columns, m == p)
     const int64_t rb_per = (nrb + RFF_RSPLIT - 1) / RFF_RSPLIT;
     const int64_t items = (int64_t)nb * ngrp * RFF_RSPLIT;
-    static_assert(RFF_COLS == 32 && TBM == 128 && GEN_T == 256, "4 x 4 thread tile map");
+    static_assert(RFF_COLS == 32 && RFF_T == 2 * RFF_RB && TBM % RFF_RB == 0, "4 x 4 thread tile map");
     const int t0 = 4 * (tid & 7), r0 = 4 * (tid >> 3);
     const int ch = t0 / TBK, tt = t0 % TBK;
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
@@ -433,7 +440,7 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
             s_b[tid] = j >= 0 ? M.rff_b[j] : 0.f;
         }
         __syncthreads();
-        for (int e = tid; e < D * RFF_COLS; e += GEN_T) {
+        for (int e = tid; e < D * RFF_COLS; e += RFF_T) {
             const int d = e / RFF_COLS, t = e - d * RFF_COLS;
             const int j = s_j[t];
             wsm[d * RFF_COLS + t] = j >= 0 ? M.rff_w[(int64_t)d * M.n + j] : 0.f;
@@ -451,21 +458,21 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
         const bool col_ok = kc < nkc;
         const int64_t rb_end = nrb < (rs + 1) * rb_per ? nrb : (rs + 1) * rb_per;
         for (int64_t rbi = rs * rb_per; rbi < rb_end; ++rbi) {
-            const int64_t rb = rbi * TBM;
+            const int64_t rb = rbi * RFF_RB;
             const int64_t lim = M.m - rb;
             __syncthreads();  // previous X tile consumed
             // X tile from the transposed copy: rows contiguous per dimension, so
             // the global reads coalesce and the shared stores are conflict-free
-            if (lim >= TBM && (M.m & 3) == 0) {
-                for (int e = tid; e < TBM / 4 * D; e += GEN_T) {
-                    const int d = e / (TBM / 4), r4 = e - d * (TBM / 4);
-                    reinterpret_cast<float4*>(xs + d * TBM)[r4] =
+            if (lim >= RFF_RB && (M.m & 3) == 0) {
+                for (int e = tid; e < RFF_RB / 4 * D; e += RFF_T) {
+                    const int d = e / (RFF_RB / 4), r4 = e - d * (RFF_RB / 4);
+                    reinterpret_cast<float4*>(xs + d * RFF_RB)[r4] =
                         __ldg(reinterpret_cast<const float4*>(M.rff_xt + (int64_t)d * M.m + rb) + r4);
                 }
             } else {
-                for (int e = tid; e < TBM * D; e += GEN_T) {
-                    const int d = e / TBM, r = e - d * TBM;
-                    xs[d * TBM + r] = r < lim ? M.rff_xt[(int64_t)d * M.m + rb + r] : 0.f;
+                for (int e = tid; e < RFF_RB * D; e += RFF_T) {
+                    const int d = e / RFF_RB, r = e - d * RFF_RB;
+                    xs[d * RFF_RB + r] = r < lim ? M.rff_xt[(int64_t)d * M.m + rb + r] : 0.f;
                 }
             }
             __syncthreads();
@@ -480,7 +487,7 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
 #pragma unroll 4
             for (int d = 0; d < D; ++d) {
                 const float4 wv = *reinterpret_cast<const float4*>(wsm + d * RFF_COLS + t0);
-                const float4 xv = *reinterpret_cast<const float4*>(xs + d * TBM + r0);
+                const float4 xv = *reinterpret_cast<const float4*>(xs + d * RFF_RB + r0);
                 const float xa[4] = {xv.x, xv.y, xv.z, xv.w}, wa[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
@@ -488,16 +495,17 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                     for (int q = 0; q < 4; ++q) acc[i][q] = __fmaf_rn(xa[i], wa[q], acc[i][q]);
             }
             if (!col_ok) continue;
-            const int64_t oa = (((int64_t)b * nkc + kc) * MP + rb) * TBK;
-            const int64_t ob = (((int64_t)b * nkc + kc) * PP + rb) * TBK;  // B panels are padded to 256
+            const int64_t rt = rb & ~(int64_t)(TBM - 1);  // the 128-row panel tile holding this block
+            const int64_t oa = (((int64_t)b * nkc + kc) * MP + rt) * TBK;
+            const int64_t ob = (((int64_t)b * nkc + kc) * PP + rt) * TBK;  // B panels are padded to 256
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const int r = r0 + i;
+                const int r = (int)(rb - rt) + r0 + i;  // row within the 128-row tile
                 float z[4], v[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     z[q] = 0.f;
-                    if (jv[q] >= 0 && r < lim) z[q] = scale * cosf(acc[i][q] + bv[q]);
+                    if (jv[q] >= 0 && r0 + i < lim) z[q] = scale * cosf(acc[i][q] + bv[q]);
                     v[q] = __fmul_rn(wv4[q], z[q]);
                 }
                 const int off = sw_off(r, tt) / 4;  // floats
@@ -966,7 +974,7 @@ class TcEngine final : public PanelEngine {
         if (M_.dm.kind == MLSK_MODEL_RFF && M_.dm.rff_dim <= RFF_DMAX) {
             k_gen_panels_rff<<<(int)std::min<int64_t>((int64_t)nb * ((k + RFF_CH - 1) / RFF_CH) * RFF_RSPLIT,
                                                       (int64_t)nsm_ * 5),
-                               GEN_T, rff_smem_, s>>>(
+                               RFF_T, rff_smem_, s>>>(
                 S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, kr.kc0,
                 shared_panel(c, cc, w_fine, w_coarse) ? 0 : 1, Ahi, Alo, Bhi, Blo, idx);
         } else {
