@@ -62,9 +62,23 @@ def panel_bytes_of(N):
     return sum(8.0 * (M_ + P_) * C0 * 2 ** l * n for l, n in enumerate(N))
 
 
-def data_seed():
-    from paper_1904_00429_b200.mlsketch import RngStream
-    return RngStream.derive_seed(MASTER, 0xD47A0002, 0)
+_U64 = 0xFFFFFFFFFFFFFFFF
+
+
+def _mix(z):  # RngStream::mix, rng.hpp:22-27 (pure host arithmetic: the reference arm loads no product code)
+    z = (z + 0x9E3779B97F4A7C15) & _U64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _U64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _U64
+    return z ^ (z >> 31)
+
+
+def derive_seed(master, a, b):  # RngStream::derive_seed, rng.hpp:31-37
+    return _mix(_mix(_mix(master) ^ ((a + 0x9E3779B97F4A7C15) & _U64)) ^ ((b + 0xBF58476D1CE4E5B9) & _U64))
+
+
+def data_seed(config=2):
+    """Seed of the config's fixed-from-seed data: derive_seed(master, 0xD47A0000 + config, 0)."""
+    return derive_seed(MASTER, 0xD47A0000 + config, 0)
 
 
 def config_dict(world, flush, warm=None):
@@ -215,6 +229,22 @@ def run_reference_arm(args, rank):
 # ------------------------------------------------------------- GPU arm
 
 
+def relaunch(n):
+    """`bench.py --gpus N` outside torchrun: run itself as N ranks (one process
+    per GPU) under torch.distributed.run on 127.0.0.1 and return its exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # NCCL's init lines show every rank joining
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -225,12 +255,16 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl != "reference":
+        return relaunch(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
         return run_reference_arm(args, rank)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     import torch
     device = local_rank % max(1, torch.cuda.device_count())

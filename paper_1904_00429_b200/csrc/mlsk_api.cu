@@ -96,6 +96,32 @@ struct Trace {
 };
 
 // Per-call execution context: device selection and stream.
+// One library stream per (host thread, device), destroyed with the thread
+// (a host thread pool calling the library does not leak streams).
+struct LibStreams {
+    std::map<int, cudaStream_t> by_device;
+    cudaStream_t get(int device) {
+        auto it = by_device.find(device);
+        if (it == by_device.end()) {
+            cudaStream_t st;
+            MLSK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            it = by_device.emplace(device, st).first;
+        }
+        return it->second;
+    }
+    ~LibStreams() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) != cudaSuccess) return;  // runtime already torn down
+        for (auto& kv : by_device) {
+            if (cudaSetDevice(kv.first) == cudaSuccess) {
+                cudaStreamSynchronize(kv.second);
+                cudaStreamDestroy(kv.second);
+            }
+        }
+        cudaSetDevice(cur);
+    }
+};
+
 struct Exec {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -132,14 +158,8 @@ struct Exec {
             // stream-ordered pool then recycles the per-call allocations in order
             // (a fresh stream per call made pool reuse opportunistic and call
             // times erratic)
-            static thread_local std::map<int, cudaStream_t> streams;
-            auto it = streams.find(device);
-            if (it == streams.end()) {
-                cudaStream_t st;
-                MLSK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-                it = streams.emplace(device, st).first;
-            }
-            stream = it->second;
+            static thread_local LibStreams streams;
+            stream = streams.get(device);
             owns = true;  // library stream: calls synchronise before returning
         }
     }
@@ -574,6 +594,11 @@ int mlsk_session_level_buffer(mlsk_session* s, void** device_ptr, int64_t* n_dou
                 s->packed.p + l * (cells + 2));
             launched();
         }
+        // library-owned stream: nothing outside the library can order itself
+        // after the pack, so the buffer is complete when the call returns.  With
+        // a caller stream the pack is ordered on that stream (the caller's
+        // collective must run on it or wait on it).
+        if (s->ex->owns) MLSK_CUDA(cudaStreamSynchronize(s->ex->stream));
         *device_ptr = s->packed.p;
         *n_doubles = (int64_t)(s->L + 1) * (cells + 2);
     });

@@ -276,11 +276,6 @@ __device__ __forceinline__ double2 lds128(uint32_t addr) {
     return v;
 }
 
-__device__ __forceinline__ double lds64(uint32_t addr) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
-    return v;
-}
 
 __device__ __forceinline__ void tm_ld32(uint32_t taddr, uint32_t* r) {
     asm volatile(
@@ -587,282 +582,6 @@ __global__ void k_reduce_tiles(const double* __restrict__ part, const double* __
         const double acc = warp_sum_array(part_sq, sh.T * sh.Gs, threadIdx.x);
         if (threadIdx.x == 0) *total_sq += acc;
     }
-}
-
-// ------------------------------------------- cluster engine (m, p in (128, 256])
-//
-// One kernel per level: generation and contraction fused, no panels in HBM.
-// A cluster of four CTAs owns the 2 x 2 grid of 128 x 128 output tiles of a
-// strided set of samples.  Each CTA generates ONE of the four operand blocks
-// of every K-chunk (A rows 0-127, A rows 128-255, B cols 0-127 or B cols
-// 128-255) into its own stage buffer and forwards it with one shared->DSMEM
-// bulk copy to the one other CTA of the cluster that needs it; the four
-// copies form a ring 0 -> 1 -> 3 -> 2 -> 0:
-//     rank 0  tile (0,0)  generates A0, receives B0 from rank 2
-//     rank 1  tile (0,1)  generates B1, receives A0 from rank 0
-//     rank 3  tile (1,1)  generates A1, receives B1 from rank 1
-//     rank 2  tile (1,0)  generates B0, receives A1 from rank 3
-// so every element is generated exactly once, as in k_gen_panels_f64.
-// Warps 0-7 run the DMMA contraction (32 x 64 warp tiles, running sum S in
-// tensor memory), warps 8-15 generate; setmaxnreg moves the register file to
-// the contraction (192 / 64 per thread).
-// Stage s: full[s] completes on the local generator's arrive (with the
-// expected bytes of the incoming copy) plus those bytes; empty[s] needs the 8
-// local consumer warps (own block read) and the 8 consumer warps of the ring
-// successor (its copy of our block read, so our next copy may overwrite it).
-constexpr int CL_CTAS = 4;
-constexpr int CL_TILE = 128;
-constexpr int CL_BLOCK_BYTES = CL_TILE * KC * 8;  // one operand block of a K-chunk (16 KB)
-constexpr int CL_STAGES = 6;
-constexpr int CL_THREADS = 512;
-constexpr int CL_WN = 64, CL_NJ = 8;
-constexpr uint32_t CL_TMEM_COLS = 256;
-constexpr int CL_DYN_SMEM = CL_STAGES * 2 * CL_BLOCK_BYTES;
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
-    uint32_t done;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    } while (!done);
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_bar) {
-    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
-}
-__device__ __forceinline__ void bulk_s2cluster(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t bar) {
-    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     dst),
-                 "r"(src), "r"(bytes), "r"(bar)
-                 : "memory");
-}
-__device__ __forceinline__ void gen_bar_sync() {
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-}
-
-__global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_THREADS, 1)
-k_level_cluster_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
-                    int64_t cc, double w_fine, double w_coarse, double* __restrict__ part,
-                    double* __restrict__ part_sq) {
-    extern __shared__ __align__(1024) unsigned char smem[];
-    __shared__ __align__(16) double2 s_sc[1024];
-    __shared__ __align__(16) double2 s_lg[128];
-    __shared__ __align__(8) uint64_t bars[2 * CL_STAGES];
-    __shared__ int s_j[2][KC];
-    __shared__ double s_w[2][KC];
-    __shared__ double s_sq[8];
-    __shared__ uint32_t s_tmem;
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
-    const int tm = (int)(rank >> 1), tn = (int)(rank & 1);
-    const bool own_a = rank == 0 || rank == 3;
-    const uint32_t next = rank == 0 ? 1u : rank == 1 ? 3u : rank == 3 ? 2u : 0u;
-    const uint32_t prev = rank == 0 ? 2u : rank == 1 ? 0u : rank == 3 ? 1u : 3u;
-    const int grp = (int)(blockIdx.x / CL_CTAS), Gc = (int)(gridDim.x / CL_CTAS);
-    const int64_t nkc = (c + KC - 1) / KC;
-    const int my_samples = grp < nb ? (nb - 1 - grp) / Gc + 1 : 0;
-    const int64_t iters = (int64_t)my_samples * nkc;
-    const uint32_t full0 = smem_u32(&bars[0]), empty0 = smem_u32(&bars[CL_STAGES]);
-    const uint32_t stage0 = smem_u32(smem);
-    // stage s: A block at +0, B block at +16 KB
-    const uint32_t own_off = own_a ? 0u : (uint32_t)CL_BLOCK_BYTES;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < CL_STAGES; ++s) {
-            mbar_init(full0 + 8 * s, 1);
-            mbar_init(empty0 + 8 * s, 16);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
-                     "r"(CL_TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    load_tables_full(s_sc, s_lg, M.tab);
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    cluster_sync_all();  // barriers of every CTA initialised before any remote traffic
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-
-    if (warp >= 8) {
-        // ------------------------------------------------ generator warps
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
-        Tables T = M.tab;
-        T.sincos_d = reinterpret_cast<const double*>(s_sc);
-        T.log_d = reinterpret_cast<const double*>(s_lg);
-        const int gtid = threadIdx.x - 256;
-        const int64_t rb = (int64_t)CL_TILE * (own_a ? tm : tn);
-        const uint32_t rfull0 = mapa(full0, next);
-        const uint32_t rstage0 = mapa(stage0, next);
-        int s = 0;
-        uint32_t ph = 0;
-        int64_t b = grp, kc = 0;
-        for (int64_t it = 0; it < iters; ++it) {
-            const int jb = (int)(it & 1);
-            const uint64_t key = derive_seed(seed, tag, (uint64_t)ks[b]);
-            if (gtid < KC) {
-                const int64_t t = kc * KC + gtid;
-                int j = 0;  // padding columns (t >= c): column 0 with weight 0
-                double w = 0.0;
-                if (t < c) {
-                    const u32x4 r = philox((uint32_t)(t >> 1), 0, 0, MLSK_CTR_INDEX, key);
-                    const uint32_t ix = index_from_u64((t & 1) ? hi64(r) : lo64(r), M.n, M.log2n, M.cum);
-                    j = (int)(ix - 1);
-                    w = t < cc ? w_coarse : w_fine;
-                }
-                s_j[jb][gtid] = j;
-                s_w[jb][gtid] = w;
-            }
-            mbar_wait_cluster(empty0 + 8 * s, ph ^ 1u);
-            gen_bar_sync();  // s_j visible; every generator past the wait
-            double* tl = reinterpret_cast<double*>(smem + s * 2 * CL_BLOCK_BYTES + own_off);
-            if (own_a) gen_phase<true>(M, T, key, rb, s_j[jb], s_w[jb], tl, gtid);
-            else gen_phase<false>(M, T, key, rb, s_j[jb], s_w[jb], tl, gtid);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            gen_bar_sync();
-            if (gtid == 0) {
-                const uint32_t off = (uint32_t)(s * 2 * CL_BLOCK_BYTES) + own_off;
-                mbar_expect_tx(full0 + 8 * s, CL_BLOCK_BYTES);  // + the block arriving from prev
-                bulk_s2cluster(rstage0 + off, stage0 + off, CL_BLOCK_BYTES, rfull0 + 8 * s);
-            }
-            if (++s == CL_STAGES) {
-                s = 0;
-                ph ^= 1u;
-            }
-            if (++kc == nkc) {
-                kc = 0;
-                b += Gc;
-            }
-        }
-    } else {
-        // ------------------------------------------------- DMMA warps
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 168;");
-        const int wi = warp >> 1, wj = warp & 1;
-        const int gid = lane >> 2, tig = lane & 3;
-        double acc[4][CL_NJ][2];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < CL_NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-        double sq = 0.0;
-        // running sums at TMEM lane (warp % 4) * 32 + lane, columns (warp / 4) * 128 + 32 i + [0, 32)
-        const uint32_t s_t = s_tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 128);
-        {
-            uint32_t z[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) z[e] = 0u;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) tm_st32(s_t + 32 * i, z);
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        }
-        const uint32_t rempty0 = mapa(empty0, prev);
-        const uint32_t a_off = (uint32_t)((wi * 32 + gid) * KC * 8);
-        const uint32_t b_off = (uint32_t)(CL_BLOCK_BYTES + (wj * CL_WN + gid) * KC * 8);
-        const uint32_t g0 = (uint32_t)((((2 * tig) ^ gid) << 4)), g1 = (uint32_t)((((2 * tig + 1) ^ gid) << 4));
-        int s = 0;
-        uint32_t ph = 0;
-        int64_t kc = 0;
-        for (int64_t it = 0; it < iters; ++it) {
-            mbar_wait(full0 + 8 * s, ph);
-            const uint32_t a_st = stage0 + s * 2 * CL_BLOCK_BYTES + a_off;
-            const uint32_t b_st = stage0 + s * 2 * CL_BLOCK_BYTES + b_off;
-            // one k at a time (4 + 8 LDS.64): 24 fragment registers, leaving the
-            // generator warps 96
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t gg = ((q >> 1) ? g1 : g0) + 8 * (q & 1);
-                double af[4], bf[CL_NJ];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) af[i] = lds64(a_st + i * (8 * KC * 8) + gg);
-#pragma unroll
-                for (int j = 0; j < CL_NJ; ++j) bf[j] = lds64(b_st + j * (8 * KC * 8) + gg);
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < CL_NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-            }
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(empty0 + 8 * s);         // own block read
-                mbar_arrive_remote(rempty0 + 8 * s);  // prev's block (its copy target) read
-            }
-            if (++s == CL_STAGES) {
-                s = 0;
-                ph ^= 1u;
-            }
-            if (++kc == nkc) {
-                kc = 0;
-                // sample boundary: Y^2 and the running sum
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    uint32_t r[32];
-                    tm_ld32(s_t + 32 * i, r);
-#pragma unroll
-                    for (int j = 0; j < CL_NJ; ++j)
-#pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const double y = acc[i][j][e];
-                            sq = __fma_rn(y, y, sq);
-                            const int w = 2 * (2 * j + e);
-                            const double v = __dadd_rn(__hiloint2double((int)r[w + 1], (int)r[w]), y);
-                            r[w] = (uint32_t)__double2loint(v);
-                            r[w + 1] = (uint32_t)__double2hiint(v);
-                            acc[i][j][e] = 0.0;
-                        }
-                    tm_st32(s_t + 32 * i, r);
-                }
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            }
-        }
-        // partial outputs of this CTA: tile (tm, tn) of group grp
-        double* out = part + ((int64_t)grp * CL_CTAS + tm * 2 + tn) * (CL_TILE * CL_TILE);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            uint32_t r32[32];
-            tm_ld32(s_t + 32 * i, r32);
-#pragma unroll
-            for (int j = 0; j < CL_NJ; ++j) {
-                const int r = wi * 32 + 8 * i + gid;
-                const int q = wj * CL_WN + 8 * j + 2 * tig;
-                *reinterpret_cast<double2*>(out + r * CL_TILE + q) =
-                    make_double2(__hiloint2double((int)r32[4 * j + 1], (int)r32[4 * j]),
-                                 __hiloint2double((int)r32[4 * j + 3], (int)r32[4 * j + 2]));
-            }
-        }
-        sq = warp_sum(sq);
-        if (lane == 0) s_sq[warp] = sq;
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < 8; ++w) t += s_sq[w];
-        part_sq[(int64_t)grp * CL_CTAS + tm * 2 + tn] = t;
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(CL_TMEM_COLS));
-    }
-    cluster_sync_all();  // no CTA leaves while a peer may still signal or copy into it
 }
 
 // ----------------------------------------------------- vector (config 1)
@@ -1209,17 +928,6 @@ struct Batch {
     KRange kr;       // K-chunk range (split samples)
 };
 
-bool cluster_eligible(const Model& M, int target, const std::vector<FusedJob>& jobs) {
-    // opt-in (MLSK_CLUSTER=1, read per round): measured slower than the panel
-    // pipeline on config 2 ("cluster engine")
-    const char* e = getenv("MLSK_CLUSTER");
-    if (!(e && e[0] == '1') || M.vector || M.dm.dtype != MLSK_F64 || tc_supported(M, target) || sm_count() < CL_CTAS) return false;
-    if (M.rows <= CL_TILE || M.rows > 2 * CL_TILE || M.cols <= CL_TILE || M.cols > 2 * CL_TILE) return false;
-    for (const auto& job : jobs)
-        if (job.probe_host) return false;  // the coupling probe reads the panel pipeline's index lists
-    return true;
-}
-
 }  // namespace
 
 void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
@@ -1341,63 +1049,6 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         return;
     }
 
-    // ---- matrix path, m and p in (128, 256], opt-in: one fused cluster kernel
-    // per level, no panels in HBM
-    if (cluster_eligible(M, a.target, jobs)) {
-        once_per_device((const void*)&k_level_cluster_f64, [] {
-            MLSK_CUDA(cudaFuncSetAttribute(k_level_cluster_f64, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           CL_DYN_SMEM));
-        });
-        // clusters live inside one GPC: fewer than sms / 4 may be co-resident
-        int Gc = sms / CL_CTAS;
-        {
-            cudaLaunchConfig_t cfg{};
-            cfg.gridDim = dim3(Gc * CL_CTAS);
-            cfg.blockDim = dim3(CL_THREADS);
-            cfg.dynamicSmemBytes = CL_DYN_SMEM;
-            cudaLaunchAttribute at{};
-            at.id = cudaLaunchAttributeClusterDimension;
-            at.val.clusterDim.x = CL_CTAS;
-            at.val.clusterDim.y = 1;
-            at.val.clusterDim.z = 1;
-            cfg.attrs = &at;
-            cfg.numAttrs = 1;
-            int active = 0;
-            MLSK_CUDA(cudaOccupancyMaxActiveClusters(&active, (void*)k_level_cluster_f64, &cfg));
-            if (active > 0) Gc = std::min(Gc, active);
-            if (getenv("MLSK_TRACE")) fprintf(stderr, "[mlsk] cluster engine: %d clusters of %d CTAs\n", Gc, CL_CTAS);
-        }
-        const size_t tiles = (size_t)Gc * CL_CTAS;
-        ws.partial.ensure(tiles * CL_TILE * CL_TILE + tiles);
-        double* part = ws.partial.p;
-        double* part_sq = part + tiles * CL_TILE * CL_TILE;
-        for (size_t j = 0; j < jobs.size(); ++j) {
-            FusedJob& job = jobs[j];
-            const int64_t total = (int64_t)jks[j].size();
-            if (total == 0) continue;
-            const int64_t c = job.lv.c, cc = job.lv.cc;
-            const double w_fine = n / (double)c;
-            const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;
-            {
-                Prof p("level_cluster_f64", P.s_gen);
-                k_level_cluster_f64<<<Gc * CL_CTAS, CL_THREADS, CL_DYN_SMEM, P.s_gen>>>(
-                    M.dm, a.seed, job.lv.tag, P.ks.p + job_off[j], (int)total, c, cc, w_fine, w_coarse, part, part_sq);
-            }
-            const GemmShape sh{(int)total, (c + KC - 1) / KC, 2 * CL_TILE, 2 * CL_TILE, CL_CTAS, Gc, 2};
-            const int64_t cells = M.rows * M.cols;
-            {
-                Prof p("reduce_tiles", P.s_gen);
-                k_reduce_tiles<CL_TILE, CL_TILE>
-                    <<<(int)std::min<int64_t>((cells + 255) / 256, (int64_t)sms * 8), 256, 0, P.s_gen>>>(
-                        part, part_sq, sh, M.rows, M.cols, job.st->total(), job.st->total_sq());
-            }
-            launched(2);
-            job.st->count += total;
-        }
-        MLSK_CUDA(cudaEventRecord(P.end, P.s_gen));
-        MLSK_CUDA(cudaStreamWaitEvent(a.stream, P.end, 0));
-        return;
-    }
 
     // ---- matrix path: batches of replications, software-pipelined over a
     // panel engine (fp64 DMMA or the tcgen05 3xTF32 engine for fp32 models)
@@ -1422,7 +1073,7 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
             // one sample's panels exceed a batch: K-segments of one sample each,
             // the partial Y carried between them
             if (jobs[j].probe_host)
-                throw Error(MLSK_EINVAL, "probe: not available for level-samples split along K (panels > 384 MiB)");
+                throw Error(MLSK_EINVAL, "probe: not available for level-samples split along K (panels > " + std::to_string(split_limit >> 20) + " MiB)");
             const int64_t nk = (jobs[j].lv.c + E.chunk_cols() - 1) / E.chunk_cols();
             const int64_t seg = std::max<int64_t>(1, split_limit / E.chunk_bytes());  // few, large segments
             for (int64_t off = 0; off < total; ++off)

@@ -11,19 +11,21 @@
 //  k_gen_panels_tf32  sampled indices + the sampled columns of A / rows of B
 //                     (gauss f32, Student-t or random-Fourier features,
 //                     generated on the fly), written as hi / lo K-chunks in the
-//                     UMMA canonical K-major SWIZZLE_128B layout.
+//                     UMMA canonical K-major SWIZZLE_64B layout (16 tf32 = 64 B
+//                     per row of a K-chunk).
 //  k_gemm_tf32x3      persistent CTAs, one 128 x 256 output tile per CTA over a
 //                     strided set of samples.  warp 0: cp.async.bulk producer
-//                     (2-stage mbarrier ring, 96 KB per stage); warp 1: TMEM
-//                     allocation + single-thread tcgen05.mma (M128 N256 K8)
-//                     issue into two 256-column TMEM accumulators (all 512
-//                     columns, double-buffered across samples); warps 2-9:
-//                     epilogue, two warps per TMEM lane quadrant taking 128
-//                     columns each (tcgen05.ld, Y^2 into fp64, running sum in
-//                     128 registers per thread, flushed to an fp64 per-CTA
-//                     partial every 32 samples).  N = 256 cuts the operand
-//                     bytes per flop that cross L2 -> SMEM by a quarter vs
-//                     128 x 128 tiles.
+//                     (4-stage mbarrier ring, 48 KB per stage: A_hi, A_lo,
+//                     B_hi, B_lo of one K-chunk); warp 1: TMEM allocation +
+//                     single-thread tcgen05.mma (M128 N256 K8) issue into two
+//                     256-column TMEM accumulators (all 512 columns,
+//                     double-buffered across samples); warps 2-17: epilogue,
+//                     four warps per TMEM lane quadrant taking 64 columns each
+//                     (tcgen05.ld, Y^2 into fp64, running sum in 64 registers
+//                     per thread, flushed to an fp64 per-CTA partial every 32
+//                     samples).  N = 256 cuts the operand bytes per flop that
+//                     cross L2 -> SMEM by a quarter vs 128 x 128 tiles.
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -662,7 +664,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             int abuf = 0;
             uint32_t aph = 0;  // bit a = phase of accumulator a (no indexed local array)
             for (int64_t it = 0; it < iters; ++it) {
-                if (kc == 0) {
+                if (kc == kb) {  // first K-chunk of this CTA's range of a sample (kpar: kb > 0)
                     bar_wait(tempty0 + 8 * abuf, ((aph >> abuf) & 1u) ^ 1u);  // epilogue released this accumulator
                     tc_fence_after();
                 }

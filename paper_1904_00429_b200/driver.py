@@ -101,6 +101,9 @@ def allreduce_stats(session, levels: int, group=None) -> LevelStats:
         import torch
 
         ptr, n = session.level_buffer()
+        # the pack runs on the session's stream, which need not be torch's
+        # current stream: wait for it before NCCL reads the buffer
+        session.synchronize()
         t = torch.as_tensor(_DevBuf(ptr, n), device="cuda")
         dist.all_reduce(t, group=group)
         return unpack(t.double().cpu().numpy(), levels)

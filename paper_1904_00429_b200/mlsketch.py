@@ -59,8 +59,9 @@ class RngStream:
         return z ^ (z >> 31)
 
     @staticmethod
-    def derive_seed(master: int, a: int, b: int) -> int:  # rng.hpp:31-37
-        return int(lib().mlsk_derive_seed(master, a, b))
+    def derive_seed(master: int, a: int, b: int) -> int:  # rng.hpp:31-37 (== mlsk_derive_seed)
+        mix, u = RngStream.mix, 0xFFFFFFFFFFFFFFFF
+        return mix(mix(mix(master & u) ^ ((a + 0x9E3779B97F4A7C15) & u)) ^ ((b + 0xBF58476D1CE4E5B9) & u))
 
 
 # ------------------------------------------------------------------ models

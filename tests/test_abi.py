@@ -31,6 +31,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_derive_seed_matches_reference_definition():
+    from paper_1904_00429_b200 import _lib
     from paper_1904_00429_b200.mlsketch import RngStream
 
     def mix(z):
@@ -44,6 +45,7 @@ def test_derive_seed_matches_reference_definition():
         h = mix(h ^ ((a + 0x9E3779B97F4A7C15) & (2 ** 64 - 1)))
         h = mix(h ^ ((b + 0xBF58476D1CE4E5B9) & (2 ** 64 - 1)))
         assert RngStream.derive_seed(m, a, b) == h
+        assert _lib.lib().mlsk_derive_seed(m, a, b) == h  # the C-ABI's host function
 
 
 def test_no_cpu_fallback_without_device():
