@@ -253,6 +253,8 @@ def main():
     ap.add_argument("--impl", default="mlsk", choices=["mlsk", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--configs", default="1,3,4,5",
+                    help="BASELINE configs measured as extra blocks of the JSON line (N=1 only; '' = none)")
     args = ap.parse_args()
 
     if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl != "reference":
@@ -383,6 +385,15 @@ def main():
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "unavailable", "sample": str(e)}
 
+    blocks = None
+    if args.configs and world == 1:
+        # the other BASELINE configurations, same timing rules (bench_configs_lib.py)
+        import bench_configs_lib
+        torch.cuda.synchronize()
+        blocks = bench_configs_lib.measure([int(x) for x in args.configs.split(",") if x], steps=3,
+                                           with_cpu=not args.no_cpu_baseline, device=device)
+        torch.cuda.set_stream(stream)
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -404,6 +415,8 @@ def main():
                 "clocks": clk.summary(),
                 "e2e": e2e,
                 "cpu_baseline": cpu}
+        if blocks is not None:
+            line["configs"] = blocks
         print(json.dumps(line), flush=True)
     sess.close()
     if dist is not None:

@@ -108,6 +108,23 @@ typedef struct mlsk_exec_opts {
     int64_t probe_k;     /* coupling probe: dump index sets of the first probe_k
                             replications of every level >= 1 (estimators.hpp:38-48) */
     uint32_t* probe_out; /* host [(L+1)][probe_k][c_L] 1-based indices, row l holds c_l */
+    /* Multi-GPU inside one call (the reference parallelises inside the library,
+     * parallel.hpp:18-52).  n_devices > 1: the replications are dealt to
+     * n_devices device slots (device_ids[i], NULL = 0 .. n_devices-1; an ordinal
+     * may repeat), one host thread per slot; slot i of this process is shard
+     * rank * n_devices + i of world * n_devices.  The per-level sums of the
+     * slots are added on the host in slot order.  Estimators and sessions only
+     * (mc_* / reference_* run on the first device). */
+    int32_t n_devices;         /* 0 or 1: one device (`device`) */
+    const int32_t* device_ids;
+    /* deterministic = 1: the samples go to `vshards` fixed virtual shards
+     * (chunk q -> shard q mod vshards), each accumulated on its own and added
+     * in shard order, so results are bit-identical for every n_devices that
+     * divides vshards (the reference's thread-count invariance,
+     * README.md:109-119).  Needs world == 1 (across processes: the Python
+     * driver's ShardedSession). */
+    int32_t deterministic;
+    int32_t vshards;           /* 0: 8 */
 } mlsk_exec_opts;
 
 /*
@@ -228,6 +245,9 @@ int mlsk_profile_timeline(int i, char* name, int name_len, double* t0, double* t
 double mlsk_measure_fp64_peak(int device);
 /* Dense TF32 tcgen05 throughput (M=128, N=n, one CTA per SM), TFLOP/s. */
 double mlsk_measure_tf32_peak(int device, int n);
+/* RNG roofline of the inner-product path: index-samples/s of its per-index
+ * work alone (index draw, Philox + Box-Muller pair, mean gathers), config 1. */
+double mlsk_measure_index_rate(int device);
 
 #ifdef __cplusplus
 }

@@ -65,6 +65,10 @@ class ExecOpts(C.Structure):
         ("world", C.c_int32),
         ("probe_k", C.c_int64),
         ("probe_out", C.POINTER(C.c_uint32)),
+        ("n_devices", C.c_int32),
+        ("device_ids", C.POINTER(C.c_int32)),
+        ("deterministic", C.c_int32),
+        ("vshards", C.c_int32),
     ]
 
 

@@ -71,6 +71,8 @@ def lib():
     L.mlsk_measure_fp64_peak.argtypes = [C.c_int]
     L.mlsk_measure_tf32_peak.restype = C.c_double
     L.mlsk_measure_tf32_peak.argtypes = [C.c_int, C.c_int]
+    L.mlsk_measure_index_rate.restype = C.c_double
+    L.mlsk_measure_index_rate.argtypes = [C.c_int]
     _lib = L
     return L
 

@@ -15,6 +15,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <thread>
 
 #include "mlsk_internal.h"
 
@@ -130,6 +131,35 @@ struct Exec {
     int rank = 0, world = 1;
     int64_t probe_k = 0;
     uint32_t* probe_out = nullptr;
+    std::vector<int> slots;  // device slots (multi-GPU inside the call); empty: one device
+    bool deterministic = false;
+    int vshards = 8;
+
+    // the options' multi-device request, validated (no device is touched)
+    static void multi_of(const mlsk_exec_opts* o, std::vector<int>& slots, bool& det, int& vsh) {
+        slots.clear();
+        det = false;
+        vsh = 8;
+        if (!o) return;
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess) ndev = 0;
+        if (o->n_devices < 0) invalid("exec: n_devices must be non-negative");
+        if (o->n_devices > 1 || o->deterministic) {
+            const int nd = o->n_devices > 1 ? o->n_devices : 1;
+            for (int i = 0; i < nd; ++i) {
+                const int d = o->device_ids ? o->device_ids[i] : (o->n_devices > 1 ? i : std::max(0, o->device));
+                if (d < 0 || d >= ndev) invalid("exec: device id out of range");
+                slots.push_back(d);
+            }
+        }
+        det = o->deterministic != 0;
+        vsh = o->vshards > 0 ? o->vshards : 8;
+        if (det) {
+            const int world = o->world <= 0 ? 1 : o->world;
+            if (world != 1) invalid("exec: deterministic mode needs world == 1 (across processes: ShardedSession)");
+            if (vsh % (int)slots.size() != 0) invalid("exec: n_devices must divide vshards");
+        }
+    }
 
     explicit Exec(const mlsk_exec_opts* o) {
         int ndev = 0;
@@ -141,6 +171,7 @@ struct Exec {
             world = o->world <= 0 ? 1 : o->world;
             probe_k = o->probe_k;
             probe_out = o->probe_out;
+            multi_of(o, slots, deterministic, vshards);
             if (rank < 0 || rank >= world) invalid("exec: rank out of range");
             if (engine < MLSK_ENGINE_AUTO || engine > MLSK_ENGINE_FUSED) invalid("exec: unknown engine");
         }
@@ -204,7 +235,7 @@ struct Runner {
     void resolve_engine(int requested) {
         const bool fused_ok = fused_supported(model, target);
         if (requested == MLSK_ENGINE_FUSED && !fused_ok)
-            invalid("engine: the fused engine needs the philox stream, an identity target and a supported model");
+            invalid("engine: the fused engine needs the philox stream and a supported model (fp32 models: identity target)");
         engine = requested == MLSK_ENGINE_AUTO ? (fused_ok ? MLSK_ENGINE_FUSED : MLSK_ENGINE_EXACT) : requested;
     }
 
@@ -285,6 +316,18 @@ int mlmc_impl(bool matrix, const mlsk_model_desc* model, int32_t target, double 
         check_target(target, tparam);
         if (!model) invalid("model: null descriptor");
         if (model_is_vector(model) == matrix) invalid("estimator: model kind does not match the estimator");
+        if (opts && (opts->n_devices > 1 || opts->deterministic)) {
+            // multi-GPU inside the call: a multi-device session, one round
+            mlsk_session* s = nullptr;
+            int rc = mlsk_session_create(model, target, tparam, plan->M, plan->c0, plan->L, seed, opts, &s);
+            if (rc == MLSK_OK) rc = mlsk_session_run_round(s, plan->N);
+            if (rc == MLSK_OK && rep) rc = mlsk_session_stats(s, rep);
+            const std::string msg = rc == MLSK_OK ? "" : mlsk_last_error();
+            if (s) mlsk_session_destroy(s);
+            if (rc != MLSK_OK) throw Error(rc, msg);
+            if (rep) rep->wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            return;
+        }
         Exec ex(opts);
         Trace tr(ex.stream);
         Runner R;
@@ -465,7 +508,123 @@ struct mlsk_session {
     std::vector<LevelState> levels;
     std::vector<int64_t> next_k;
     DevArray<double> packed;
+    // multi-GPU session (mlsk_exec_opts.n_devices > 1 or deterministic): the
+    // shards, each a one-device session, in the fixed order their sums are
+    // added; shard_slot[i] = the device slot (host thread) that runs shard i
+    std::vector<std::unique_ptr<mlsk_session>> shards;
+    std::vector<int> shard_slot;
+    int nslots = 0;
+    bool multi() const { return !shards.empty(); }
 };
+
+namespace {
+
+std::unique_ptr<mlsk_session> session_single(const mlsk_model_desc* model, int32_t target, double tp, int64_t M,
+                                             int64_t c0, int64_t L, uint64_t seed, const mlsk_exec_opts* opts) {
+    auto s = std::make_unique<mlsk_session>();
+    s->ex = std::make_unique<Exec>(opts);
+    build_model(s->R.model, model, s->ex->stream);
+    s->R.target = target;
+    s->R.tparam = tp;
+    s->R.seed = seed;
+    s->R.rank = s->ex->rank;
+    s->R.world = s->ex->world;
+    s->R.resolve_engine(s->ex->engine);
+    s->M = M;
+    s->c0 = c0;
+    s->L = L;
+    const int64_t cells = s->R.model.rows * s->R.model.cols;
+    s->levels.resize(L + 1);
+    for (auto& st : s->levels) st.init(cells, s->ex->stream);
+    s->next_k.assign(L + 1, 0);
+    s->packed.alloc((size_t)(L + 1) * (cells + 2));
+    s->packed.zero(s->ex->stream);
+    return s;
+}
+
+// A multi-GPU session: one single-device session per shard.  Plain mode:
+// shard i = device slot i, chunk sharding rank' = rank * n + i of world * n.
+// Deterministic mode: shard v = virtual shard v (rank' = v, world' = vshards)
+// on slot v mod n; shards are summed in v order, so the result does not
+// depend on n.
+std::unique_ptr<mlsk_session> session_multi(const mlsk_model_desc* model, int32_t target, double tp, int64_t M,
+                                            int64_t c0, int64_t L, uint64_t seed, const mlsk_exec_opts* opts) {
+    std::vector<int> slots;
+    bool det;
+    int vsh;
+    Exec::multi_of(opts, slots, det, vsh);
+    if (opts->probe_k > 0) invalid("exec: the coupling probe needs a single device");
+    const int n = (int)slots.size();
+    const int world = opts->world <= 0 ? 1 : opts->world;
+    mlsk_exec_opts home = *opts;
+    home.n_devices = 0;
+    home.device_ids = nullptr;
+    home.deterministic = 0;
+    home.device = slots[0];
+    home.stream = nullptr;  // every shard runs on its device's library stream
+    auto s = session_single(model, target, tp, M, c0, L, seed, &home);  // shape, packed buffer
+    s->nslots = n;
+    const int nshards = det ? vsh : n;
+    for (int i = 0; i < nshards; ++i) {
+        mlsk_exec_opts so = home;
+        so.device = slots[i % n];
+        so.rank = det ? i : opts->rank * n + i;
+        so.world = det ? vsh : world * n;
+        s->shards.push_back(session_single(model, target, tp, M, c0, L, seed, &so));
+        s->shard_slot.push_back(i % n);
+    }
+    return s;
+}
+
+// run `f(shard)` for every shard: one host thread per device slot, each
+// running its shards in order; the first error is rethrown
+void for_shards(mlsk_session* s, const std::function<void(mlsk_session*)>& f) {
+    std::vector<std::thread> pool;
+    std::vector<std::string> err(s->nslots);
+    std::vector<int> code(s->nslots, MLSK_OK);
+    for (int slot = 0; slot < s->nslots; ++slot) {
+        pool.emplace_back([&, slot] {
+            try {
+                for (size_t i = 0; i < s->shards.size(); ++i)
+                    if (s->shard_slot[i] == slot) {
+                        MLSK_CUDA(cudaSetDevice(s->shards[i]->ex->device));
+                        f(s->shards[i].get());
+                    }
+            } catch (const Error& e) {
+                err[slot] = e.what();
+                code[slot] = e.code;
+            } catch (const std::exception& e) {
+                err[slot] = e.what();
+                code[slot] = MLSK_ERUNTIME;
+            }
+        });
+    }
+    for (auto& t : pool) t.join();
+    for (int slot = 0; slot < s->nslots; ++slot)
+        if (code[slot] != MLSK_OK) throw Error(code[slot], err[slot]);
+}
+
+// the shards' level sums / sums of squares / counts added in shard order
+void multi_levels(mlsk_session* s, std::vector<std::vector<double>>& sums, std::vector<double>& sqs,
+                  std::vector<int64_t>& counts) {
+    const int64_t cells = s->R.model.rows * s->R.model.cols;
+    sums.assign(s->L + 1, std::vector<double>(cells, 0.0));
+    sqs.assign(s->L + 1, 0.0);
+    counts.assign(s->L + 1, 0);
+    for (auto& sh : s->shards) {
+        MLSK_CUDA(cudaSetDevice(sh->ex->device));
+        std::vector<const double*> ps;
+        std::vector<double> pq;
+        read_levels(sh->levels, sh->ex->stream, *sh->R.wsp, ps, pq);
+        for (int64_t l = 0; l <= s->L; ++l) {
+            for (int64_t t = 0; t < cells; ++t) sums[l][t] += ps[l][t];
+            sqs[l] += pq[l];
+            counts[l] += sh->levels[l].count;
+        }
+    }
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -505,24 +664,10 @@ int mlsk_session_create(const mlsk_model_desc* model, int32_t target, double tp,
         if (!out) invalid("session: null output pointer");
         if (M < 2 || L < 0 || c0 < 1) invalid("estimator: malformed plan");
         check_target(target, tp);
-        auto s = std::make_unique<mlsk_session>();
-        s->ex = std::make_unique<Exec>(opts);
-        build_model(s->R.model, model, s->ex->stream);
-        s->R.target = target;
-        s->R.tparam = tp;
-        s->R.seed = seed;
-        s->R.rank = s->ex->rank;
-        s->R.world = s->ex->world;
-        s->R.resolve_engine(s->ex->engine);
-        s->M = M;
-        s->c0 = c0;
-        s->L = L;
-        const int64_t cells = s->R.model.rows * s->R.model.cols;
-        s->levels.resize(L + 1);
-        for (auto& st : s->levels) st.init(cells, s->ex->stream);
-        s->next_k.assign(L + 1, 0);
-        s->packed.alloc((size_t)(L + 1) * (cells + 2));
-        s->packed.zero(s->ex->stream);
+        if (!model) invalid("model: null descriptor");
+        const bool multi = opts && (opts->n_devices > 1 || opts->deterministic);
+        auto s = multi ? session_multi(model, target, tp, M, c0, L, seed, opts)
+                       : session_single(model, target, tp, M, c0, L, seed, opts);
         *out = s.release();
     });
 }
@@ -541,6 +686,19 @@ int mlsk_session_run_round(mlsk_session* s, const int64_t* dN) {
                              nullptr});
             s->next_k[l] += dN[l];
         }
+        if (s->multi()) {
+            // every shard runs the round's replication ranges (its chunks of them)
+            for_shards(s, [&](mlsk_session* sh) {
+                std::vector<Runner::Item> its;
+                for (const auto& it : items) {
+                    const int64_t l = (int64_t)it.lv.tag;
+                    its.push_back({it.lv, it.k0, it.k1, &sh->levels[l], nullptr});
+                }
+                sh->R.run(its, sh->ex->stream, 0);
+                MLSK_CUDA(cudaStreamSynchronize(sh->ex->stream));
+            });
+            return;
+        }
         s->R.run(items, s->ex->stream, 0);
         // without a caller stream the call is synchronous; with one, the round is
         // ordered on that stream and the call returns once it is enqueued
@@ -557,11 +715,18 @@ int mlsk_session_stats(mlsk_session* s, mlsk_report* rep) {
         int64_t total_cost = 0;
         std::vector<const double*> sums;
         std::vector<double> sqs;
-        read_levels(s->levels, s->ex->stream, *s->R.wsp, sums, sqs);
+        std::vector<std::vector<double>> msums;
+        std::vector<int64_t> mcounts;
+        if (s->multi()) {
+            multi_levels(s, msums, sqs, mcounts);
+            for (auto& v : msums) sums.push_back(v.data());
+        } else {
+            read_levels(s->levels, s->ex->stream, *s->R.wsp, sums, sqs);
+        }
         for (int64_t l = 0; l <= s->L; ++l) {
             const double* sum = sums[l];
             const double sq = sqs[l];
-            const int64_t n = s->levels[l].count;
+            const int64_t n = s->multi() ? mcounts[l] : s->levels[l].count;
             const int64_t fine = s->c0 * ipow(s->M, l), coarse = l > 0 ? fine / s->M : 0;
             const double inv_n = n > 0 ? 1.0 / (double)n : 0.0;
             const int64_t cost = n * (fine + coarse) * cells;
@@ -586,6 +751,24 @@ int mlsk_session_level_buffer(mlsk_session* s, void** device_ptr, int64_t* n_dou
         if (!s || !device_ptr || !n_doubles) invalid("session: null argument");
         MLSK_CUDA(cudaSetDevice(s->ex->device));
         const int64_t cells = s->R.model.rows * s->R.model.cols;
+        if (s->multi()) {
+            // the shards' sums (added on the host in shard order) into the home device's buffer
+            std::vector<std::vector<double>> ms;
+            std::vector<double> mq;
+            std::vector<int64_t> mc;
+            multi_levels(s, ms, mq, mc);
+            std::vector<double> h((size_t)(s->L + 1) * (cells + 2));
+            for (int64_t l = 0; l <= s->L; ++l) {
+                std::memcpy(h.data() + l * (cells + 2), ms[l].data(), sizeof(double) * cells);
+                h[l * (cells + 2) + cells] = mq[l];
+                h[l * (cells + 2) + cells + 1] = (double)mc[l];
+            }
+            MLSK_CUDA(cudaSetDevice(s->ex->device));
+            MLSK_CUDA(cudaMemcpy(s->packed.p, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+            *device_ptr = s->packed.p;
+            *n_doubles = (int64_t)h.size();
+            return;
+        }
         // pack [(sum Y, sum ||Y||^2, count)] per level on the device (sum includes the open chunk)
         for (int64_t l = 0; l <= s->L; ++l) {
             const LevelState& st = s->levels[l];
@@ -607,6 +790,10 @@ int mlsk_session_level_buffer(mlsk_session* s, void** device_ptr, int64_t* n_dou
 int mlsk_session_synchronize(mlsk_session* s) {
     return guard([&] {
         if (!s) invalid("session: null argument");
+        for (auto& sh : s->shards) {
+            MLSK_CUDA(cudaSetDevice(sh->ex->device));
+            MLSK_CUDA(cudaStreamSynchronize(sh->ex->stream));
+        }
         MLSK_CUDA(cudaSetDevice(s->ex->device));
         MLSK_CUDA(cudaStreamSynchronize(s->ex->stream));
     });
@@ -615,6 +802,10 @@ int mlsk_session_synchronize(mlsk_session* s) {
 int mlsk_session_destroy(mlsk_session* s) {
     return guard([&] {
         if (!s) return;
+        for (auto& sh : s->shards) {
+            cudaSetDevice(sh->ex->device);
+            cudaStreamSynchronize(sh->ex->stream);
+        }
         cudaSetDevice(s->ex->device);
         cudaStreamSynchronize(s->ex->stream);
         delete s;

@@ -170,7 +170,11 @@ __device__ __forceinline__ void gen_phase(const DevModel& M, const Tables& T, ui
 __global__ void __launch_bounds__(GEN_THREADS, 4)
 k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
                  int64_t cc, double w_fine, double w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kc0,
-                 double* __restrict__ Apan, double* __restrict__ Bpan, uint32_t* __restrict__ idx_out) {
+                 double* __restrict__ Apan, double* __restrict__ Bpan, uint32_t* __restrict__ idx_out, int64_t pcc) {
+    // pcc >= cc: K slots [0, pcc) hold the coarse prefix t < cc (zero padding
+    // up to pcc), slots [pcc, ...) the suffix t >= cc.  pcc = cc (identity
+    // target) is the plain layout; a nonlinear target pads the prefix to whole
+    // K-chunks so the GEMM can read the coarse sum at a chunk boundary.
     __shared__ __align__(16) double2 s_sc[1024];
     __shared__ __align__(16) double2 s_lg[128];
     extern __shared__ __align__(16) double gen_dyn[];  // 2 x GROWS x KC tiles (past the 48 KB static limit)
@@ -190,10 +194,11 @@ k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restr
         const uint64_t key = derive_seed(seed, tag, (uint64_t)ks[b]);
         __syncthreads();  // previous item's readers of s_j are done
         if (tid < KC) {
-            const int64_t t = (kc0 + kc) * KC + tid;  // column of the sample (kc0: first chunk of this K-range)
-            int j = 0;  // padding columns (t >= c): column 0 with weight 0
+            const int64_t sl = (kc0 + kc) * KC + tid;  // K slot (kc0: first chunk of this K-range)
+            const int64_t t = sl < pcc ? sl : sl - pcc + cc;  // column of the sample
+            int j = 0;  // padding slots: column 0 with weight 0
             double w = 0.0;
-            if (t < c) {
+            if (sl < pcc ? t < cc : t < c) {
                 const u32x4 r = philox((uint32_t)(t >> 1), 0, 0, MLSK_CTR_INDEX, key);
                 const uint32_t ix = index_from_u64((t & 1) ? hi64(r) : lo64(r), M.n, M.log2n, M.cum);
                 j = (int)(ix - 1);
@@ -320,10 +325,32 @@ struct GemmShape {
 // one generator CTA beside the GEMM CTA (measured +2% on the config-2 step).
 // SPLIT: one sample split along K per launch (split_part 1 first, 2 middle,
 // 3 last); a separate instantiation keeps the common path's registers intact.
-template <bool SPLIT>
+// NL: nonlinear target.  The panels hold the coarse prefix in K-chunks
+// [0, pre_kc) (uniform weights n / c); after chunk pre_kc - 1 every thread
+// stores f(cscale * acc) (the coarse estimate, cscale = c / cc) of its
+// fragments to `nl_scratch` (coalesced, L2-resident), and the sample's
+// epilogue forms Y = f(acc) - f(coarse) (estimators.cpp:137-147).
+struct NlArgs {
+    int target;
+    double tparam;
+    int64_t pre_kc;  // 0: level 0 (no coarse term)
+    double cscale;
+    double* scratch;
+};
+// Y of one fragment entry at the sample's end: f(fine) - f(coarse)
+__device__ __forceinline__ double nl_y(const NlArgs& a, int g, int i, int j, int e, double fine) {
+    double y = apply_target(a.target, a.tparam, fine);
+    if (a.pre_kc > 0) {
+        const double* sc = a.scratch + (int64_t)g * (4 * NJ * 2) * GEMM_THREADS + threadIdx.x;
+        y = __dsub_rn(y, sc[(int64_t)((i * NJ + j) * 2 + e) * GEMM_THREADS]);
+    }
+    return y;
+}
+template <bool SPLIT, bool NL>
 __global__ void __maxnreg__(GEMM_MAXNREG)
 k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, GemmShape sh,
-           double* __restrict__ part, double* __restrict__ part_sq, int split_part, double* __restrict__ ypart) {
+           double* __restrict__ part, double* __restrict__ part_sq, int split_part, double* __restrict__ ypart,
+           NlArgs nla) {
     extern __shared__ __align__(1024) unsigned char smem[];
     double* sA = reinterpret_cast<double*>(smem);
     double* sB = reinterpret_cast<double*>(smem + STAGES * A_STAGE_BYTES);
@@ -474,6 +501,18 @@ k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, Gem
             s = 0;
             ph ^= 1u;
         }
+        if (NL && kc + 1 == nla.pre_kc) {
+            // the coarse prefix is complete: f(coarse) of this thread's fragments
+            double* sc = nla.scratch + (int64_t)g * (4 * NJ * 2) * GEMM_THREADS + threadIdx.x;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        sc[(int64_t)((i * NJ + j) * 2 + e) * GEMM_THREADS] =
+                            apply_target(nla.target, nla.tparam, __dmul_rn(nla.cscale, acc[i][j][e]));
+        }
         if (++kc == sh.nkc) {
             kc = 0;
             if (SPLIT) {
@@ -507,7 +546,7 @@ k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, Gem
                     for (int j = 0; j < NJ; ++j)
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
-                            const double y = acc[i][j][e];
+                            const double y = NL ? nl_y(nla, g, i, j, e, acc[i][j][e]) : acc[i][j][e];
                             sq = __fma_rn(y, y, sq);
                             const int w = 2 * (2 * j + e);
                             const double v = __dadd_rn(__hiloint2double((int)r[w + 1], (int)r[w]), y);
@@ -525,7 +564,7 @@ k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, Gem
                     for (int j = 0; j < NJ; ++j)
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
-                            const double y = acc[i][j][e];
+                            const double y = NL ? nl_y(nla, g, i, j, e, acc[i][j][e]) : acc[i][j][e];
                             sq = __fma_rn(y, y, sq);
                             S[i][j][e] = __dadd_rn(S[i][j][e], y);
                             acc[i][j][e] = 0.0;
@@ -591,7 +630,8 @@ __global__ void k_reduce_tiles(const double* __restrict__ part, const double* __
 __global__ void __launch_bounds__(256)
 k_fused_inner(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
               int64_t cc, double w_fine, double w_coarse, double* __restrict__ y_out,
-              uint32_t* __restrict__ idx_out) {
+              uint32_t* __restrict__ idx_out, int target, double tparam) {
+    const bool nl = target != MLSK_TARGET_IDENTITY;  // prefix / suffix apart (k_fused_inner_multi<true>)
     __shared__ __align__(16) double2 s_sc[256];
     __shared__ __align__(16) double2 s_lg[128];
     load_tables(s_sc, s_lg, M.tab);
@@ -603,7 +643,7 @@ k_fused_inner(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restrict
     const int warps = (gridDim.x * blockDim.x) >> 5;
     for (int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
         const uint64_t key = derive_seed(seed, tag, (uint64_t)ks[b]);
-        double acc = 0.0;
+        double acc = 0.0, pre = 0.0;
         for (int64_t tp = lane; 2 * tp < c; tp += 32) {
             const u32x4 ri = philox((uint32_t)tp, 0, 0, MLSK_CTR_INDEX, key);
 #pragma unroll
@@ -618,10 +658,17 @@ k_fused_inner(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restrict
                 box_muller(lo64(r), hi64(r), z0, z1, T);
                 const double a = __dadd_rn(M.mean_a[j], __dmul_rn(M.sd, z0));
                 const double bb = __dadd_rn(M.mean_b[j], __dmul_rn(M.sd, z1));
-                acc = __fma_rn(__dmul_rn(a, bb), t < cc ? w_coarse : w_fine, acc);
+                if (nl && t < cc) pre = __fma_rn(__dmul_rn(a, bb), w_fine, pre);
+                else acc = __fma_rn(__dmul_rn(a, bb), t < cc ? w_coarse : w_fine, acc);
             }
         }
         acc = warp_sum(acc);
+        if (nl) {
+            pre = warp_sum(pre);
+            double y = apply_target(target, tparam, __dadd_rn(pre, acc));
+            if (cc > 0) y = __dsub_rn(y, apply_target(target, tparam, __dmul_rn((double)c / (double)cc, pre)));
+            acc = y;
+        }
         if (lane == 0) y_out[b] = acc;
     }
 }
@@ -658,7 +705,7 @@ constexpr int INNER_G = 8;
 struct InnerPart {
     uint64_t tag;
     int64_t c, cc;
-    double w_fine, w_coarse;
+    double w_fine, w_coarse;  // nonlinear targets: both n / c (prefix and suffix kept apart)
     int64_t ks_off;  // into the round's replication list
     int64_t y_off;   // first output slot (parts are contiguous)
     int64_t nb;
@@ -670,9 +717,13 @@ struct InnerParts {
     InnerPart p[INNER_MAX_PARTS];
 };
 
+// NL (nonlinear target f1 / f2, models.cpp:99-117): the prefix and suffix
+// sums are kept apart, Y = f((n/c)(S_pre + S_suf)) - f((n/cc) S_pre) per
+// replication (estimators.cpp:78-80), instead of one signed sum.
+template <bool NL>
 __global__ void __launch_bounds__(256)
 k_fused_inner_multi(DevModel M, uint64_t seed, const int64_t* __restrict__ ks, InnerParts P, int64_t total,
-                    double* __restrict__ y_out) {
+                    double* __restrict__ y_out, int target, double tparam) {
     __shared__ __align__(16) double2 s_sc[256];
     __shared__ __align__(16) double2 s_lg[128];
     load_tables(s_sc, s_lg, M.tab);
@@ -692,7 +743,7 @@ k_fused_inner_multi(DevModel M, uint64_t seed, const int64_t* __restrict__ ks, I
         if (live)
             while (pi + 1 < P.n && sidx >= P.p[pi + 1].y_off) ++pi;
         const InnerPart& q = P.p[pi];
-        double acc = 0.0;
+        double acc = 0.0, pre = 0.0;
         if (live) {
             const int64_t b = sidx - q.y_off;
             const uint64_t key = derive_seed(seed, q.tag, (uint64_t)ks[q.ks_off + b]);
@@ -709,12 +760,24 @@ k_fused_inner_multi(DevModel M, uint64_t seed, const int64_t* __restrict__ ks, I
                     box_muller(lo64(r), hi64(r), z0, z1, T);
                     const double a = __dadd_rn(M.mean_a[j], __dmul_rn(M.sd, z0));
                     const double bb = __dadd_rn(M.mean_b[j], __dmul_rn(M.sd, z1));
-                    acc = __fma_rn(__dmul_rn(a, bb), t < q.cc ? q.w_coarse : q.w_fine, acc);
+                    if (NL && t < q.cc) pre = __fma_rn(__dmul_rn(a, bb), q.w_fine, pre);
+                    else acc = __fma_rn(__dmul_rn(a, bb), t < q.cc ? q.w_coarse : q.w_fine, acc);
                 }
             }
         }
 #pragma unroll
         for (int o = INNER_G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (NL) {
+#pragma unroll
+            for (int o = INNER_G / 2; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+            if (live && gl == 0) {
+                // fine = (n/c)(S_pre + S_suf), coarse = (n/cc) S_pre = (c/cc) (n/c) S_pre
+                double y = apply_target(target, tparam, __dadd_rn(pre, acc));
+                if (q.cc > 0)
+                    y = __dsub_rn(y, apply_target(target, tparam, __dmul_rn((double)q.c / (double)q.cc, pre)));
+                acc = y;
+            }
+        }
         if (live && gl == 0) y_out[sidx] = acc;
     }
 }
@@ -752,13 +815,48 @@ int sm_count() {
     return v;
 }
 
+
+// RNG roofline of the inner-product path (config 1): exactly the per-index
+// work of k_fused_inner_multi -- half an index Philox block, the (a, b)
+// Philox block, one Box-Muller pair, two mean gathers, one fma -- with no
+// level bookkeeping, replication reduction or launch boundary.  Its
+// index-samples / s is the ceiling the fused inner kernel is measured against.
+__global__ void __launch_bounds__(256) k_index_rate(DevModel M, uint64_t seed, int64_t pairs, double* sink) {
+    __shared__ __align__(16) double2 s_sc[256];
+    __shared__ __align__(16) double2 s_lg[128];
+    load_tables(s_sc, s_lg, M.tab);
+    __syncthreads();
+    Tables T = M.tab;
+    T.sincos_d = reinterpret_cast<const double*>(s_sc);
+    T.log_d = reinterpret_cast<const double*>(s_lg);
+    const uint64_t key = derive_seed(seed, blockIdx.x, threadIdx.x);
+    double acc = 0.0;
+    for (int64_t tp = 0; tp < pairs; ++tp) {
+        const u32x4 ri = philox((uint32_t)tp, 0, 0, MLSK_CTR_INDEX, key);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t ix = index_from_u64(h ? hi64(ri) : lo64(ri), M.n, M.log2n, M.cum);
+            const int64_t j = (int64_t)ix - 1;
+            const u32x4 r = philox((uint32_t)j, 0, 0, MLSK_CTR_A, key);
+            double z0, z1;
+            box_muller(lo64(r), hi64(r), z0, z1, T);
+            const double a = __dadd_rn(M.mean_a[j], __dmul_rn(M.sd, z0));
+            const double bb = __dadd_rn(M.mean_b[j], __dmul_rn(M.sd, z1));
+            acc = __fma_rn(__dmul_rn(a, bb), 0.5, acc);
+        }
+    }
+    if (acc == 1234.5678) sink[0] = acc;  // keeps the loop
+}
+
 }  // namespace
 
 bool tc_supported(const Model& M, int target);                                   // mlsk_tc.cu
 
+// fp64 gauss models (configs 1-2) take any target: identity as one signed
+// contraction, f1 / f2 with the prefix and suffix kept apart (k_fused_inner*
+// and k_gemm_f64<NL>); the fp32 engine is identity-only (tc_supported).
 bool fused_supported(const Model& M, int target) {
-    return (target == MLSK_TARGET_IDENTITY && M.dm.stream == MLSK_STREAM_PHILOX &&
-            M.dm.kind == MLSK_MODEL_GAUSS_MEAN && M.dm.dtype == MLSK_F64) ||
+    return (M.dm.stream == MLSK_STREAM_PHILOX && M.dm.kind == MLSK_MODEL_GAUSS_MEAN && M.dm.dtype == MLSK_F64) ||
            tc_supported(M, target);
 }
 
@@ -766,7 +864,8 @@ namespace {
 
 class F64Engine final : public PanelEngine {
    public:
-    F64Engine(const Model& M, Workspace& ws) : M_(M), ws_(ws) {
+    F64Engine(const Model& M, Workspace& ws, int target, double tparam)
+        : M_(M), ws_(ws), target_(target), tparam_(tparam), nl_(target != MLSK_TARGET_IDENTITY) {
         nsm_ = sm_count();
         MP_ = (M.rows + BM - 1) / BM * BM;
         PP_ = (M.cols + BN - 1) / BN * BN;
@@ -775,9 +874,9 @@ class F64Engine final : public PanelEngine {
         Gs_ = std::max(1, nsm_ / T_);
         smem_ = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 2 * STAGES * 8;
         const int smem = smem_;
-        once_per_device((const void*)&k_gemm_f64<false>, [smem] {
-            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_f64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_f64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        once_per_device((const void*)&k_gemm_f64<false, false>, [smem] {
+            for (auto f : {k_gemm_f64<false, false>, k_gemm_f64<true, false>, k_gemm_f64<false, true>})
+                MLSK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_f64, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            GEN_DYN_SMEM));
         });
@@ -794,17 +893,17 @@ class F64Engine final : public PanelEngine {
     int64_t group_size() const override { return Gs_; }
     void gen(cudaStream_t s, uint64_t seed, uint64_t tag, const int64_t* ks, int nb, int64_t c, int64_t cc,
              double w_fine, double w_coarse, void* panels, uint32_t* idx, const KRange& kr) override {
-        const int64_t k = kr.nkc >= 0 ? kr.nkc : nkc(c);
+        const int64_t k = kr.nkc >= 0 ? kr.nkc : nchunks(c, cc);
         double* Apan = static_cast<double*>(panels);
         double* Bpan = Apan + (size_t)nb * k * MP_ * KC;
         Prof p("gen_panels_f64", s);
         k_gen_panels_f64<<<(int)std::min<int64_t>((int64_t)nb * k, (int64_t)gen_ctas_), GEN_THREADS, GEN_DYN_SMEM, s>>>(
-            M_.dm, seed, tag, ks, nb, c, cc, w_fine, w_coarse, MP_, PP_, k, kr.kc0, Apan, Bpan, idx);
+            M_.dm, seed, tag, ks, nb, c, cc, w_fine, w_coarse, MP_, PP_, k, kr.kc0, Apan, Bpan, idx, pcc(cc));
         launched();
     }
-    void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, int64_t, double, double, LevelState& st,
+    void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, int64_t cc, double, double, LevelState& st,
               const KRange& kr) override {
-        const int64_t k = kr.nkc >= 0 ? kr.nkc : nkc(c);
+        const int64_t k = kr.nkc >= 0 ? kr.nkc : nchunks(c, cc);
         const double* Apan = static_cast<const double*>(panels);
         const double* Bpan = Apan + (size_t)nb * k * MP_ * KC;
         double* part = ws_.partial.p;
@@ -817,10 +916,21 @@ class F64Engine final : public PanelEngine {
         GemmShape sh{nb, k, MP_, PP_, T_, Gs_, tiles_n_};
         {
             Prof p("gemm_f64", s);
-            if (kr.part == 0)
-                k_gemm_f64<false><<<T_ * Gs_, GEMM_THREADS, smem_, s>>>(Apan, Bpan, sh, part, part_sq, 0, nullptr);
+            NlArgs nla{target_, tparam_, 0, 1.0, nullptr};
+            if (nl_) {
+                if (kr.part != 0) throw Error(MLSK_EINVAL, "fused engine: nonlinear targets need whole level-samples");
+                nla.pre_kc = cc > 0 ? (cc + KC - 1) / KC : 0;
+                nla.cscale = cc > 0 ? (double)c / (double)cc : 1.0;
+                ws_.nl_scratch.ensure((size_t)T_ * Gs_ * (4 * NJ * 2) * GEMM_THREADS);
+                nla.scratch = ws_.nl_scratch.p;
+                k_gemm_f64<false, true><<<T_ * Gs_, GEMM_THREADS, smem_, s>>>(Apan, Bpan, sh, part, part_sq, 0,
+                                                                              nullptr, nla);
+            } else if (kr.part == 0)
+                k_gemm_f64<false, false><<<T_ * Gs_, GEMM_THREADS, smem_, s>>>(Apan, Bpan, sh, part, part_sq, 0,
+                                                                               nullptr, nla);
             else
-                k_gemm_f64<true><<<T_ * Gs_, GEMM_THREADS, smem_, s>>>(Apan, Bpan, sh, part, part_sq, kr.part, ypart);
+                k_gemm_f64<true, false><<<T_ * Gs_, GEMM_THREADS, smem_, s>>>(Apan, Bpan, sh, part, part_sq, kr.part,
+                                                                              ypart, nla);
         }
         if (kr.part == 1 || kr.part == 2) {  // the sample completes in a later launch
             launched();
@@ -835,16 +945,24 @@ class F64Engine final : public PanelEngine {
         launched(2);
     }
 
+    // nonlinear targets: the coarse prefix padded to whole K-chunks
+    int64_t nchunks(int64_t c, int64_t cc) const override {
+        return nl_ ? (cc + KC - 1) / KC + (c - cc + KC - 1) / KC : (c + KC - 1) / KC;
+    }
+
    private:
-    static int64_t nkc(int64_t c) { return (c + KC - 1) / KC; }
+    int64_t pcc(int64_t cc) const { return nl_ ? (cc + KC - 1) / KC * KC : cc; }
     const Model& M_;
     Workspace& ws_;
+    int target_;
+    double tparam_;
+    bool nl_;
     int nsm_, T_, Gs_, tiles_n_, smem_, gen_ctas_;
     int64_t MP_, PP_;
 };
 
-std::unique_ptr<PanelEngine> make_f64_engine(const Model& M, Workspace& ws) {
-    return std::unique_ptr<PanelEngine>(new F64Engine(M, ws));
+std::unique_ptr<PanelEngine> make_f64_engine(const Model& M, Workspace& ws, int target, double tparam) {
+    return std::unique_ptr<PanelEngine>(new F64Engine(M, ws, target, tparam));
 }
 
 constexpr int NBUF = 3;  // panel buffers in flight (gen i+1, i+2 while GEMM i)
@@ -936,6 +1054,8 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
     Pipe& P = pipe_of(ws);
     const int sms = sm_count();
     const double n = (double)M.desc.n;
+    // nonlinear target: fine and coarse kept apart (uniform weights n / c)
+    const bool nl = a.target != MLSK_TARGET_IDENTITY;
 
     // replication lists of all jobs, staged to the device once per round
     std::vector<std::vector<int64_t>> jks(jobs.size());
@@ -967,8 +1087,12 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
             const int64_t grid = std::min<int64_t>((filled * INNER_G + 255) / 256, (int64_t)sms * 16);
             {
                 Prof p("fused_inner_f64", P.s_gen);
-                k_fused_inner_multi<<<(int)std::max<int64_t>(grid, 1), 256, 0, P.s_gen>>>(M.dm, a.seed, P.ks.p, parts,
-                                                                                         filled, ws.v.p);
+                if (nl)
+                    k_fused_inner_multi<true><<<(int)std::max<int64_t>(grid, 1), 256, 0, P.s_gen>>>(
+                        M.dm, a.seed, P.ks.p, parts, filled, ws.v.p, a.target, a.target_param);
+                else
+                    k_fused_inner_multi<false><<<(int)std::max<int64_t>(grid, 1), 256, 0, P.s_gen>>>(
+                        M.dm, a.seed, P.ks.p, parts, filled, ws.v.p, a.target, a.target_param);
             }
             {
                 Prof p("reduce_inner", P.s_gen);
@@ -989,7 +1113,7 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
             FusedJob& job = jobs[j];
             const int64_t c = job.lv.c, cc = job.lv.cc;
             const double w_fine = n / (double)c;
-            const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;
+            const double w_coarse = cc > 0 && !nl ? w_fine - n / (double)cc : w_fine;
             const int64_t total = (int64_t)jks[j].size();
             for (int64_t off = 0; off < total;) {
                 if (parts.n == INNER_MAX_PARTS || filled == max_slice) flush();
@@ -1012,7 +1136,7 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
             FusedJob& job = jobs[j];
             const int64_t c = job.lv.c, cc = job.lv.cc;
             const double w_fine = n / (double)c;
-            const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;
+            const double w_coarse = cc > 0 && !nl ? w_fine - n / (double)cc : w_fine;
             const int64_t total = (int64_t)jks[j].size();
             const int64_t max_batch = 1 << 20;
             for (int64_t off = 0; off < total; off += max_batch) {
@@ -1027,7 +1151,8 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
                 {
                     Prof p("fused_inner_f64", P.s_gen);
                     k_fused_inner<<<grid, 256, 0, P.s_gen>>>(M.dm, a.seed, job.lv.tag, P.ks.p + job_off[j] + off, nb,
-                                                             c, cc, w_fine, w_coarse, ws.v.p, idx);
+                                                             c, cc, w_fine, w_coarse, ws.v.p, idx, a.target,
+                                                             a.target_param);
                 }
                 {
                     Prof p("reduce_inner", P.s_gen);
@@ -1053,7 +1178,8 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
     // ---- matrix path: batches of replications, software-pipelined over a
     // panel engine (fp64 DMMA or the tcgen05 3xTF32 engine for fp32 models)
     // geometry-only object, rebuilt per round (the workspace may be shared by models)
-    std::unique_ptr<PanelEngine> engine = tc_supported(M, a.target) ? make_tc_engine(M, ws) : make_f64_engine(M, ws);
+    std::unique_ptr<PanelEngine> engine =
+        tc_supported(M, a.target) ? make_tc_engine(M, ws) : make_f64_engine(M, ws, a.target, a.target_param);
     PanelEngine& E = *engine;
     const int64_t Gs = E.group_size();
     int64_t budget = int64_t(768) << 20;  // panel bytes per batch (x NBUF in flight; 384 MiB measured 1% slower)
@@ -1067,9 +1193,12 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
     std::vector<Batch> batches;
     int64_t max_panel = 0;
     for (size_t j = 0; j < jobs.size(); ++j) {
-        const int64_t per = E.panel_bytes(jobs[j].lv.c);
+        const int64_t per = E.panel_bytes(jobs[j].lv.c, jobs[j].lv.cc);
         const int64_t total = (int64_t)jks[j].size();
         if (per > split_limit && E.splits_k()) {
+            if (nl)
+                throw Error(MLSK_EINVAL, "fused engine: nonlinear targets need a level-sample's panels within one "
+                                         "batch (" + std::to_string(split_limit >> 20) + " MiB)");
             // one sample's panels exceed a batch: K-segments of one sample each,
             // the partial Y carried between them
             if (jobs[j].probe_host)
@@ -1118,8 +1247,8 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         const Batch& bt = batches[i];
         FusedJob& job = jobs[bt.job];
         const int64_t c = job.lv.c, cc = job.lv.cc;
-        const double w_fine = n / (double)c;                                 // n/c
-        const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;  // n/c - n/cc on the prefix
+        const double w_fine = n / (double)c;                                        // n/c
+        const double w_coarse = cc > 0 && !nl ? w_fine - n / (double)cc : w_fine;  // n/c - n/cc on the prefix
         const int buf = (int)(i % NBUF);
         void* panels = P.panels[buf].p;
         uint32_t* idx = nullptr;
@@ -1154,6 +1283,45 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
     }
     MLSK_CUDA(cudaEventRecord(P.end, P.s_mm));
     MLSK_CUDA(cudaStreamWaitEvent(a.stream, P.end, 0));
+}
+
+
+double measure_index_rate(int device) {
+    if (device >= 0) MLSK_CUDA(cudaSetDevice(device));
+    mlsk_model_desc d{};
+    d.kind = MLSK_MODEL_GAUSS_MEAN;
+    d.dtype = MLSK_F64;
+    d.stream_mode = MLSK_STREAM_PHILOX;
+    d.n = 4096;  // config 1
+    d.sd = 1.0;
+    d.mean_lo = 0.0;
+    d.mean_hi = 1.0;
+    d.data_seed = 1;
+    Model M;
+    build_model(M, &d, 0);
+    DevArray<double> sink(1);
+    const int grid = sm_count() * 8;
+    const int64_t pairs = 256;
+    k_index_rate<<<grid, 256>>>(M.dm, 7, 4, sink.p);
+    launched();
+    MLSK_CUDA(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0);
+        k_index_rate<<<grid, 256>>>(M.dm, 7 + r, pairs, sink.p);
+        cudaEventRecord(e1);
+        launched();
+        MLSK_CUDA(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = std::min(best, ms);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return (double)grid * 256 * pairs * 2 / (best * 1e-3);
 }
 
 }  // namespace mlsk

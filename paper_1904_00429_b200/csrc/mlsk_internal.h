@@ -134,6 +134,8 @@ struct Model {
 void build_model(Model& M, const mlsk_model_desc* d, cudaStream_t st);
 bool model_is_vector(const mlsk_model_desc* d);
 Tables device_tables();
+// index-samples / s of the config-1 per-index RNG work (mlsk_measure_index_rate)
+double measure_index_rate(int device);
 
 // A level of the MLMC hierarchy (estimators.cpp:120-122 with c_l = c0 M^l).
 struct LevelSpec {
@@ -214,6 +216,7 @@ struct Workspace {
     DevArray<double> panel_a, panel_b, partial;
     DevArray<float> ypart;     // partial Y of a sample split along K (tcgen05 engine)
     DevArray<double> ypart64;  // same, fp64 engine
+    DevArray<double> nl_scratch;  // f(coarse) per fragment entry (fp64 engine, nonlinear targets)
 };
 
 struct RunArgs {
@@ -252,7 +255,12 @@ struct PanelEngine {
     virtual ~PanelEngine() = default;
     virtual int64_t chunk_cols() const = 0;   // K columns per chunk
     virtual int64_t chunk_bytes() const = 0;  // panel bytes of one chunk of one sample
-    int64_t panel_bytes(int64_t c) const { return (c + chunk_cols() - 1) / chunk_cols() * chunk_bytes(); }
+    // K-chunks of one level-sample (c indices, coarse prefix cc)
+    virtual int64_t nchunks(int64_t c, int64_t cc) const {
+        (void)cc;
+        return (c + chunk_cols() - 1) / chunk_cols();
+    }
+    int64_t panel_bytes(int64_t c, int64_t cc) const { return nchunks(c, cc) * chunk_bytes(); }
     virtual bool splits_k() const { return false; }
     virtual int64_t group_size() const = 0;   // samples per round of the CTA groups
     virtual void gen(cudaStream_t s, uint64_t seed, uint64_t tag, const int64_t* ks, int nb, int64_t c, int64_t cc,

@@ -276,4 +276,12 @@ double mlsk_measure_tf32_peak(int device, int n) {
     return result;
 }
 
+// Config-1 RNG roofline: index-samples / s of the fused inner kernel's
+// per-index work alone (k_index_rate).
+double mlsk_measure_index_rate(int device) {
+    double result = -1.0;
+    run_guarded([&] { result = measure_index_rate(device); });
+    return result;
+}
+
 }  // extern "C"

@@ -47,12 +47,25 @@ constexpr int TTILE = TBM * TBK * 4;                // 8 KB: one 128-row K-chunk
 constexpr int TA_BYTES = TTILE, TB_BYTES = 2 * TTILE;
 constexpr int TSTAGE_BYTES = 2 * TA_BYTES + 2 * TB_BYTES;  // A_hi, A_lo, B_hi, B_lo: 48 KB
 constexpr int EPI_WARPS = 16;                       // four per TMEM lane quadrant (64-column quarters)
-constexpr int TC_THREADS = 64 + 32 * EPI_WARPS;     // producer, MMA, epilogue warps
+// warpgroup 0: producer (warp 0), TMEM allocation + MMA issue (warp 1), two
+// idle warps; warpgroups 1-4: epilogue.  setmaxnreg moves registers from the
+// control warpgroup to the epilogue (24 / 112 per thread) for its 64-entry
+// running sum / sample Y plus a 16-column TMEM load.  The budget is the
+// launch's own allocation (640 threads x 96 = 61440; a launch of 18 warps
+// or more is capped at 96 registers: five warps share one SMSP's 16 K):
+// 4 x 32 x 24 + 16 x 32 x 112 = 60416 <= 61440, so setmaxnreg.inc cannot
+// wait forever for registers no warp will release.
+constexpr int CTRL_WARPS = 4;
+constexpr int TC_THREADS = 32 * (CTRL_WARPS + EPI_WARPS);
+constexpr int CTRL_REGS = 24, EPI_REGS = 112;
+static_assert(32 * (CTRL_WARPS * CTRL_REGS + EPI_WARPS * EPI_REGS) <= TC_THREADS * 96,
+              "setmaxnreg budget exceeds the launch allocation: the epilogue's inc would block forever");
 #ifndef MLSK_TC_FLUSH
 #define MLSK_TC_FLUSH 32
 #endif
 constexpr int FLUSH = MLSK_TC_FLUSH;                // samples per fp32 running-sum flush
 constexpr uint32_t TMEM_COLS = 2 * TBN;             // two accumulators: all 512 columns
+constexpr int TC_SEG = 32;                          // K-chunks (K = 512) per TMEM accumulation segment
 constexpr int GEN_T = 256;
 
 // ----------------------------------------------------------------- PTX
@@ -552,6 +565,13 @@ struct TcShape {
     // the epilogue scales Y by escale = |w| -- bit-identical to B = diag(w) A^T
     int64_t neg_kc, kc0;
     float escale;
+    // K-chunks per TMEM accumulation segment (0: a CTA's whole K-range of a
+    // sample is one segment).  tcgen05's fp32 accumulation rounds the running
+    // sum toward zero, so its error grows with the number of MMAs folded into
+    // one accumulator (measured: ~4e-8 relative per MMA, 1.3e-4 at K = 16384);
+    // long samples restart the accumulator every `seg` K-chunks and the
+    // epilogue adds the segments in registers with round-to-nearest.
+    int seg = 0;
 };
 
 // tile index -> (tile row of 128, tile column of 256)
@@ -582,7 +602,9 @@ __device__ __forceinline__ int tile_index(const TcShape& sh, int tm, int tn) {
 
 // SPLIT: one sample split along K per launch (split_part 1 first, 2 middle,
 // 3 last, partial Y in ypart); a separate instantiation for the common path.
-template <bool SPLIT>
+// SEGM: a sample's K-range runs as several TMEM accumulation segments of
+// sh.seg K-chunks (TcShape::seg) summed in registers; else one segment.
+template <bool SPLIT, bool SEGM>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, const float* __restrict__ Bhi,
               const float* __restrict__ Blo, TcShape sh, double* __restrict__ part, double* __restrict__ part_sq,
@@ -590,7 +612,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
     extern __shared__ __align__(1024) unsigned char dsm[];
     // 1024-byte aligned stage ring (SW128 atoms)
     unsigned char* ring = dsm + ((1024 - (smem_addr(dsm) & 1023)) & 1023);
-    __shared__ __align__(8) uint64_t bars[2 * TSTAGES + 4];  // full, empty, tmem_full[2], tmem_empty[2]
+    __shared__ __align__(8) uint64_t bars[2 * TSTAGES + 5];  // full, empty, tmem_full[2], tmem_empty[2], tmem_done
     __shared__ uint32_t s_tmem;
     __shared__ double s_sq[EPI_WARPS];
 
@@ -605,9 +627,12 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
     const int64_t kb = kpar ? grp * kh : 0;                              // this CTA's K-chunk range
     const int64_t ke = kpar ? (kb + kh < sh.nkc ? kb + kh : sh.nkc) : sh.nkc;
     const int64_t iters = (int64_t)my_samples * (ke - kb);
+    const int64_t seg = SEGM && sh.seg > 0 && sh.seg < ke - kb ? sh.seg : ke - kb;  // K-chunks per TMEM segment
+    const int nseg = (int)((ke - kb + seg - 1) / seg);                             // segments per sample
 
     const uint32_t full0 = smem_addr(&bars[0]), empty0 = smem_addr(&bars[TSTAGES]);
     const uint32_t tfull0 = smem_addr(&bars[2 * TSTAGES]), tempty0 = smem_addr(&bars[2 * TSTAGES + 2]);
+    const uint32_t tdone = smem_addr(&bars[2 * TSTAGES + 4]);
     if (threadIdx.x == 0) {
         for (int s = 0; s < TSTAGES; ++s) {
             bar_init(full0 + 8 * s, 1);
@@ -617,6 +642,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             bar_init(tfull0 + 8 * a, 1);
             bar_init(tempty0 + 8 * a, EPI_WARPS);
         }
+        bar_init(tdone, EPI_WARPS);  // every epilogue warp finished with TMEM
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -629,6 +655,11 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
     tc_fence_after();
     const uint32_t tmem = s_tmem;
 
+    // Role dispatch.  Each setmaxnreg dominates its role's code and the roles
+    // do not join again (no common tail): ptxas then allocates each region
+    // within its own register budget.
+    if (warp < CTRL_WARPS) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CTRL_REGS));
     if (warp == 0) {
         // --------------------------------------------------- producer
         if (lane == 0) {
@@ -661,10 +692,11 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             int s = 0;
             uint32_t ph = 0;
             int64_t kc = kb;
+            int64_t sgc = 0;  // K-chunks of the current accumulation segment so far
             int abuf = 0;
             uint32_t aph = 0;  // bit a = phase of accumulator a (no indexed local array)
             for (int64_t it = 0; it < iters; ++it) {
-                if (kc == kb) {  // first K-chunk of this CTA's range of a sample (kpar: kb > 0)
+                if (sgc == 0) {  // first K-chunk of a segment (kpar: this CTA's range starts at kb > 0)
                     bar_wait(tempty0 + 8 * abuf, ((aph >> abuf) & 1u) ^ 1u);  // epilogue released this accumulator
                     tc_fence_after();
                 }
@@ -679,31 +711,43 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                     const uint64_t bh = sw_desc(st + 2 * TA_BYTES + kk * 32);
                     const uint64_t bl = sw_desc(st + 2 * TA_BYTES + TB_BYTES + kk * 32);
 #ifndef MLSK_TC_ABL_NOMMA  // ablation: no MMAs (commits only)
-                    tc_mma_tf32(dcol, ah, bh, id, (kc > kb || kk > 0) ? 1u : 0u);
+                    tc_mma_tf32(dcol, ah, bh, id, (sgc > 0 || kk > 0) ? 1u : 0u);
                     tc_mma_tf32(dcol, ah, bl, id, 1u);
                     tc_mma_tf32(dcol, al, bh, id, 1u);
 #endif
                 }
                 tc_commit(empty0 + 8 * s);  // smem stage free once these MMAs complete
                 if (++s == TSTAGES) { s = 0; ph ^= 1; }
-                if (++kc == ke) {
-                    kc = kb;
-                    tc_commit(tfull0 + 8 * abuf);  // accumulator complete
+                ++sgc;
+                const bool sample_end = ++kc == ke;
+                if (sample_end) kc = kb;
+                if (sample_end || sgc == seg) {
+                    sgc = 0;
+                    tc_commit(tfull0 + 8 * abuf);  // accumulator segment complete
                     aph ^= 1u << abuf;
                     abuf ^= 1;
                 }
             }
         }
-    } else {
+        // TMEM is freed once every epilogue warp has read its last accumulator
+        __syncwarp();
+        bar_wait(tdone, 0);
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+    return;  // warps 2, 3: idle
+    }
+    {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(EPI_REGS));
         // --------------------------------------------------- epilogue
-        const int ew = warp - 2;               // 0 .. EPI_WARPS-1
+        const int ew = warp - CTRL_WARPS;      // 0 .. EPI_WARPS-1
         const int q = warp & 3;                // TMEM lane quadrant of this warp
         const int h = ew >> 2;                 // column quarter
         const int row = q * 32 + lane;         // tile row owned by this thread
         constexpr int HC = TBN / (EPI_WARPS / 4);  // columns per epilogue warp
-        float S[HC];
+        float R[HC];
 #pragma unroll
-        for (int i = 0; i < HC; ++i) S[i] = 0.f;
+        for (int i = 0; i < HC; ++i) R[i] = 0.f;
         double sq = 0.0;
         // per-CTA partial tile, column-major ([col][row]): for a fixed column the
         // 32 lanes (rows) of a warp touch 256 contiguous bytes, so a flush is 2 x 64
@@ -712,27 +756,73 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
         double* out = part + (int64_t)g * (TBM * TBN) + (int64_t)(h * HC) * TBM + row;
         int abuf = 0;
         uint32_t aph = 0;  // bit a = phase of accumulator a (no indexed local array)
-        for (int smp = 0; smp < my_samples; ++smp) {
+        // R: the fp32 running sum S over samples when a sample is one TMEM
+        // segment (flushed every FLUSH samples); with several segments per
+        // sample, the sample's Y accumulated over its segments (flushed every
+        // sample)
+        constexpr bool segmented = SEGM;  // R holds the sample's Y, flushed every sample
+        // one 16-column piece of the accumulator in buffer `ab` (|w| applied)
+        auto load = [&](int ab, int ch, float (&y)[16]) {
+#ifdef MLSK_TC_ABL_NOEPI  // ablation: no accumulator reads
+            for (int i = 0; i < 16; ++i) y[i] = (float)i;
+#else
+            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * TBN + h * HC + ch * 16), y);
+#endif
+            if (sh.escale != 1.0f) {  // shared panel: |w| (a power of two, exact)
+#pragma unroll
+                for (int i = 0; i < 16; ++i) y[i] = __fmul_rn(y[i], sh.escale);
+            }
+        };
+        auto wait_full = [&]() {
             bar_wait(tfull0 + 8 * abuf, (aph >> abuf) & 1u);
             tc_fence_after();
+        };
+        auto release = [&]() {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(tempty0 + 8 * abuf);
+            aph ^= 1u << abuf;
+            abuf ^= 1;
+        };
+        for (int smp = 0; smp < my_samples; ++smp) {
             float ssq = 0.f;
             // split sample (one sample per launch): the partial Y of earlier K-segments
             float4* yp = SPLIT ? reinterpret_cast<float4*>(ypart + (int64_t)((kpar ? grp * sh.T : 0) + tile) * (TBM * TBN) +
                                                            (int64_t)row * TBN + h * HC)
                                : nullptr;
+            if (segmented && nseg > 1) {
+                // all but the last segment: R = Y so far (round-to-nearest adds)
+                wait_full();
+#pragma unroll
+                for (int ch = 0; ch < HC / 16; ++ch) {
+                    float y[16];
+                    load(abuf, ch, y);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) R[ch * 16 + i] = y[i];
+                }
+                release();
+                for (int sg = 1; sg + 1 < nseg; ++sg) {
+                    wait_full();
+#pragma unroll
+                    for (int ch = 0; ch < HC / 16; ++ch) {
+                        float y[16];
+                        load(abuf, ch, y);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) R[ch * 16 + i] = __fadd_rn(R[ch * 16 + i], y[i]);
+                    }
+                    release();
+                }
+            }
+            wait_full();  // the sample's last (or only) segment
 #pragma unroll
             for (int ch = 0; ch < HC / 16; ++ch) {
                 float y[16];
-#ifdef MLSK_TC_ABL_NOEPI  // ablation: no accumulator reads
-                for (int i = 0; i < 16; ++i) y[i] = (float)i;
-#else
-                tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(abuf * TBN + h * HC + ch * 16), y);
-#endif
-                if (sh.escale != 1.0f) {  // shared panel: |w| (a power of two, exact)
+                load(abuf, ch, y);
+                if (segmented && nseg > 1) {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) y[i] = __fmul_rn(y[i], sh.escale);
+                    for (int i = 0; i < 16; ++i) y[i] = __fadd_rn(R[ch * 16 + i], y[i]);
                 }
-                if (SPLIT && split_part >= 2) {  // middle / last segment: add the carried partial
+                if (SPLIT && split_part >= 2) {  // middle / last launch: add the carried partial
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
                         const float4 pv = yp[ch * 4 + v];
@@ -742,31 +832,43 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                         y[4 * v + 3] = __fadd_rn(pv.w, y[4 * v + 3]);
                     }
                 }
-                if (SPLIT && split_part <= 2) {  // not the last segment: carry Y on
+                if (SPLIT && split_part <= 2) {  // not the last launch: carry Y on
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) yp[ch * 4 + v] = make_float4(y[4 * v], y[4 * v + 1], y[4 * v + 2], y[4 * v + 3]);
+                    for (int v = 0; v < 4; ++v)
+                        yp[ch * 4 + v] = make_float4(y[4 * v], y[4 * v + 1], y[4 * v + 2], y[4 * v + 3]);
                     continue;
                 }
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     ssq = __fmaf_rn(y[i], y[i], ssq);
 #ifndef MLSK_TC_ABL_NOSUM  // ablation (timing only, wrong sums): no register running sum
-                    S[ch * 16 + i] = __fadd_rn(S[ch * 16 + i], y[i]);
+                    // one segment: R = running sum S; several: R = this sample's Y
+                    R[ch * 16 + i] = segmented ? y[i] : __fadd_rn(R[ch * 16 + i], y[i]);
 #endif
                 }
             }
+            release();
             sq += (double)ssq;
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) bar_arrive(tempty0 + 8 * abuf);
-            aph ^= 1u << abuf;
-            abuf ^= 1;
 #ifdef MLSK_TC_ABL_NOSUM
             if (false) {
 #else
-            if (!(SPLIT && split_part <= 2) && ((smp + 1) % FLUSH == 0 || smp + 1 == my_samples)) {
+            if (!(SPLIT && split_part <= 2) && (segmented || (smp + 1) % FLUSH == 0 || smp + 1 == my_samples)) {
 #endif
-                if (sh.direct) {
+                if (segmented) {
+                    // the sample's Y into this CTA's partial tile (L2-resident;
+                    // one CTA per tile: the first sample stores, and the tile is
+                    // added into the level total after the last sample)
+                    const bool fresh = sh.direct && smp == 0;
+#pragma unroll
+                    for (int i0 = 0; i0 < HC; i0 += 8) {
+                        double ov[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) ov[i] = fresh ? 0.0 : out[(i0 + i) * TBM];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) out[(i0 + i) * TBM] = ov[i] + (double)R[i0 + i];
+                        asm volatile("" ::: "memory");
+                    }
+                } else if (sh.direct) {
                     // (tile-aligned outputs, one CTA per tile) this thread's 64
                     // consecutive columns of the row-major level total, 16 bytes a time
                     double2* o = reinterpret_cast<double2*>(sh.direct + ((int64_t)tm * TBM + row) * sh.cols +
@@ -778,11 +880,11 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                         for (int i = 0; i < 4; ++i) ov[i] = o[i0 + i];
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
-                            ov[i].x += (double)S[2 * (i0 + i)];
-                            ov[i].y += (double)S[2 * (i0 + i) + 1];
+                            ov[i].x += (double)R[2 * (i0 + i)];
+                            ov[i].y += (double)R[2 * (i0 + i) + 1];
                             o[i0 + i] = ov[i];
-                            S[2 * (i0 + i)] = 0.f;
-                            S[2 * (i0 + i) + 1] = 0.f;
+                            R[2 * (i0 + i)] = 0.f;
+                            R[2 * (i0 + i) + 1] = 0.f;
                         }
                         asm volatile("" ::: "memory");  // bound the live doubles: 8 at a time
                     }
@@ -794,27 +896,44 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                         for (int i = 0; i < 8; ++i) ov[i] = out[(i0 + i) * TBM];
 #pragma unroll
                         for (int i = 0; i < 8; ++i) {
-                            out[(i0 + i) * TBM] = ov[i] + (double)S[i0 + i];
-                            S[i0 + i] = 0.f;
+                            out[(i0 + i) * TBM] = ov[i] + (double)R[i0 + i];
+                            R[i0 + i] = 0.f;
                         }
                         asm volatile("" ::: "memory");
                     }
                 }
             }
         }
+        if (segmented && sh.direct && my_samples > 0 && !(SPLIT && split_part <= 2)) {
+            // one CTA per tile: its partial (this thread's own entries) into the level total
+            double2* o = reinterpret_cast<double2*>(sh.direct + ((int64_t)tm * TBM + row) * sh.cols +
+                                                    (int64_t)tn * TBN + h * HC);
+#pragma unroll
+            for (int i0 = 0; i0 < HC / 2; i0 += 4) {
+                double2 ov[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) ov[i] = o[i0 + i];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    ov[i].x += out[(2 * (i0 + i)) * TBM];
+                    ov[i].y += out[(2 * (i0 + i) + 1) * TBM];
+                    o[i0 + i] = ov[i];
+                }
+                asm volatile("" ::: "memory");
+            }
+        }
         sq = warp_sum(sq);
         if (lane == 0) s_sq[ew] = sq;
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (threadIdx.x == 0 && !kpar) {  // kpar: the squares come from k_kpar_combine
-        double t = 0.0;
-        for (int w = 0; w < EPI_WARPS; ++w) t += s_sq[w];
-        part_sq[g] = sh.sym_nb && (tm >> 1) != tn ? 2.0 * t : t;  // a mirrored block counts twice
-    }
-    if (warp == 1) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) bar_arrive(tdone);
+        // the CTA's ||Y||^2: named barrier over the epilogue warps only
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+        if (ew == 0 && lane == 0 && !kpar) {  // kpar: the squares come from k_kpar_combine
+            double t = 0.0;
+            for (int w = 0; w < EPI_WARPS; ++w) t += s_sq[w];
+            part_sq[g] = sh.sym_nb && (tm >> 1) != tn ? 2.0 * t : t;  // a mirrored block counts twice
+        }
     }
 }
 
@@ -942,6 +1061,11 @@ class TcEngine final : public PanelEngine {
         const char* sh_env = std::getenv("MLSK_TC_SHARED");
         shared_env_ = !(sh_env && std::strcmp(sh_env, "0") == 0);
         Gs_ = std::max(1, nsm_ / T_);
+        // TMEM accumulation segment (K-chunks): samples longer than one segment
+        // sum their segments in registers (TcShape::seg).  MLSK_TC_SEG overrides
+        // (0: never segment -- accuracy experiments only)
+        const char* seg_env = std::getenv("MLSK_TC_SEG");
+        seg_ = seg_env ? std::max(0, atoi(seg_env)) : TC_SEG;
         S_.M = M.dm;
         smem_ = TSTAGES * TSTAGE_BYTES + 1024;
         ws_.partial.ensure((size_t)T_ * Gs_ * (TBM * TBN) + (size_t)T_ * Gs_);
@@ -950,17 +1074,25 @@ class TcEngine final : public PanelEngine {
         gen_cap_ = (int64_t)nsm_ * 8;
         rff_smem_ = RFF_SMEM;
         const int smem = smem_, rsmem = rff_smem_;
-        once_per_device((const void*)&k_gemm_tf32x3<false>, [smem, rsmem] {
-            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        once_per_device((const void*)&k_gemm_tf32x3<false, false>, [smem, rsmem] {
+            for (auto f : {k_gemm_tf32x3<false, false>, k_gemm_tf32x3<false, true>, k_gemm_tf32x3<true, false>,
+                           k_gemm_tf32x3<true, true>}) {
+                MLSK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                MLSK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                // setmaxnreg redistributes the launch's registers: the launch must
+                // hold what the warps ask for (else the epilogue's inc never returns)
+                cudaFuncAttributes fa{};
+                MLSK_CUDA(cudaFuncGetAttributes(&fa, f));
+                if (fa.numRegs * TC_THREADS < 32 * (CTRL_WARPS * CTRL_REGS + EPI_WARPS * EPI_REGS))
+                    throw Error(MLSK_ERUNTIME, "tcgen05 GEMM built with " + std::to_string(fa.numRegs) +
+                                                  " registers per thread: too few for its setmaxnreg split");
+            }
             MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_rff, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem));
             // full shared-memory carveout for every kernel of the pipeline, so a
             // generator CTA never leaves an SM configured too small for a GEMM CTA
             MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_tf32<GK_GAUSS>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
             MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_tf32<GK_STUDENT_T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
             MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_tf32<GK_GENERIC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-            MLSK_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         });
     }
     int64_t chunk_cols() const override { return TBK; }
@@ -1020,11 +1152,11 @@ class TcEngine final : public PanelEngine {
         const int64_t w1 = (T_ + nsm_ - 1) / nsm_, w2 = (2 * T_ + nsm_ - 1) / nsm_;
         if (kr.part == 0 && nb == 1 && direct && w2 < 2 * w1 && k >= 16 && !sym_nb_) {
             ws_.ypart.ensure((size_t)2 * T_ * TBM * TBN);
-            TcShape sh{1, k, MP_, PP_, T_, 2, tiles_n_, nullptr, M_.rows, M_.cols, 1, 0, 0, 0, 1.0f};
+            TcShape sh{1, k, MP_, PP_, T_, 2, tiles_n_, nullptr, M_.rows, M_.cols, 1, 0, 0, 0, 1.0f, seg_};
             {
                 Prof p("gemm_tf32x3", s);
-                k_gemm_tf32x3<true><<<2 * T_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq, 1,
-                                                                      ws_.ypart.p);
+                (segmented(k - (k + 1) / 2) ? k_gemm_tf32x3<true, true> : k_gemm_tf32x3<true, false>)
+                    <<<2 * T_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq, 1, ws_.ypart.p);
             }
             {
                 Prof p("reduce_tiles_tc", s);
@@ -1043,15 +1175,15 @@ class TcEngine final : public PanelEngine {
             ypart = ws_.ypart.p;
         }
         TcShape sh{nb,      k,       MP_,     PP_,    T_,     Gs_,        tiles_n_, direct ? st.total() : nullptr,
-                   M_.rows, M_.cols, 0,       sym_nb_, neg_kc, kr.kc0, escale};
+                   M_.rows, M_.cols, 0,       sym_nb_, neg_kc, kr.kc0, escale, seg_};
         {
             Prof p("gemm_tf32x3", s);
             if (kr.part == 0)
-                k_gemm_tf32x3<false><<<T_ * Gs_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq, 0,
-                                                                         nullptr);
+                (segmented(k) ? k_gemm_tf32x3<false, true> : k_gemm_tf32x3<false, false>)
+                    <<<T_ * Gs_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq, 0, nullptr);
             else
-                k_gemm_tf32x3<true><<<T_ * Gs_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq,
-                                                                        kr.part, ypart);
+                (segmented(k) ? k_gemm_tf32x3<true, true> : k_gemm_tf32x3<true, false>)
+                    <<<T_ * Gs_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq, kr.part, ypart);
         }
         if (!finishes) {
             launched();
@@ -1078,6 +1210,8 @@ class TcEngine final : public PanelEngine {
 
    private:
     static int64_t nkc(int64_t c) { return (c + TBK - 1) / TBK; }
+    // a CTA K-range of `k` chunks (at least) runs as several TMEM segments
+    bool segmented(int64_t k) const { return seg_ > 0 && k > seg_; }
     // RFF Gram with the fast generator: the B panel is diag(w) A^T.  When every
     // |w| is the same power of two and the coarse prefix is whole K-chunks, the
     // GEMM reads B from the A panel (negated prefix chunks, Y scaled by |w|):
@@ -1103,6 +1237,7 @@ class TcEngine final : public PanelEngine {
     TcModel S_{};
     int nsm_, T_, Gs_, tiles_n_, smem_, rff_smem_;
     int sym_nb_ = 0;  // symmetric output: 256-blocks per side (0 = full tile grid)
+    int seg_ = TC_SEG;
     bool shared_env_ = true;
     int64_t gen_cap_;
     int64_t MP_, PP_;

@@ -23,7 +23,10 @@ all-reduce of the packed per-level buffer [(sum Y, sum ||Y||^2, count)] per
 round -- NCCL on the device buffer when the process group's backend is NCCL,
 gloo on a host copy otherwise.  Every rank then holds the same global
 statistics and computes the same next allocation; there is no other
-communication.
+communication.  Matrix sums then differ across world sizes by reassociation
+(ulp level); `ShardedSession` (fixed virtual shards, one all-gather and a
+vshard-ordered sum per round) makes results bit-identical for any world
+size dividing its shard count.
 """
 from __future__ import annotations
 
@@ -90,10 +93,89 @@ def unpack(buf: np.ndarray, levels: int) -> LevelStats:
     return LevelStats(b[:, :cells].copy(), b[:, cells].copy(), np.rint(b[:, cells + 1]).astype(np.int64))
 
 
-def allreduce_stats(session, levels: int, group=None) -> LevelStats:
-    """One all-reduce of the packed level buffer across the process group."""
+class ShardedSession:
+    """Deterministic multi-GPU split: the samples are dealt to `vshards`
+    VIRTUAL shards (64-replication chunk q -> virtual shard q mod vshards, the
+    library's rank/world sharding with world = vshards), and rank r of `world`
+    (world dividing vshards) runs the virtual shards v = r (mod world), each in
+    its own session.  Every virtual shard's sums then do not depend on how many
+    GPUs run them, and `gather_ordered_stats` adds the vshards' buffers in
+    vshard order -- so the statistics, and every decision taken from them, are
+    bit-identical for world = 1, 2, 4, 8 (the reference's thread-count
+    invariance, README.md:109-119, test_estimators.cpp:162-186, which a plain
+    all-reduce of per-rank sums cannot give: its grouping depends on world).
+
+    `make_session(v, vshards)` builds the session of virtual shard v (an
+    MlmcSession with EstimatorOptions(rank=v, world=vshards), or any object
+    with run_round / packed_stats / cells)."""
+
+    def __init__(self, make_session, rank: int = 0, world: int = 1, vshards: int = 8):
+        if world < 1 or vshards % world != 0 or not 0 <= rank < world:
+            raise ValueError("ShardedSession: world must divide vshards and 0 <= rank < world")
+        self.rank, self.world, self.vshards = rank, world, vshards
+        self.owned = list(range(rank, vshards, world))
+        self.sessions = [make_session(v, vshards) for v in self.owned]
+        self.cells = self.sessions[0].cells
+
+    def run_round(self, dN: Sequence[int]) -> None:
+        for s in self.sessions:
+            s.run_round(dN)
+
+    def packed_parts(self) -> List[np.ndarray]:
+        """This rank's virtual shards' packed buffers, in self.owned order."""
+        return [np.asarray(s.packed_stats(), dtype=np.float64) for s in self.sessions]
+
+    def close(self) -> None:
+        for s in self.sessions:
+            if hasattr(s, "close"):
+                s.close()
+
+
+def ordered_sum(parts: Sequence[np.ndarray]) -> np.ndarray:
+    """sum of the virtual shards' buffers, strictly in vshard order from 0.0"""
+    total = np.zeros_like(parts[0])
+    for p in parts:
+        total = total + p
+    return total
+
+
+def gather_ordered_stats(session: ShardedSession, levels: int, group=None) -> LevelStats:
+    """All ranks' virtual-shard buffers (one all-gather), added in vshard
+    order on every rank: the same bits for any world size."""
     import torch.distributed as dist
 
+    mine = session.packed_parts()
+    if group is None and not (dist.is_available() and dist.is_initialized()):
+        if session.world != 1:
+            raise RuntimeError("gather_ordered_stats: world > 1 needs an initialised process group")
+        return unpack(ordered_sum(mine), levels)
+    import torch
+
+    world = dist.get_world_size(group)
+    if world != session.world:
+        raise ValueError("gather_ordered_stats: process group size != session world")
+    n = mine[0].size
+    local = torch.from_numpy(np.concatenate(mine))
+    on_dev = dist.get_backend(group) == "nccl"
+    if on_dev:
+        local = local.cuda()
+    bufs = [torch.empty_like(local) for _ in range(world)]
+    dist.all_gather(bufs, local, group=group)
+    per_v = [None] * session.vshards
+    for r, b in enumerate(bufs):
+        b = b.cpu().numpy()
+        for j, v in enumerate(range(r, session.vshards, world)):
+            per_v[v] = b[j * n:(j + 1) * n]
+    return unpack(ordered_sum(per_v), levels)
+
+
+def allreduce_stats(session, levels: int, group=None) -> LevelStats:
+    """One all-reduce of the packed level buffer across the process group
+    (a ShardedSession: the fixed-order all-gather reduction instead)."""
+    import torch.distributed as dist
+
+    if isinstance(session, ShardedSession):
+        return gather_ordered_stats(session, levels, group)
     if group is None and not (dist.is_available() and dist.is_initialized()):
         return unpack(session.packed_stats(), levels)
     backend = dist.get_backend(group)
@@ -143,7 +225,8 @@ def adaptive_mlmc(session, M: int, c0: int, L: int, eps: float, n_pilot: int = 2
     packed_stats / cells) until sum_l V_l / N_l <= theta eps^2.
 
     `session` must be created with rank / world matching the process group:
-    each rank then runs its chunk share of every round's dN.
+    each rank then runs its chunk share of every round's dN.  A
+    ShardedSession makes the whole run bit-identical across world sizes.
     """
     levels = L + 1
     cells = session.cells

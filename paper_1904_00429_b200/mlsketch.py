@@ -295,11 +295,23 @@ class EstimatorOptions:
     rank: int = 0
     world: int = 1
     stream: Optional[int] = None
+    # multi-GPU inside the library (mlsk_exec_opts.n_devices / device_ids):
+    # one host thread per device slot, slot sums added in slot order
+    devices: Optional[Sequence[int]] = None
+    # fixed virtual shards: bit-identical results for any device count dividing vshards
+    deterministic: bool = False
+    vshards: int = 8
 
     def _c(self, probe_buf=None, probe_k=0):
         eng = {"auto": abi.ENGINE_AUTO, "exact": abi.ENGINE_EXACT, "fused": abi.ENGINE_FUSED}[self.engine]
+        ids = None
+        if self.devices is not None:
+            self._ids = np.ascontiguousarray(self.devices, dtype=np.int32)  # kept alive with the options
+            ids = self._ids.ctypes.data_as(C.POINTER(C.c_int32))
         return abi.ExecOpts(self.device, eng, self.stream, self.rank, self.world, probe_k,
-                            _ptr(probe_buf, _u32p) if probe_buf is not None else None)
+                            _ptr(probe_buf, _u32p) if probe_buf is not None else None,
+                            len(self.devices) if self.devices is not None else 0, ids,
+                            1 if self.deterministic else 0, self.vshards)
 
 
 class LevelStatistic:

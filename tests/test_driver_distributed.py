@@ -89,6 +89,56 @@ def test_adaptive_driver_two_ranks_matches_single_process():
     assert abs(r0[3] - single.rmse_estimate) <= 1e-12 * single.rmse_estimate
 
 
+def _det_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sess = driver.ShardedSession(lambda v, V: OracleSession(2, 4, 3, 99, v, V), rank, world, vshards=4)
+        r = driver.adaptive_mlmc(sess, 2, 4, 3, eps=0.5, n_pilot=96, max_rounds=6)
+        out[rank] = (r.value.tobytes(), r.stats.sums.tobytes(), r.stats.sumsq.tobytes(), r.N, r.history)
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_ranks(target, world):
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as mgr:
+        out = mgr.dict()
+        port = _free_port()
+        procs = [ctx.Process(target=target, args=(r, world, port, out)) for r in range(world)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(120)
+            assert p.exitcode == 0
+        return [out[r] for r in range(world)]
+
+
+def test_deterministic_sharding_bit_identical_across_world_sizes():
+    """ShardedSession (fixed virtual shards, all-gather + vshard-ordered sum):
+    the world-2 run (gloo) reproduces the single-process run bit for bit --
+    every level sum, the estimate and the adaptive decisions."""
+    one = driver.ShardedSession(lambda v, V: OracleSession(2, 4, 3, 99, v, V), 0, 1, vshards=4)
+    single = driver.adaptive_mlmc(one, 2, 4, 3, eps=0.5, n_pilot=96, max_rounds=6)
+    r0, r1 = _run_ranks(_det_worker, 2)
+    assert r0 == r1
+    assert r0[0] == single.value.tobytes() and r0[1] == single.stats.sums.tobytes()
+    assert r0[2] == single.stats.sumsq.tobytes()
+    assert r0[3] == single.N and r0[4] == single.history
+    # and the virtual shards partition the plain run's samples
+    plain = driver.adaptive_mlmc(OracleSession(2, 4, 3, 99), 2, 4, 3, eps=0.5, n_pilot=96, max_rounds=6)
+    assert plain.N == single.N
+    np.testing.assert_allclose(plain.value, single.value, rtol=1e-12, atol=1e-12)
+
+
+def test_sharded_session_rejects_bad_split():
+    with pytest.raises(ValueError):
+        driver.ShardedSession(lambda v, V: OracleSession(2, 4, 3, 99, v, V), 0, 3, vshards=8)
+    with pytest.raises(ValueError):
+        driver.ShardedSession(lambda v, V: OracleSession(2, 4, 3, 99, v, V), 2, 2, vshards=8)
+
+
 def test_optimal_allocation_and_costs():
     C = driver.level_costs(2, 32, 2, 4)
     assert C == [32 * 4.0, (64 + 32) * 4.0, (128 + 64) * 4.0]

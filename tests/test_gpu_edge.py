@@ -94,12 +94,13 @@ def test_bad_device_and_engine_rejected(gpu):
     from paper_1904_00429_b200._lib import MlskRuntimeError
     with pytest.raises((ValueError, MlskRuntimeError)):
         gpu.mlmc_matmul(model, gpu.target_identity(), plan, 1, gpu.EstimatorOptions(device=4096))
-    # the fused engine needs the philox stream and an identity target
+    # the fused engine needs the philox stream; on the fp32 (tcgen05) engine an identity target
     with pytest.raises(ValueError):
         gpu.mlmc_matmul(gpu.paper_matrix_model(), gpu.target_identity(), plan, 1,
                         gpu.EstimatorOptions(engine="fused"))
+    m32 = gpu.gaussian_mean_matrix_model(8, 64, 8, sd=1.0, data_seed=1, dtype=1)
     with pytest.raises(ValueError):
-        gpu.mlmc_matmul(model, gpu.target_f2(), plan, 1, gpu.EstimatorOptions(engine="fused"))
+        gpu.mlmc_matmul(m32, gpu.target_f2(), plan, 1, gpu.EstimatorOptions(engine="fused"))
 
 
 def test_large_level0_count(gpu):

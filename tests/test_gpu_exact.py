@@ -48,13 +48,31 @@ def test_config1_ref_stream_indices_bitexact(gpu, oracle):
         i_g, a_g, b_g = gpu.draw_sample(model, MASTER, tag, k, c)
         i_o, a_o, b_o = om.draw(MASTER, tag, k, c)
         assert np.array_equal(i_g, i_o)
-        # CUDA log/sin/cos vs glibc: a few ulp
-        np.testing.assert_allclose(a_g, a_o, rtol=4e-15, atol=4e-15)
-        np.testing.assert_allclose(b_g, b_o, rtol=4e-15, atol=4e-15)
+        # glibc's log / sin / cos restated on the device (mlsk_libm.cuh): bit for bit
+        assert np.array_equal(a_g, a_o) and np.array_equal(b_g, b_o)
     plan = gpu.LevelPlan(2, 3, [100, 64, 40, 10], c0=8)
     r = gpu.mlmc_inner(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="exact"))
     o = om.mlmc(2, 8, list(plan.N), MASTER)
-    _levels_equal(r, o, exact=False, rtol=1e-12)
+    _levels_equal(r, o)
+
+
+def test_ref_stream_normals_bitexact_at_scale(gpu, oracle):
+    """Reference-stream Box-Muller normals (rng.hpp:55-65: sqrt(-2 log u),
+    2 pi u', cos / sin) for ~2 M draws of a config-2-shaped model: every value
+    identical to the oracle's glibc-computed one (the fraction of differing
+    values and the largest ulp distance are reported on failure)."""
+    model = gpu.gaussian_mean_matrix_model(256, 4096, 256, sd=0.5, data_seed=5, stream="ref")
+    om = _oracle_model(oracle, model)
+    bad, total, worst = 0, 0, 0
+    for k in range(2):
+        _, a_g, b_g = gpu.draw_sample(model, MASTER, 3, k, 4096)
+        _, a_o, b_o = om.draw(MASTER, 3, k, 4096)
+        for g_, o_ in ((a_g, a_o), (b_g, b_o)):
+            d = g_.view(np.int64) - o_.view(np.int64)
+            bad += int(np.count_nonzero(d))
+            total += d.size
+            worst = max(worst, int(np.max(np.abs(d))))
+    assert bad == 0, f"{bad} of {total} draws differ, max {worst} ulp"
 
 
 @pytest.mark.parametrize("kind", ["constant", "deterministic"])
@@ -81,13 +99,21 @@ def test_config2_small_philox_bitexact(gpu, oracle):
 
 
 def test_paper_models_ref_stream(gpu, oracle):
+    """Paper models (models.cpp:12-52: Box-Muller, Poisson, Exp(1), cos, sin)
+    with the identity, f1 and f2 targets (f2's sin included): bit for bit."""
     plan = gpu.LevelPlan(3, 2, [300, 100, 33])
     for tgt in (gpu.target_identity(), gpu.target_f1(), gpu.target_f2()):
         r = gpu.mlmc_inner(gpu.paper_inner_model(), tgt, plan, 314, gpu.EstimatorOptions(engine="exact"))
         o = _oracle_model(oracle, gpu.paper_inner_model()).mlmc(3, 1, [300, 100, 33], 314, target=tgt.kind)
-        _levels_equal(r, o, exact=False, rtol=1e-11)
+        _levels_equal(r, o)
     m = gpu.paper_matrix_model()
-    r = gpu.mlmc_matmul(m, gpu.target_f2(), gpu.LevelPlan(4, 1, [40, 10]), 11,
-                        gpu.EstimatorOptions(engine="exact"))
-    o = _oracle_model(oracle, m).mlmc(4, 1, [40, 10], 11, target=abi.TARGET_F2)
-    _levels_equal(r, o, exact=False, rtol=1e-11)
+    for tgt in (gpu.target_identity(), gpu.target_f1(), gpu.target_f2()):
+        r = gpu.mlmc_matmul(m, tgt, gpu.LevelPlan(4, 1, [40, 10]), 11, gpu.EstimatorOptions(engine="exact"))
+        o = _oracle_model(oracle, m).mlmc(4, 1, [40, 10], 11, target=tgt.kind)
+        _levels_equal(r, o)
+    for kind in (abi.MODEL_PAPER_INNER, abi.MODEL_PAPER_MATRIX):
+        mod = gpu.paper_inner_model() if kind == abi.MODEL_PAPER_INNER else m
+        for k in range(3):
+            i_g, a_g, b_g = gpu.draw_sample(mod, 99, 2, k, 64)
+            i_o, a_o, b_o = _oracle_model(oracle, mod).draw(99, 2, k, 64)
+            assert np.array_equal(i_g, i_o) and np.array_equal(a_g, a_o) and np.array_equal(b_g, b_o)
