@@ -698,31 +698,43 @@ __global__ void k_reduce_inner(const double* __restrict__ y, int nb, double* tot
 }
 
 // All levels of a round in one launch (config 1 is launch-bound: c = 8 .. 256).
-// A part = one level's slice of the round; 8 threads per replication, lanes
-// over index pairs, reduced within the 8-lane group.
+// A part = one level's slice of the round.  A warp task is 32 / g
+// replications of one part, g = the part's threads per replication (up to
+// INNER_G, no more than its index pairs: level 0 of config 1 has c = 8, i.e. 4
+// pairs, and 8 threads left half of them idle), lanes over index pairs,
+// reduced within the g-lane group.
 constexpr int INNER_MAX_PARTS = 16;
 constexpr int INNER_G = 8;
 struct InnerPart {
     uint64_t tag;
     int64_t c, cc;
     double w_fine, w_coarse;  // nonlinear targets: both n / c (prefix and suffix kept apart)
-    int64_t ks_off;  // into the round's replication list
-    int64_t y_off;   // first output slot (parts are contiguous)
+    int64_t ks_off;    // into the round's replication list
+    int64_t y_off;     // first output slot (parts are contiguous)
     int64_t nb;
+    int64_t task_off;  // first warp task
+    int g;             // threads per replication (power of two <= INNER_G)
     double* total;
     double* total_sq;
 };
 struct InnerParts {
     int n;
+    int64_t tasks;
     InnerPart p[INNER_MAX_PARTS];
 };
+
+inline int inner_group(int64_t c) {
+    int g = 1;
+    while (g < INNER_G && 2 * g < c) g *= 2;  // g <= ceil(c / 2) index pairs
+    return g;
+}
 
 // NL (nonlinear target f1 / f2, models.cpp:99-117): the prefix and suffix
 // sums are kept apart, Y = f((n/c)(S_pre + S_suf)) - f((n/cc) S_pre) per
 // replication (estimators.cpp:78-80), instead of one signed sum.
 template <bool NL>
 __global__ void __launch_bounds__(256)
-k_fused_inner_multi(DevModel M, uint64_t seed, const int64_t* __restrict__ ks, InnerParts P, int64_t total,
+k_fused_inner_multi(DevModel M, uint64_t seed, const int64_t* __restrict__ ks, InnerParts P,
                     double* __restrict__ y_out, int target, double tparam) {
     __shared__ __align__(16) double2 s_sc[256];
     __shared__ __align__(16) double2 s_lg[128];
@@ -731,23 +743,19 @@ k_fused_inner_multi(DevModel M, uint64_t seed, const int64_t* __restrict__ ks, I
     Tables T = M.tab;
     T.sincos_d = reinterpret_cast<const double*>(s_sc);
     T.log_d = reinterpret_cast<const double*>(s_lg);
-    const int gl = threadIdx.x & (INNER_G - 1);
-    const int64_t groups = ((int64_t)gridDim.x * blockDim.x) / INNER_G;
-    // the whole warp iterates together (uniform trip count for the shuffles):
-    // base = its first group, lane / INNER_G selects the group
-    const int64_t warp_first = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / INNER_G;
-    for (int64_t base = warp_first; base < total; base += groups) {
-        const int64_t sidx = base + (threadIdx.x & 31) / INNER_G;
-        const bool live = sidx < total;
-        int pi = 0;
-        if (live)
-            while (pi + 1 < P.n && sidx >= P.p[pi + 1].y_off) ++pi;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t task = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < P.tasks; task += warps) {
+        int pi = 0;  // warp-uniform
+        while (pi + 1 < P.n && task >= P.p[pi + 1].task_off) ++pi;
         const InnerPart& q = P.p[pi];
+        const int g = q.g, gl = lane & (g - 1);
+        const int64_t b = (task - q.task_off) * (32 / g) + lane / g;
+        const bool live = b < q.nb;
         double acc = 0.0, pre = 0.0;
         if (live) {
-            const int64_t b = sidx - q.y_off;
             const uint64_t key = derive_seed(seed, q.tag, (uint64_t)ks[q.ks_off + b]);
-            for (int64_t tp = gl; 2 * tp < q.c; tp += INNER_G) {
+            for (int64_t tp = gl; 2 * tp < q.c; tp += g) {
                 const u32x4 ri = philox((uint32_t)tp, 0, 0, MLSK_CTR_INDEX, key);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -765,11 +773,9 @@ k_fused_inner_multi(DevModel M, uint64_t seed, const int64_t* __restrict__ ks, I
                 }
             }
         }
-#pragma unroll
-        for (int o = INNER_G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        for (int o = g / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (NL) {
-#pragma unroll
-            for (int o = INNER_G / 2; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+            for (int o = g / 2; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
             if (live && gl == 0) {
                 // fine = (n/c)(S_pre + S_suf), coarse = (n/cc) S_pre = (c/cc) (n/c) S_pre
                 double y = apply_target(target, tparam, __dadd_rn(pre, acc));
@@ -778,16 +784,25 @@ k_fused_inner_multi(DevModel M, uint64_t seed, const int64_t* __restrict__ ks, I
                 acc = y;
             }
         }
-        if (live && gl == 0) y_out[sidx] = acc;
+        if (live && gl == 0) y_out[q.y_off + b] = acc;
     }
 }
 
-// one block per part: total += sum y, total_sq += sum y^2 (fixed order)
-__global__ void k_reduce_inner_multi(const double* __restrict__ y, InnerParts P) {
+// INNER_RB blocks per part, each over a fixed contiguous range of the part's
+// replications; the last block of a part to finish adds the INNER_RB partials
+// in block order (fixed order: bit-identical reruns).  One block per part
+// (the previous form) serialised 0.5 M replications of level 0 on one SM.
+constexpr int INNER_RB = 64;
+__global__ void __launch_bounds__(256)
+k_reduce_inner_multi(const double* __restrict__ y, InnerParts P, double* __restrict__ part,
+                     unsigned* __restrict__ done) {
     __shared__ double s1[256], s2[256];
-    const InnerPart& q = P.p[blockIdx.x];
+    __shared__ bool last;
+    const int pi = blockIdx.y;
+    const InnerPart& q = P.p[pi];
+    const int64_t b0 = q.nb * blockIdx.x / INNER_RB, b1 = q.nb * (blockIdx.x + 1) / INNER_RB;
     double a = 0.0, r = 0.0;
-    for (int64_t b = threadIdx.x; b < q.nb; b += blockDim.x) {
+    for (int64_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
         const double v = y[q.y_off + b];
         a += v;
         r = __fma_rn(v, v, r);
@@ -803,8 +818,23 @@ __global__ void k_reduce_inner_multi(const double* __restrict__ y, InnerParts P)
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        *q.total += s1[0];
-        *q.total_sq += s2[0];
+        part[(pi * INNER_RB + blockIdx.x) * 2] = s1[0];
+        part[(pi * INNER_RB + blockIdx.x) * 2 + 1] = s2[0];
+        __threadfence();
+        last = atomicAdd(&done[pi], 1u) == INNER_RB - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        const volatile double* vp = part + pi * INNER_RB * 2;
+        double t = 0.0, t2 = 0.0;
+        for (int k = 0; k < INNER_RB; ++k) {
+            t += vp[2 * k];
+            t2 += vp[2 * k + 1];
+        }
+        *q.total += t;
+        *q.total_sq += t2;
+        done[pi] = 0;  // ready for the next launch (stream-ordered)
     }
 }
 
@@ -965,6 +995,22 @@ std::unique_ptr<PanelEngine> make_f64_engine(const Model& M, Workspace& ws, int 
     return std::unique_ptr<PanelEngine>(new F64Engine(M, ws, target, tparam));
 }
 
+// ks[dst + i] = k0 + i for i < count, runs sorted by dst and covering [0, total)
+struct KsRun {
+    int64_t k0, count, dst;
+};
+__global__ void k_expand_ks(const KsRun* __restrict__ runs, int nruns, int64_t total, int64_t* __restrict__ ks) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nruns - 1;  // last run with dst <= e
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (runs[mid].dst <= e) lo = mid;
+            else hi = mid - 1;
+        }
+        ks[e] = runs[lo].k0 + (e - runs[lo].dst);
+    }
+}
+
 constexpr int NBUF = 3;  // panel buffers in flight (gen i+1, i+2 while GEMM i)
 
 // Engine-private pipeline state kept in the Workspace across rounds.
@@ -975,11 +1021,21 @@ struct Pipe {
     bool used[NBUF] = {};
     DevArray<double> panels[NBUF];
     DevArray<uint32_t> idx[NBUF];
-    DevArray<int64_t> ks;      // all replication indices of the round
-    int64_t* ks_host = nullptr;  // pinned staging
-    size_t ks_cap = 0;
+    DevArray<int64_t> ks;      // all replication indices of the round (expanded on the device)
+    DevArray<KsRun> runs;      // the round's replication runs
+    KsRun* runs_host = nullptr;  // pinned staging
+    size_t runs_cap = 0;
     DevArray<double> part;
+    DevArray<double> red_part;    // k_reduce_inner_multi: per-block partials
+    DevArray<unsigned> red_done;  // per-part finished-block counters (self-resetting)
     bool staged_pending = false;
+
+    void ensure_inner_red() {
+        if (red_done.p) return;
+        red_part.ensure((size_t)INNER_MAX_PARTS * INNER_RB * 2);
+        red_done.ensure(INNER_MAX_PARTS);
+        MLSK_CUDA(cudaMemsetAsync(red_done.p, 0, INNER_MAX_PARTS * sizeof(unsigned), s_gen));
+    }
 
     Pipe() {
         int lo = 0, hi = 0;
@@ -1004,22 +1060,30 @@ struct Pipe {
         cudaEventDestroy(start);
         cudaEventDestroy(end);
         cudaEventDestroy(staged);
-        if (ks_host) cudaFreeHost(ks_host);
+        if (runs_host) cudaFreeHost(runs_host);
         if (s_gen) cudaStreamDestroy(s_gen);
         if (s_mm) cudaStreamDestroy(s_mm);
     }
-    void stage_ks(const std::vector<int64_t>& h, cudaStream_t s) {
+    // Replication lists go to the device as runs of consecutive k (one run per
+    // level at world = 1, one per owned 64-chunk when sharded) and are expanded
+    // there: a config-1 round of 1 M level-samples otherwise spent ~4 ms of host
+    // time building and copying 8 MB of indices per step.
+    void stage_ks(const std::vector<KsRun>& h, int64_t total, cudaStream_t s) {
         if (staged_pending) MLSK_CUDA(cudaEventSynchronize(staged));  // previous round's copy done
-        if (h.size() > ks_cap) {
-            if (ks_host) cudaFreeHost(ks_host);
-            ks_cap = std::max<size_t>(h.size(), 1 << 16);
-            MLSK_CUDA(cudaMallocHost(&ks_host, ks_cap * sizeof(int64_t)));
+        if (h.size() > runs_cap) {
+            if (runs_host) cudaFreeHost(runs_host);
+            runs_cap = std::max<size_t>(h.size(), 1 << 10);
+            MLSK_CUDA(cudaMallocHost(&runs_host, runs_cap * sizeof(KsRun)));
         }
-        std::memcpy(ks_host, h.data(), h.size() * sizeof(int64_t));
-        ks.ensure(h.size());
-        MLSK_CUDA(cudaMemcpyAsync(ks.p, ks_host, h.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        std::memcpy(runs_host, h.data(), h.size() * sizeof(KsRun));
+        runs.ensure(h.size());
+        ks.ensure((size_t)total);
+        MLSK_CUDA(cudaMemcpyAsync(runs.p, runs_host, h.size() * sizeof(KsRun), cudaMemcpyHostToDevice, s));
         MLSK_CUDA(cudaEventRecord(staged, s));
         staged_pending = true;
+        const int64_t grid = std::min<int64_t>((total + 255) / 256, 4096);
+        k_expand_ks<<<(int)grid, 256, 0, s>>>(runs.p, (int)h.size(), total, ks.p);
+        launched();
     }
 };
 
@@ -1057,24 +1121,36 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
     // nonlinear target: fine and coarse kept apart (uniform weights n / c)
     const bool nl = a.target != MLSK_TARGET_IDENTITY;
 
-    // replication lists of all jobs, staged to the device once per round
-    std::vector<std::vector<int64_t>> jks(jobs.size());
-    std::vector<int64_t> all;
-    std::vector<int64_t> job_off(jobs.size());
+    // replication lists of all jobs as runs of consecutive k, expanded on the
+    // device once per round (job j's list starts at job_off[j])
+    std::vector<KsRun> runs;
+    std::vector<int64_t> job_off(jobs.size()), job_cnt(jobs.size(), 0);
+    int64_t all = 0;
     for (size_t j = 0; j < jobs.size(); ++j) {
-        for (const auto& sg : jobs[j].segs)
-            for (int64_t k = 0; k < sg.count; ++k) jks[j].push_back(sg.k0 + k);
-        job_off[j] = (int64_t)all.size();
-        all.insert(all.end(), jks[j].begin(), jks[j].end());
+        job_off[j] = all;
+        for (const auto& sg : jobs[j].segs) {
+            if (sg.count <= 0) continue;
+            if (!runs.empty() && job_cnt[j] > 0 && runs.back().k0 + runs.back().count == sg.k0)
+                runs.back().count += sg.count;
+            else
+                runs.push_back({sg.k0, sg.count, all});
+            all += sg.count;
+            job_cnt[j] += sg.count;
+        }
     }
-    if (all.empty()) return;
+    if (all == 0) return;
+    bool any_probe = false;
+    for (const auto& job : jobs) any_probe = any_probe || job.probe_host;
+    // host copies of the lists only for the coupling probe (which k is < probe_k)
+    std::vector<std::vector<int64_t>> jks(any_probe ? jobs.size() : 0);
+    if (any_probe)
+        for (size_t j = 0; j < jobs.size(); ++j)
+            for (const auto& sg : jobs[j].segs)
+                for (int64_t k = 0; k < sg.count; ++k) jks[j].push_back(sg.k0 + k);
     MLSK_CUDA(cudaEventRecord(P.start, a.stream));
     MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.start, 0));
     MLSK_CUDA(cudaStreamWaitEvent(P.s_mm, P.start, 0));
-    P.stage_ks(all, P.s_gen);
-
-    bool any_probe = false;
-    for (const auto& job : jobs) any_probe = any_probe || job.probe_host;
+    P.stage_ks(runs, all, P.s_gen);
     if (M.vector && !any_probe) {
         // config-1 shape: every level of the round in one launch (+ one reduction
         // launch), in slices of at most 4M replications / INNER_MAX_PARTS parts
@@ -1084,19 +1160,21 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         auto flush = [&]() {
             if (parts.n == 0) return;
             ws.v.ensure((size_t)filled);
-            const int64_t grid = std::min<int64_t>((filled * INNER_G + 255) / 256, (int64_t)sms * 16);
+            const int64_t grid = std::min<int64_t>((parts.tasks * 32 + 255) / 256, (int64_t)sms * 16);
             {
                 Prof p("fused_inner_f64", P.s_gen);
                 if (nl)
                     k_fused_inner_multi<true><<<(int)std::max<int64_t>(grid, 1), 256, 0, P.s_gen>>>(
-                        M.dm, a.seed, P.ks.p, parts, filled, ws.v.p, a.target, a.target_param);
+                        M.dm, a.seed, P.ks.p, parts, ws.v.p, a.target, a.target_param);
                 else
                     k_fused_inner_multi<false><<<(int)std::max<int64_t>(grid, 1), 256, 0, P.s_gen>>>(
-                        M.dm, a.seed, P.ks.p, parts, filled, ws.v.p, a.target, a.target_param);
+                        M.dm, a.seed, P.ks.p, parts, ws.v.p, a.target, a.target_param);
             }
             {
                 Prof p("reduce_inner", P.s_gen);
-                k_reduce_inner_multi<<<parts.n, 256, 0, P.s_gen>>>(ws.v.p, parts);
+                P.ensure_inner_red();
+                k_reduce_inner_multi<<<dim3(INNER_RB, parts.n), 256, 0, P.s_gen>>>(ws.v.p, parts, P.red_part.p,
+                                                                                   P.red_done.p);
             }
             launched(2);
             parts = InnerParts{};
@@ -1114,12 +1192,15 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
             const int64_t c = job.lv.c, cc = job.lv.cc;
             const double w_fine = n / (double)c;
             const double w_coarse = cc > 0 && !nl ? w_fine - n / (double)cc : w_fine;
-            const int64_t total = (int64_t)jks[j].size();
+            const int64_t total = job_cnt[j];
             for (int64_t off = 0; off < total;) {
                 if (parts.n == INNER_MAX_PARTS || filled == max_slice) flush();
                 const int64_t take = std::min(total - off, max_slice - filled);
-                parts.p[parts.n++] = InnerPart{job.lv.tag, c, cc, w_fine, w_coarse, job_off[j] + off, filled, take,
-                                               job.st->total(), job.st->total_sq()};
+                const int g = inner_group(c);
+                parts.p[parts.n++] = InnerPart{job.lv.tag, c,        cc,          w_fine, w_coarse, job_off[j] + off,
+                                               filled,     take,     parts.tasks, g,      job.st->total(),
+                                               job.st->total_sq()};
+                parts.tasks += (take * g + 31) / 32;
                 filled += take;
                 off += take;
             }
@@ -1137,7 +1218,7 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
             const int64_t c = job.lv.c, cc = job.lv.cc;
             const double w_fine = n / (double)c;
             const double w_coarse = cc > 0 && !nl ? w_fine - n / (double)cc : w_fine;
-            const int64_t total = (int64_t)jks[j].size();
+            const int64_t total = job_cnt[j];
             const int64_t max_batch = 1 << 20;
             for (int64_t off = 0; off < total; off += max_batch) {
                 const int nb = (int)std::min<int64_t>(max_batch, total - off);
@@ -1194,7 +1275,7 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
     int64_t max_panel = 0;
     for (size_t j = 0; j < jobs.size(); ++j) {
         const int64_t per = E.panel_bytes(jobs[j].lv.c, jobs[j].lv.cc);
-        const int64_t total = (int64_t)jks[j].size();
+        const int64_t total = job_cnt[j];
         if (per > split_limit && E.splits_k()) {
             if (nl)
                 throw Error(MLSK_EINVAL, "fused engine: nonlinear targets need a level-sample's panels within one "
