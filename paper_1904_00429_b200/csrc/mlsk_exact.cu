@@ -284,7 +284,7 @@ void exact_run(const RunArgs& a, const LevelSpec& lv, const std::vector<Segment>
     // uniform inv_probs = n (sampling.cpp:39), scaled by 1/s (sketch.cpp:37,73);
     // the full draw is the plain product: exact_inner / exact_matmul
     // (tensor.cpp:97-131) -- (a*b)*1 and o*1 are exact, so the same kernel serves
-    const double w = lv.full ? 1.0 : (double)M.desc.n;
+    const double w = lv.full ? 1.0 : (double)M.desc.n * kRescalePerturb;  // (1 unless the negative control)
     const double vdiv = lv.full ? 1.0 : (double)c;
     const double sf = lv.full ? 1.0 : 1.0 / (double)c;
     const double sc = lv.cc > 0 ? 1.0 / (double)lv.cc : 0.0;

@@ -1190,7 +1190,7 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         for (size_t j : order) {
             FusedJob& job = jobs[j];
             const int64_t c = job.lv.c, cc = job.lv.cc;
-            const double w_fine = n / (double)c;
+            const double w_fine = n / (double)c * kRescalePerturb;
             const double w_coarse = cc > 0 && !nl ? w_fine - n / (double)cc : w_fine;
             const int64_t total = job_cnt[j];
             for (int64_t off = 0; off < total;) {
@@ -1216,7 +1216,7 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         for (size_t j = 0; j < jobs.size(); ++j) {
             FusedJob& job = jobs[j];
             const int64_t c = job.lv.c, cc = job.lv.cc;
-            const double w_fine = n / (double)c;
+            const double w_fine = n / (double)c * kRescalePerturb;
             const double w_coarse = cc > 0 && !nl ? w_fine - n / (double)cc : w_fine;
             const int64_t total = job_cnt[j];
             const int64_t max_batch = 1 << 20;
@@ -1328,7 +1328,7 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         const Batch& bt = batches[i];
         FusedJob& job = jobs[bt.job];
         const int64_t c = job.lv.c, cc = job.lv.cc;
-        const double w_fine = n / (double)c;                                        // n/c
+        const double w_fine = n / (double)c * kRescalePerturb;                                        // n/c
         const double w_coarse = cc > 0 && !nl ? w_fine - n / (double)cc : w_fine;  // n/c - n/cc on the prefix
         const int buf = (int)(i % NBUF);
         void* panels = P.panels[buf].p;

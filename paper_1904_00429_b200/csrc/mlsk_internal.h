@@ -25,6 +25,16 @@ struct Error : std::runtime_error {
 
 [[noreturn]] inline void invalid(const std::string& m) { throw Error(MLSK_EINVAL, m); }
 
+// Negative control of the parity harness (the reference's `oracle
+// --inject-rescale-bug`, mlsketch_main.cpp:219-221, perturbs the rescale by
+// 1 + 1e-6): a build with -DMLSK_INJECT_RESCALE_BUG=1 scales every level-sample
+// rescale n / c by that factor, and the fp64 parity tests must then fail
+// (tests/test_gpu_negative_control.py).  Never set in the product build.
+#ifndef MLSK_INJECT_RESCALE_BUG
+#define MLSK_INJECT_RESCALE_BUG 0
+#endif
+constexpr double kRescalePerturb = MLSK_INJECT_RESCALE_BUG ? 1.0 + 1e-6 : 1.0;
+
 #define MLSK_CUDA(x)                                                                      \
     do {                                                                                  \
         cudaError_t e_ = (x);                                                             \
