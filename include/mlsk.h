@@ -196,6 +196,13 @@ int mlsk_session_stats(mlsk_session* s, mlsk_report* report);
 /* Packed per-level device buffer [(L+1)][cells + 2] = (sum Y, sum ||Y||^2,
  * count) in fp64, for an in-place NCCL all-reduce across ranks. */
 int mlsk_session_level_buffer(mlsk_session* s, void** device_ptr, int64_t* n_doubles);
+/* Checkpoint / resume: the session's accumulators and
+ * replication counters as host bytes.  buf = NULL: *bytes = the size needed.
+ * Restore into a session created with the same model, target, plan shape,
+ * seed and sharding (else MLSK_EINVAL); continuing it then gives the same bits
+ * as an uninterrupted run. */
+int mlsk_session_checkpoint(mlsk_session* s, void* buf, int64_t* bytes);
+int mlsk_session_restore(mlsk_session* s, const void* buf, int64_t bytes);
 int mlsk_session_synchronize(mlsk_session* s);
 int mlsk_session_destroy(mlsk_session* s);
 

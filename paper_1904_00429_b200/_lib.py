@@ -49,6 +49,8 @@ def lib():
     L.mlsk_session_run_round.argtypes = [C.c_void_p, _P(C.c_int64)]
     L.mlsk_session_stats.argtypes = [C.c_void_p, _P(abi.Report)]
     L.mlsk_session_level_buffer.argtypes = [C.c_void_p, _P(C.c_void_p), _P(C.c_int64)]
+    L.mlsk_session_checkpoint.argtypes = [C.c_void_p, C.c_void_p, _P(C.c_int64)]
+    L.mlsk_session_restore.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
     L.mlsk_session_synchronize.argtypes = [C.c_void_p]
     L.mlsk_session_destroy.argtypes = [C.c_void_p]
     L.mlsk_sketch_inner.argtypes = [_P(C.c_double), _P(C.c_double), C.c_int64, _P(C.c_uint32),

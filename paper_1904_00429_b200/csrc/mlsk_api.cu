@@ -787,6 +787,159 @@ int mlsk_session_level_buffer(mlsk_session* s, void** device_ptr, int64_t* n_dou
     });
 }
 
+// ---- checkpoint / resume ---------------------------------------------------
+// A session's state is its per-level accumulators and replication counters:
+// per level the device buffer [total | total_sq | open chunk | open_sq] and
+// (count, open_count, open_chunk), plus the next replication index of every
+// level.  The image is plain host bytes (little-endian PODs): a header that
+// identifies the run (plan shape, seed, target, model scalars, sharding), then
+// next_k[L+1], then for every accumulator unit (the session itself, or each
+// shard of a multi-device session in shard order) its levels.  Restoring into
+// a session created with the same arguments and continuing gives the same bits
+// as a run that never stopped.
+namespace {
+
+constexpr uint64_t kCkptMagic = 0x31504B43534B4C4DULL;  // "MLSKCKP1"
+
+struct CkptHeader {
+    uint64_t magic, version;
+    int64_t M, c0, L, cells, units;
+    uint64_t seed;
+    int32_t target, kind, dtype, stream_mode;
+    double tparam;
+    int64_t m, n, p, rff_dim;
+    uint64_t data_seed;
+    double sd, mean_lo, mean_hi, nu, sigma;
+    int64_t rank, world, host_means;
+};
+
+std::vector<mlsk_session*> ckpt_units(mlsk_session* s) {
+    std::vector<mlsk_session*> u;
+    if (s->multi())
+        for (auto& sh : s->shards) u.push_back(sh.get());
+    else
+        u.push_back(s);
+    return u;
+}
+
+CkptHeader ckpt_header(mlsk_session* s) {
+    CkptHeader h{};
+    const mlsk_model_desc& d = s->R.model.desc;
+    h.magic = kCkptMagic;
+    h.version = 1;
+    h.M = s->M;
+    h.c0 = s->c0;
+    h.L = s->L;
+    h.cells = s->R.model.rows * s->R.model.cols;
+    h.units = (int64_t)ckpt_units(s).size();
+    h.seed = s->R.seed;
+    h.target = s->R.target;
+    h.tparam = s->R.tparam;
+    h.kind = d.kind;
+    h.dtype = d.dtype;
+    h.stream_mode = d.stream_mode;
+    h.m = d.m;
+    h.n = d.n;
+    h.p = d.p;
+    h.rff_dim = d.rff_dim;
+    h.data_seed = d.data_seed;
+    h.sd = d.sd;
+    h.mean_lo = d.mean_lo;
+    h.mean_hi = d.mean_hi;
+    h.nu = d.nu;
+    h.sigma = d.sigma;
+    h.rank = s->R.rank;
+    h.world = s->R.world;
+    h.host_means = (d.mean_a || d.mean_b) ? 1 : 0;
+    return h;
+}
+
+int64_t ckpt_bytes(mlsk_session* s) {
+    const CkptHeader h = ckpt_header(s);
+    const int64_t per_level = 3 * (int64_t)sizeof(int64_t) + (2 * h.cells + 2) * (int64_t)sizeof(double);
+    return (int64_t)sizeof(CkptHeader) + (h.L + 1) * (int64_t)sizeof(int64_t) + h.units * (h.L + 1) * per_level;
+}
+
+}  // namespace
+
+int mlsk_session_checkpoint(mlsk_session* s, void* buf, int64_t* bytes) {
+    return guard([&] {
+        if (!s || !bytes) invalid("session: null argument");
+        const int64_t need = ckpt_bytes(s);
+        if (!buf) {  // size query
+            *bytes = need;
+            return;
+        }
+        if (*bytes < need) invalid("session_checkpoint: buffer too small");
+        const CkptHeader h = ckpt_header(s);
+        unsigned char* o = static_cast<unsigned char*>(buf);
+        std::memcpy(o, &h, sizeof h);
+        o += sizeof h;
+        std::memcpy(o, s->next_k.data(), sizeof(int64_t) * (h.L + 1));
+        o += sizeof(int64_t) * (h.L + 1);
+        for (mlsk_session* u : ckpt_units(s)) {
+            MLSK_CUDA(cudaSetDevice(u->ex->device));
+            for (const LevelState& st : u->levels) {
+                const int64_t meta[3] = {st.count, st.open_count, st.open_chunk};
+                std::memcpy(o, meta, sizeof meta);
+                o += sizeof meta;
+                MLSK_CUDA(cudaMemcpyAsync(o, st.buf.p, sizeof(double) * (2 * h.cells + 2), cudaMemcpyDeviceToHost,
+                                          u->ex->stream));
+                o += sizeof(double) * (2 * h.cells + 2);
+            }
+            MLSK_CUDA(cudaStreamSynchronize(u->ex->stream));
+        }
+        MLSK_CUDA(cudaSetDevice(s->ex->device));
+        *bytes = need;
+    });
+}
+
+int mlsk_session_restore(mlsk_session* s, const void* buf, int64_t bytes) {
+    return guard([&] {
+        if (!s || !buf) invalid("session: null argument");
+        const CkptHeader mine = ckpt_header(s);
+        if (bytes < (int64_t)sizeof(CkptHeader)) invalid("session_restore: not a session checkpoint");
+        CkptHeader h;
+        std::memcpy(&h, buf, sizeof h);
+        if (h.magic != kCkptMagic || h.version != 1) invalid("session_restore: not a session checkpoint");
+        // the run must be the same: plan shape, seed, target, model and sharding
+        if (h.M != mine.M || h.c0 != mine.c0 || h.L != mine.L || h.cells != mine.cells || h.units != mine.units ||
+            h.seed != mine.seed || h.target != mine.target || h.tparam != mine.tparam || h.kind != mine.kind ||
+            h.dtype != mine.dtype || h.stream_mode != mine.stream_mode || h.m != mine.m || h.n != mine.n ||
+            h.p != mine.p || h.rff_dim != mine.rff_dim || h.data_seed != mine.data_seed || h.sd != mine.sd ||
+            h.mean_lo != mine.mean_lo || h.mean_hi != mine.mean_hi || h.nu != mine.nu || h.sigma != mine.sigma ||
+            h.rank != mine.rank || h.world != mine.world || h.host_means != mine.host_means)
+            invalid("session_restore: the checkpoint belongs to a different run (model, plan, seed, target or "
+                    "sharding differ)");
+        if (bytes < ckpt_bytes(s)) invalid("session_restore: truncated checkpoint");
+        const unsigned char* i = static_cast<const unsigned char*>(buf) + sizeof h;
+        std::vector<int64_t> nk(h.L + 1);
+        std::memcpy(nk.data(), i, sizeof(int64_t) * (h.L + 1));
+        i += sizeof(int64_t) * (h.L + 1);
+        for (int64_t l = 0; l <= h.L; ++l)
+            if (nk[l] < 0) invalid("session_restore: corrupt checkpoint");
+        for (mlsk_session* u : ckpt_units(s)) {
+            MLSK_CUDA(cudaSetDevice(u->ex->device));
+            for (LevelState& st : u->levels) {
+                int64_t meta[3];
+                std::memcpy(meta, i, sizeof meta);
+                i += sizeof meta;
+                if (meta[0] < 0 || meta[1] < 0 || meta[1] > 64 || meta[2] < -1)
+                    invalid("session_restore: corrupt checkpoint");
+                st.count = meta[0];
+                st.open_count = meta[1];
+                st.open_chunk = meta[2];
+                MLSK_CUDA(cudaMemcpyAsync(st.buf.p, i, sizeof(double) * (2 * h.cells + 2), cudaMemcpyHostToDevice,
+                                          u->ex->stream));
+                i += sizeof(double) * (2 * h.cells + 2);
+            }
+            MLSK_CUDA(cudaStreamSynchronize(u->ex->stream));
+        }
+        MLSK_CUDA(cudaSetDevice(s->ex->device));
+        s->next_k = nk;
+    });
+}
+
 int mlsk_session_synchronize(mlsk_session* s) {
     return guard([&] {
         if (!s) invalid("session: null argument");

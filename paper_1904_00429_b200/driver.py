@@ -125,6 +125,28 @@ class ShardedSession:
         """This rank's virtual shards' packed buffers, in self.owned order."""
         return [np.asarray(s.packed_stats(), dtype=np.float64) for s in self.sessions]
 
+    def checkpoint(self) -> bytes:
+        """The owned virtual shards' images, length-prefixed, in owned order."""
+        import struct
+
+        out = b""
+        for s in self.sessions:
+            img = s.checkpoint()
+            out += struct.pack("<q", len(img)) + img
+        return out
+
+    def restore(self, image: bytes) -> None:
+        import struct
+
+        off = 0
+        for s in self.sessions:
+            (n,) = struct.unpack_from("<q", image, off)
+            off += 8
+            s.restore(image[off:off + n])
+            off += n
+        if off != len(image):
+            raise ValueError("ShardedSession.restore: the image holds a different number of shards")
+
     def close(self) -> None:
         for s in self.sessions:
             if hasattr(s, "close"):
@@ -219,25 +241,83 @@ def level_costs(M: int, c0: int, L: int, cells: int) -> List[float]:
     return out
 
 
+def _rank_of(group) -> int:
+    try:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            return dist.get_rank(group)
+    except Exception:
+        pass
+    return 0
+
+
+def save_checkpoint(path: str, session, n: Sequence[int], history, rounds: int, group=None) -> None:
+    """Driver state + this rank's session image, written atomically to
+    `path`.rank<r> (checkpoint/resume: the reference has
+    none; a long adaptive run -- config 3 at eps = 1e-3 is hours -- survives a
+    lost process)."""
+    import json
+    import os
+    import struct
+
+    meta = json.dumps({"version": 1, "n": [int(x) for x in n], "history": history, "rounds": rounds}).encode()
+    img = session.checkpoint()
+    f = f"{path}.rank{_rank_of(group)}"
+    tmp = f + ".tmp"
+    with open(tmp, "wb") as fh:
+        fh.write(b"MLSKDRV1" + struct.pack("<q", len(meta)) + meta + img)
+    os.replace(tmp, f)
+
+
+def load_checkpoint(path: str, session, group=None):
+    """(n, history, rounds) after restoring this rank's session image, or None."""
+    import json
+    import os
+    import struct
+
+    f = f"{path}.rank{_rank_of(group)}"
+    if not os.path.exists(f):
+        return None
+    data = open(f, "rb").read()
+    if data[:8] != b"MLSKDRV1":
+        raise ValueError(f"{f}: not an adaptive-driver checkpoint")
+    (k,) = struct.unpack_from("<q", data, 8)
+    meta = json.loads(data[16:16 + k].decode())
+    session.restore(data[16 + k:])
+    return meta["n"], meta["history"], meta["rounds"]
+
+
 def adaptive_mlmc(session, M: int, c0: int, L: int, eps: float, n_pilot: int = 256, theta: float = 1.0,
-                  max_rounds: int = 20, max_total: Optional[int] = None, group=None) -> AdaptiveResult:
+                  max_rounds: int = 20, max_total: Optional[int] = None, group=None,
+                  checkpoint: Optional[str] = None) -> AdaptiveResult:
     """Run rounds on `session` (an MlmcSession, or any object with run_round /
     packed_stats / cells) until sum_l V_l / N_l <= theta eps^2.
 
     `session` must be created with rank / world matching the process group:
     each rank then runs its chunk share of every round's dN.  A
     ShardedSession makes the whole run bit-identical across world sizes.
+
+    `checkpoint`: a path prefix; the driver state and the session image are
+    saved after every round, and a run started with an existing checkpoint
+    resumes from it (the session must be freshly created with the same
+    arguments).  A resumed run gives the same bits as one that never stopped.
     """
     levels = L + 1
     cells = session.cells
     C = level_costs(M, c0, L, cells)
-    n = [0] * levels
-    history = []
-    session.run_round([n_pilot] * levels)
-    n = [n_pilot] * levels
-    history.append(list(n))
+    resumed = load_checkpoint(checkpoint, session, group) if checkpoint else None
+    if resumed is not None:
+        n, history, rounds = resumed
+        n = [int(x) for x in n]
+    else:
+        session.run_round([n_pilot] * levels)
+        n = [n_pilot] * levels
+        history = [list(n)]
+        rounds = 1
     stats = allreduce_stats(session, levels, group)
-    rounds = 1
+    if checkpoint and resumed is None:
+        save_checkpoint(checkpoint, session, n, history, rounds, group)
     while rounds < max_rounds:
         target = optimal_allocation(stats.variances, C, eps, theta)
         dN = [max(0, t - k) for t, k in zip(target, n)]
@@ -253,6 +333,8 @@ def adaptive_mlmc(session, M: int, c0: int, L: int, eps: float, n_pilot: int = 2
         history.append(list(dN))
         stats = allreduce_stats(session, levels, group)
         rounds += 1
+        if checkpoint:
+            save_checkpoint(checkpoint, session, n, history, rounds, group)
     cost = int(sum(k * c for k, c in zip(stats.counts, C)))
     return AdaptiveResult(stats.value, stats, rounds, [int(x) for x in stats.counts], eps,
                           math.sqrt(stats.mse), cost, history)

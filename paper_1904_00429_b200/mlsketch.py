@@ -661,6 +661,19 @@ class MlmcSession:
             buf[l, cells + 1] = st.replication_count
         return buf.ravel()
 
+    def checkpoint(self) -> bytes:
+        """The session's accumulators and replication counters as bytes
+        (mlsk_session_checkpoint); `restore` them into a session created with
+        the same arguments to continue the run bit for bit."""
+        n = C.c_int64()
+        check(lib().mlsk_session_checkpoint(self._h, None, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        check(lib().mlsk_session_checkpoint(self._h, buf, C.byref(n)))
+        return buf.raw[: n.value]
+
+    def restore(self, image: bytes) -> None:
+        check(lib().mlsk_session_restore(self._h, image, len(image)))
+
     def synchronize(self) -> None:
         check(lib().mlsk_session_synchronize(self._h))
 
