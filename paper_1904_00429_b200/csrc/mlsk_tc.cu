@@ -126,6 +126,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// fire-and-forget fp32 add in L2 (no load round trip in the epilogue); the
+// reductions of one thread to one address apply in program order, so the
+// partial's bits do not depend on timing
+__device__ __forceinline__ void red_add_f32(float* p, float v) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_f64(double* p, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
 // UMMA shared-memory descriptor, K-major, SWIZZLE_64B (ROWB = 64) or
 // SWIZZLE_128B (ROWB = 128): 8-row groups 8 * ROWB bytes apart (SBO), version
 // 1 (sm_100), layout type 4 / 2.
@@ -754,6 +764,9 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
         // coalesced accesses per thread (row-major flushes cost 0.9 ms per config-3
         // level 0: one 32-byte sector per 8-byte access)
         double* out = part + (int64_t)g * (TBM * TBN) + (int64_t)(h * HC) * TBM + row;
+        // segmented samples (one flush per sample): an fp32 partial tile in
+        // the same column-major layout, summed by red.add (zeroed per launch)
+        float* outf = reinterpret_cast<float*>(part) + (int64_t)g * (TBM * TBN) + (int64_t)(h * HC) * TBM + row;
         int abuf = 0;
         uint32_t aph = 0;  // bit a = phase of accumulator a (no indexed local array)
         // R: the fp32 running sum S over samples when a sample is one TMEM
@@ -854,72 +867,34 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
 #else
             if (!(SPLIT && split_part <= 2) && (segmented || (smp + 1) % FLUSH == 0 || smp + 1 == my_samples)) {
 #endif
-                if (segmented) {
-                    // the sample's Y into this CTA's partial tile (L2-resident;
-                    // one CTA per tile: the first sample stores, and the tile is
-                    // added into the level total after the last sample)
-                    const bool fresh = sh.direct && smp == 0;
+                if (segmented && !sh.direct) {
+                    // the sample's Y into this CTA's fp32 partial tile by
+                    // reductions in L2: a load-add-store of an fp64 partial per
+                    // sample stalled the operand stream (config 3, c = 1024:
+                    // tensor pipe 95% -> 78% active, 300 MB of extra DRAM writes)
 #pragma unroll
-                    for (int i0 = 0; i0 < HC; i0 += 8) {
-                        double ov[8];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) ov[i] = fresh ? 0.0 : out[(i0 + i) * TBM];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) out[(i0 + i) * TBM] = ov[i] + (double)R[i0 + i];
-                        asm volatile("" ::: "memory");
-                    }
+                    for (int i = 0; i < HC; ++i) red_add_f32(outf + i * TBM, R[i]);
                 } else if (sh.direct) {
-                    // (tile-aligned outputs, one CTA per tile) this thread's 64
-                    // consecutive columns of the row-major level total, 16 bytes a time
-                    double2* o = reinterpret_cast<double2*>(sh.direct + ((int64_t)tm * TBM + row) * sh.cols +
-                                                            (int64_t)tn * TBN + h * HC);
+                    // (tile-aligned outputs, one CTA per tile, one sample per
+                    // CTA) this thread's 64 consecutive columns of the row-major
+                    // level total, by reductions in L2: a load-add-store here
+                    // sat in the CTA's tail (config 5, c = 2048: 1.39 ms vs
+                    // 1.14 at the same flops with the reductions)
+                    double* o = sh.direct + ((int64_t)tm * TBM + row) * sh.cols + (int64_t)tn * TBN + h * HC;
 #pragma unroll
-                    for (int i0 = 0; i0 < HC / 2; i0 += 4) {
-                        double2 ov[4];
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) ov[i] = o[i0 + i];
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            ov[i].x += (double)R[2 * (i0 + i)];
-                            ov[i].y += (double)R[2 * (i0 + i) + 1];
-                            o[i0 + i] = ov[i];
-                            R[2 * (i0 + i)] = 0.f;
-                            R[2 * (i0 + i) + 1] = 0.f;
-                        }
-                        asm volatile("" ::: "memory");  // bound the live doubles: 8 at a time
+                    for (int i = 0; i < HC; ++i) {
+                        red_add_f64(o + i, (double)R[i]);
+                        R[i] = 0.f;
                     }
                 } else {
+                    // the running sum into this CTA's fp64 partial tile by
+                    // reductions in L2 (no load round trip in the CTA's tail)
 #pragma unroll
-                    for (int i0 = 0; i0 < HC; i0 += 8) {
-                        double ov[8];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) ov[i] = out[(i0 + i) * TBM];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            out[(i0 + i) * TBM] = ov[i] + (double)R[i0 + i];
-                            R[i0 + i] = 0.f;
-                        }
-                        asm volatile("" ::: "memory");
+                    for (int i = 0; i < HC; ++i) {
+                        red_add_f64(out + i * TBM, (double)R[i]);
+                        R[i] = 0.f;
                     }
                 }
-            }
-        }
-        if (segmented && sh.direct && my_samples > 0 && !(SPLIT && split_part <= 2)) {
-            // one CTA per tile: its partial (this thread's own entries) into the level total
-            double2* o = reinterpret_cast<double2*>(sh.direct + ((int64_t)tm * TBM + row) * sh.cols +
-                                                    (int64_t)tn * TBN + h * HC);
-#pragma unroll
-            for (int i0 = 0; i0 < HC / 2; i0 += 4) {
-                double2 ov[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) ov[i] = o[i0 + i];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    ov[i].x += out[(2 * (i0 + i)) * TBM];
-                    ov[i].y += out[(2 * (i0 + i) + 1) * TBM];
-                    o[i0 + i] = ov[i];
-                }
-                asm volatile("" ::: "memory");
             }
         }
         sq = warp_sum(sq);
@@ -944,7 +919,8 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
 __global__ void __launch_bounds__(256) k_reduce_tiles_tc(const double* __restrict__ part,
                                                          const double* __restrict__ part_sq, TcShape sh,
                                                          int64_t rows, int64_t cols, double* __restrict__ total,
-                                                         double* __restrict__ total_sq) {
+                                                         double* __restrict__ total_sq, int f32part) {
+    const float* partf = reinterpret_cast<const float*>(part);  // segmented launches: fp32 partials
     __shared__ double blk[32][33];
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int64_t brows = (rows + 31) / 32, bcols = (cols + 31) / 32;
@@ -957,7 +933,10 @@ __global__ void __launch_bounds__(256) k_reduce_tiles_tc(const double* __restric
             const int tile = r < rows && q < cols ? tile_index(sh, (int)(r / TBM), (int)(q / TBN)) : -1;
             if (tile >= 0) {  // (cells of the lower blocks of a symmetric output: filled by the mirror)
                 const int64_t off = (q % TBN) * TBM + (r % TBM);
-                for (int grp = 0; grp < sh.Gs; ++grp) acc += part[(int64_t)(grp * sh.T + tile) * (TBM * TBN) + off];
+                for (int grp = 0; grp < sh.Gs; ++grp) {
+                    const int64_t e = (int64_t)(grp * sh.T + tile) * (TBM * TBN) + off;
+                    acc += f32part ? (double)partf[e] : part[e];
+                }
             }
             blk[tx][k] = acc;
         }
@@ -1145,7 +1124,11 @@ class TcEngine final : public PanelEngine {
         double* part_sq = part + (size_t)T_ * Gs_ * (TBM * TBN);
         const bool finishes = kr.part == 0 || kr.part == 3;  // samples complete in this launch
         // one CTA per tile and a tile-aligned output: sums straight into the level total
-        const bool direct = Gs_ == 1 && M_.rows % TBM == 0 && M_.cols % TBN == 0;
+        // Only a launch of one sample per CTA writes the level total directly: with
+        // several, the CTA partials (flushed by reductions) and one reduction pass
+        // are faster (config 5, c = 256, 8 samples per CTA: 1.41 -> 1.14 ms) --
+        // the direct flush is a load-add-store of 256 KB in each CTA's tail.
+        const bool direct = Gs_ == 1 && M_.rows % TBM == 0 && M_.cols % TBN == 0 && nb == 1;
         // one sample whose tiles fill the last CTA wave poorly (config 4: 512
         // tiles = 3.5 waves): split its K range over two CTA groups, 7 waves of
         // half the work, and combine the two partial Y afterwards
@@ -1167,8 +1150,9 @@ class TcEngine final : public PanelEngine {
             launched(3);
             return;
         }
-        if (finishes && !direct)
-            MLSK_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * (size_t)T_ * Gs_ * (TBM * TBN), s));
+        if (finishes && !direct)  // (segmented launches: the fp32 partials, half the bytes)
+            MLSK_CUDA(cudaMemsetAsync(part, 0, (segmented(k) ? sizeof(float) : sizeof(double)) * (size_t)T_ * Gs_ *
+                                                   (TBM * TBN), s));
         float* ypart = nullptr;
         if (kr.part != 0) {
             ws_.ypart.ensure((size_t)T_ * TBM * TBN);  // the carried partial Y of a split sample
@@ -1195,7 +1179,7 @@ class TcEngine final : public PanelEngine {
             // direct mode: only the squares are left to add (cells = 0)
             k_reduce_tiles_tc<<<direct ? 1 : (int)std::min<int64_t>((cells + 1023) / 1024, (int64_t)nsm_ * 8),
                                 dim3(32, 8), 0, s>>>(part, part_sq, sh, direct ? 0 : M_.rows, M_.cols, st.total(),
-                                                     st.total_sq());
+                                                     st.total_sq(), segmented(k) ? 1 : 0);
         }
         if (sym_nb_) {
             Prof p("mirror_tc", s);

@@ -31,8 +31,8 @@ elif args.config == 3:
     c0, LV, STEP = 64, 8, [8 * 2 ** (8 - l) for l in range(9)]
     gemm_name = "gemm_tf32x3"
 else:  # configs 4 and 5 as tools/bench_configs.py defines them
-    from tools.bench_configs import configs as _cfgs  # noqa: E402
-    cf = _cfgs()[args.config]
+    import bench_configs_lib  # noqa: E402
+    cf = bench_configs_lib.configs(g)[args.config]
     model, m, p, c0, STEP = cf["model"], cf["m"], cf["p"], cf["c0"], cf["N"]
     LV = len(STEP) - 1
     gemm_name = "gemm_tf32x3"
