@@ -196,20 +196,21 @@ def measure(ids, steps=3, with_cpu=True, device=0):
         L.mlsk_profile_reset()
         L.mlsk_profile_enable(1)
         launches0 = L.mlsk_kernel_launch_count()
+        nsteps = max(steps, 20) if c.get("inner") else steps  # config 1: 0.4 ms steps
         with bench.ClockSampler(device) as clk:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            for _ in range(steps):
+            for _ in range(nsteps):
                 sess.run_round(c["N"])
             e1.record(stream)
             e1.synchronize()
         L.mlsk_profile_enable(0)
         launches = L.mlsk_kernel_launch_count() - launches0
-        ms = e0.elapsed_time(e1) / steps
+        ms = e0.elapsed_time(e1) / nsteps
         kern = profile_read(L)
         samples = sum(c["N"])
         blk = {"workload": c["workload"], "ms_per_step": ms, "value": samples / (ms * 1e-3),
-               "unit": "level-samples/s", "steps": steps, "gpu_launches": launches, "kernels": kern,
+               "unit": "level-samples/s", "steps": nsteps, "gpu_launches": launches, "kernels": kern,
                "clocks": clk.summary()}
         if c.get("inner"):
             idx = sum(cl * n for cl, n in zip(levels_c, c["N"]))
@@ -237,8 +238,8 @@ def measure(ids, steps=3, with_cpu=True, device=0):
         else:
             flops = alg_flops(cid, c, levels_c)
             gem = kern.get("gemm_tf32x3", {"ms": 0.0, "launches": 0})
-            ach = flops * steps / (gem["ms"] * 1e-3) / 1e12 if gem["ms"] > 0 else None
-            long_region = ms * steps >= 1000.0 and tf32_sus
+            ach = flops * nsteps / (gem["ms"] * 1e-3) / 1e12 if gem["ms"] > 0 else None
+            long_region = ms * nsteps >= 1000.0 and tf32_sus
             peak_t = tf32_sus if long_region else tf32
             which = f"sustained: {sus_note}" if long_region else "burst"
             blk["sampled_gemm_tflops"] = sum(2.0 * c["m"] * c["p"] * cl * n for cl, n in zip(levels_c, c["N"])) \
