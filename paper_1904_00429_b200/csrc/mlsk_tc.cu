@@ -584,11 +584,22 @@ struct TcShape {
     int seg = 0;
 };
 
-// tile index -> (tile row of 128, tile column of 256)
+// tile index -> (tile row of 128, tile column of 256).  Full grids run in
+// groups of RASTER_G tile rows, column by column inside a group: the CTAs
+// resident at one time (148 of config 5's 2048 tiles) then cover about 16 x 9
+// tiles instead of 4.6 rows x all 32 columns, so the panel chunks they share
+// come from L2 and not once per wave from DRAM (config 5 at c = 512: 2.6 GB
+// of DRAM reads per launch for 268 MB of panels).
+constexpr int RASTER_G = 16;
 __device__ __forceinline__ void tile_coords(const TcShape& sh, int tile, int& tm, int& tn) {
     if (sh.sym_nb == 0) {
-        tm = tile / sh.tiles_n;
-        tn = tile % sh.tiles_n;
+        const int rows_t = sh.T / sh.tiles_n;
+        const int blk = tile / (RASTER_G * sh.tiles_n);
+        const int r0 = blk * RASTER_G;
+        const int rg = rows_t - r0 < RASTER_G ? rows_t - r0 : RASTER_G;  // rows in this group
+        const int w = tile - blk * RASTER_G * sh.tiles_n;
+        tm = r0 + w % rg;
+        tn = w / rg;
         return;
     }
     // blocks (R, C >= R) in row-major order, two 128-row tiles per block
@@ -604,7 +615,12 @@ __device__ __forceinline__ void tile_coords(const TcShape& sh, int tile, int& tm
 
 // (tile row, tile column) -> tile index; -1 for a block below the diagonal
 __device__ __forceinline__ int tile_index(const TcShape& sh, int tm, int tn) {
-    if (sh.sym_nb == 0) return tm * sh.tiles_n + tn;
+    if (sh.sym_nb == 0) {
+        const int rows_t = sh.T / sh.tiles_n;
+        const int r0 = tm / RASTER_G * RASTER_G;
+        const int rg = rows_t - r0 < RASTER_G ? rows_t - r0 : RASTER_G;
+        return r0 * sh.tiles_n + tn * rg + (tm - r0);
+    }
     const int R = tm >> 1;
     if (R > tn) return -1;
     return 2 * (R * sh.sym_nb - R * (R - 1) / 2 + (tn - R)) + (tm & 1);
@@ -956,16 +972,17 @@ __global__ void __launch_bounds__(256) k_reduce_tiles_tc(const double* __restric
 
 // kpar: Y = Y_0 + Y_1 (fp32, as a carried K-segment), level total += Y,
 // per-block sum of Y^2 in fp64 into blk_sq (then summed by one warp)
-__global__ void __launch_bounds__(256) k_kpar_combine(const float* __restrict__ yp, int T, int tiles_n, int64_t rows,
+__global__ void __launch_bounds__(256) k_kpar_combine(const float* __restrict__ yp, TcShape sh, int64_t rows,
                                                       int64_t cols, double* __restrict__ total,
                                                       double* __restrict__ blk_sq) {
+    const int T = sh.T;
     __shared__ double s_red[8];
     double sq = 0.0;
     const int64_t cells = rows * cols;
     for (int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cell < cells;
          cell += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = cell / cols, q = cell - r * cols;
-        const int tile = (int)((r / TBM) * tiles_n + q / TBN);
+        const int tile = tile_index(sh, (int)(r / TBM), (int)(q / TBN));
         const int64_t off = (int64_t)tile * (TBM * TBN) + (r % TBM) * TBN + (q % TBN);
         const float y = __fadd_rn(yp[off], yp[(int64_t)T * (TBM * TBN) + off]);
         total[cell] += (double)y;
@@ -1144,7 +1161,7 @@ class TcEngine final : public PanelEngine {
             {
                 Prof p("reduce_tiles_tc", s);
                 const int blocks = nsm_ * 4;  // blk_sq scratch: the (unused) partial buffer
-                k_kpar_combine<<<blocks, 256, 0, s>>>(ws_.ypart.p, T_, tiles_n_, M_.rows, M_.cols, st.total(), part);
+                k_kpar_combine<<<blocks, 256, 0, s>>>(ws_.ypart.p, sh, M_.rows, M_.cols, st.total(), part);
                 k_sum_sq<<<1, 32, 0, s>>>(part, blocks, st.total_sq());
             }
             launched(3);
