@@ -592,13 +592,13 @@ static double philox_entry(const orc_model* m, uint64_t key, int which, int64_t 
         orc_box_muller_f(r[2], r[3], &z[2], &z[3]);
         const float v = (z[1] * z[1] + z[2] * z[2]) + z[3] * z[3];
         const float t = z[0] / sqrtf(v / 3.0f);
-        const uint64_t e = which == 0 ? (uint64_t)rq * (uint64_t)n + (uint64_t)col
-                                      : (uint64_t)col * (uint64_t)m->cols + (uint64_t)rq;
+        /* the mean of row rq (A) / entry rq of B's row col: component rq & 3 of
+         * one block per row quad (include/mlsk_stream_spec.h, "student-t means") */
         const uint64_t dkey = orc_derive_seed(m->d.data_seed, MLSK_TAG_DATA, (uint64_t)which);
         uint32_t rd[4];
-        philox_block(dkey, (uint32_t)e, (uint32_t)(e >> 32), 0, MLSK_CTR_DATA, rd);
+        philox_block(dkey, (uint32_t)col, (uint32_t)((uint64_t)rq >> 2), 0, MLSK_CTR_SMEAN, rd);
         const float flo = (float)m->d.mean_lo, fw = (float)(m->d.mean_hi - m->d.mean_lo);
-        const float mean = flo + fw * ((float)(rd[0] >> 8) * 0x1.0p-24f);
+        const float mean = flo + fw * ((float)(rd[rq & 3] >> 8) * 0x1.0p-24f);
         return (double)(mean + t);
     }
     case MLSK_MODEL_RFF: {

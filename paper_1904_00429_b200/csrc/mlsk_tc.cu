@@ -169,19 +169,20 @@ struct TcModel {
     DevModel M;
 };
 
-// Student-t(3) entry with an on-the-fly mean: A[row][col] (which = 0) or B[col][row] (which = 1)
-__device__ __forceinline__ float student_t_entry(const TcModel& S, uint64_t key, int64_t col, int64_t rq, int which,
-                                                 const Tables& T) {
+// Student-t(3) draw t of A[row][col] (which = 0) or B[col][row] (which = 1)
+__device__ __forceinline__ float student_t_draw(uint64_t key, int64_t col, int64_t rq, int which, const Tables& T) {
     const u32x4 r = philox((uint32_t)col, (uint32_t)rq, (uint32_t)which, MLSK_CTR_T, key);
     float z[4];
     box_muller_f<true>(r.x, r.y, z[0], z[1], T);
     box_muller_f<true>(r.z, r.w, z[2], z[3], T);
     const float v = __fadd_rn(__fadd_rn(__fmul_rn(z[1], z[1]), __fmul_rn(z[2], z[2])), __fmul_rn(z[3], z[3]));
-    const float t = __fdiv_rn(z[0], __fsqrt_rn(__fdiv_rn(v, 3.0f)));
-    const uint64_t e = which == 0 ? (uint64_t)rq * (uint64_t)S.M.n + (uint64_t)col
-                                  : (uint64_t)col * (uint64_t)S.M.p + (uint64_t)rq;
-    const float mean = data_mean_f32(which == 0 ? S.M.st_key_a : S.M.st_key_b, e, S.M.st_lo, S.M.st_w);
-    return __fadd_rn(mean, t);
+    return __fdiv_rn(z[0], __fsqrt_rn(__fdiv_rn(v, 3.0f)));
+}
+// the entry with its on-the-fly mean (one row at a time: the generic path)
+__device__ __forceinline__ float student_t_entry(const TcModel& S, uint64_t key, int64_t col, int64_t rq, int which,
+                                                 const Tables& T) {
+    const float mean = st_mean(which == 0 ? S.M.st_key_a : S.M.st_key_b, col, rq, S.M.st_lo, S.M.st_w);
+    return __fadd_rn(mean, student_t_draw(key, col, rq, which, T));
 }
 
 // RFF feature sqrt(2/n) cos(w_col . x_row + b_col) (fp32 dot, accurate cosf)
@@ -269,8 +270,9 @@ __device__ __forceinline__ void gauss_phase_f32(const DevModel& M, const Tables&
 
 // Student-t(3) phase (config 5): same thread map as the gauss phase (a row
 // quad x a chunk-column pair per thread, 64-bit stores of the pair per row);
-// the eight entries are independent (two Philox blocks each: the t draw and
-// the on-the-fly mean), so the unrolled loop keeps many chains in flight.
+// per column one Philox block gives the on-the-fly means of the row quad and
+// each entry one block its t draw (1.25 blocks per entry; a block per mean
+// doubled the generator's integer work), independent chains in flight.
 template <bool IS_A>
 __device__ __forceinline__ void student_t_phase_f32(const TcModel& S, const Tables& T, uint64_t key, int64_t rb,
                                                     const int* s_j, const float* s_w, unsigned char* thi,
@@ -279,15 +281,20 @@ __device__ __forceinline__ void student_t_phase_f32(const TcModel& S, const Tabl
     const int r0 = 4 * qq;
     const int64_t lim = (IS_A ? S.M.m : S.M.p) - rb;
     float v[2][4];
+    const uint64_t mkey = IS_A ? S.M.st_key_a : S.M.st_key_b;
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
         const int j = s_j[2 * cp + u];
         const float w = IS_A ? 1.0f : s_w[2 * cp + u];
+        // the means of the thread's row quad: one Philox block (r0 is a multiple of 4)
+        const u32x4 mr = philox((uint32_t)j, (uint32_t)((rb + r0) >> 2), 0, MLSK_CTR_SMEAN, mkey);
+        const uint32_t mw[4] = {mr.x, mr.y, mr.z, mr.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             float x = 0.f;
             if (r0 + e < lim) {
-                x = student_t_entry(S, key, j, rb + r0 + e, IS_A ? 0 : 1, T);
+                x = __fadd_rn(st_mean_of(mw[e], S.M.st_lo, S.M.st_w),
+                              student_t_draw(key, j, rb + r0 + e, IS_A ? 0 : 1, T));
                 if (!IS_A) x = __fmul_rn(w, x);
             }
             v[u][e] = x;
