@@ -391,6 +391,7 @@ k_gemm_f64(const double* __restrict__ Apan, const double* __restrict__ Bpan, Gem
         mbar_wait(smem_u32(&bars[STAGES + p_s]), p_ph ^ 1);
         const uint32_t full = smem_u32(&bars[p_s]);
         mbar_expect_tx(full, A_STAGE_BYTES + B_STAGE_BYTES);
+        MLSK_DCHECK(p_b < sh.nb && p_kc < sh.nkc && (int64_t)tm * BM < sh.MP && (int64_t)tn * BN < sh.PP);
         const double* srcA = Apan + ((p_b * sh.nkc + p_kc) * sh.MP + (int64_t)tm * BM) * KC;
         const double* srcB = Bpan + ((p_b * sh.nkc + p_kc) * sh.PP + (int64_t)tn * BN) * KC;
         bulk_g2s(smem_u32(sA + p_s * (BM * KC)), srcA, A_STAGE_BYTES, full);
@@ -749,6 +750,7 @@ k_fused_inner_multi(DevModel M, uint64_t seed, const int64_t* __restrict__ ks, I
         int pi = 0;  // warp-uniform
         while (pi + 1 < P.n && task >= P.p[pi + 1].task_off) ++pi;
         const InnerPart& q = P.p[pi];
+        MLSK_DCHECK(task >= q.task_off && q.g >= 1 && q.g <= INNER_G);
         const int g = q.g, gl = lane & (g - 1);
         const int64_t b = (task - q.task_off) * (32 / g) + lane / g;
         const bool live = b < q.nb;
@@ -1007,6 +1009,7 @@ __global__ void k_expand_ks(const KsRun* __restrict__ runs, int nruns, int64_t t
             if (runs[mid].dst <= e) lo = mid;
             else hi = mid - 1;
         }
+        MLSK_DCHECK(runs[lo].dst <= e && e < runs[lo].dst + runs[lo].count);
         ks[e] = runs[lo].k0 + (e - runs[lo].dst);
     }
 }

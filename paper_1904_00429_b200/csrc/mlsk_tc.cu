@@ -706,6 +706,8 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 bar_arrive(full);
 #else
                 bar_expect_tx(full, TSTAGE_BYTES);
+                MLSK_DCHECK(b < (kpar ? 1 : sh.nb) && kc < sh.nkc && (int64_t)tm * TBM < sh.MP &&
+                            (int64_t)tn * TBN < sh.PP);
                 const int64_t oa = ((b * sh.nkc + kc) * sh.MP + (int64_t)tm * TBM) * TBK;
                 const int64_t ob = ((b * sh.nkc + kc) * sh.PP + (int64_t)tn * TBN) * TBK;
                 const uint32_t st = smem_addr(ring + s * TSTAGE_BYTES);
