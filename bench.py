@@ -366,11 +366,18 @@ def main():
     # bytes) of a full batch captured with ncu --set full, times this run's
     # algorithmic bytes per launch
     traffic = None
+    step_traffic = None
     prof_json = os.path.join(ROOT, "profiles", "gemm_f64_traffic.json")
     if os.path.exists(prof_json) and gemm["launches"] > 0:
         try:
-            ratio = json.load(open(prof_json)).get("dram_over_algorithmic")
+            pj = json.load(open(prof_json))
+            ratio = pj.get("dram_over_algorithmic")
             traffic = ratio * args.steps * panel_bytes_of(STEP_N) / gemm["launches"] if ratio else None
+            sr = pj.get("step_dram_over_algorithmic")
+            if sr:  # generator + GEMM DRAM bytes of a whole step (not the GEMM's reads alone)
+                step_traffic = {"dram_bytes_per_step": sr * panel_bytes_of(STEP_N),
+                                "algorithmic_bytes_per_step": panel_bytes_of(STEP_N), "ratio": sr,
+                                "source": pj.get("source")}
         except Exception:
             traffic = None
 
@@ -409,6 +416,7 @@ def main():
                              "peak_source": "fp64 DMMA throughput measured in this run "
                                             "(MEASURED_PEAKS.json has no fp64 entry)",
                              "algorithmic": "2*m*p*c_l flops per level-sample"},
+                "step_traffic": step_traffic,
                 "kernels": kern,
                 "step_fraction_gemm": (gemm["ms"] / sum(v["ms"] for v in kern.values())) if kern else None,
                 "gpu_launches": launches,
@@ -472,10 +480,13 @@ def run_e2e(g, torch, device, args, rank=0, world=1, dist=None):
         t = torch.tensor([dt], dtype=torch.float64, device="cuda" if on_dev else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t.item())
-    # what one rank's call moves: the two mean matrices and the replication list
-    # in, each level's [sum Y | sum ||Y||^2] out (mlsk_api.cu read_levels); with
-    # world > 1 also the all-reduce buffer in and out
-    h2d = pa.nbytes + pb.nbytes + 8 * sum(STEP_N) + (8 * levels * (cells + 1) if world > 1 else 0)
+    # what one rank's call moves: the two mean matrices and the replication runs
+    # (24 B each: one per level at world 1, one per owned 64-chunk when sharded;
+    # the index lists are expanded on the device) in, each level's
+    # [sum Y | sum ||Y||^2] out (mlsk_api.cu read_levels); with world > 1 also
+    # the all-reduce buffer in and out
+    runs = levels if world == 1 else sum(len(range(rank, (n * world + 63) // 64, world)) for n in STEP_N)
+    h2d = pa.nbytes + pb.nbytes + 24 * runs + (8 * levels * (cells + 1) if world > 1 else 0)
     d2h = 8 * levels * (cells + 1) * (2 if world > 1 else 1)
     return {"value": world * args.steps * sum(STEP_N) / dt, "unit": UNIT,
             "h2d_bytes_per_step": int(h2d),
