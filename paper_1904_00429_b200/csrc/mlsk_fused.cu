@@ -733,8 +733,14 @@ inline int inner_group(int64_t c) {
 // NL (nonlinear target f1 / f2, models.cpp:99-117): the prefix and suffix
 // sums are kept apart, Y = f((n/c)(S_pre + S_suf)) - f((n/cc) S_pre) per
 // replication (estimators.cpp:78-80), instead of one signed sum.
+// (256, 3): <= 80 registers, three CTAs per SM (uncapped: 118 registers, two
+// CTAs per SM, "wait" 35% of the stall samples at 24% warps active).  Measured
+// per step: 1 / 3 / 4 / 5 CTAs per SM 0.351 / 0.340 / 0.349 / 0.359 ms.
+#ifndef MLSK_INNER_MINB
+#define MLSK_INNER_MINB 3
+#endif
 template <bool NL>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, MLSK_INNER_MINB)
 k_fused_inner_multi(DevModel M, uint64_t seed, const int64_t* __restrict__ ks, InnerParts P,
                     double* __restrict__ y_out, int target, double tparam) {
     __shared__ __align__(16) double2 s_sc[256];
@@ -749,7 +755,7 @@ k_fused_inner_multi(DevModel M, uint64_t seed, const int64_t* __restrict__ ks, I
     for (int64_t task = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < P.tasks; task += warps) {
         int pi = 0;  // warp-uniform
         while (pi + 1 < P.n && task >= P.p[pi + 1].task_off) ++pi;
-        const InnerPart& q = P.p[pi];
+        const InnerPart q = P.p[pi];  // a register copy (a reference re-read the param bank per use)
         MLSK_DCHECK(task >= q.task_off && q.g >= 1 && q.g <= INNER_G);
         const int g = q.g, gl = lane & (g - 1);
         const int64_t b = (task - q.task_off) * (32 / g) + lane / g;
