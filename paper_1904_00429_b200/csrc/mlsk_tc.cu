@@ -413,13 +413,10 @@ constexpr int RFF_DMAX = 64;
 constexpr int RFF_COLS = 32;               // sampled columns per work item (X tile reuse)
 constexpr int RFF_CH = RFF_COLS / TBK;     // K-chunks per work item
 constexpr int RFF_RSPLIT = 4;              // work items per column group (row-block ranges)
-// MLSK_RFF_SMALL (experiment): 128 threads over 64-row X tiles (24 KB, <= 72
-// registers), small enough to sit beside a GEMM CTA on the same SM
-#ifdef MLSK_RFF_SMALL
-constexpr int RFF_T = 128, RFF_RB = 64, RFF_MINB = 7;
-#else
+// 256 threads over 128-row X tiles (a 128-thread / 64-row variant small
+// enough to sit beside a GEMM CTA was measured neutral in round 1: sharing the
+// SM trades GEMM time for generator time one for one)
 constexpr int RFF_T = GEN_T, RFF_RB = TBM, RFF_MINB = 1;
-#endif
 constexpr int RFF_SMEM = (RFF_DMAX * RFF_RB + RFF_DMAX * RFF_COLS) * 4;  // X tile + W columns (40 KB)
 
 // work item (b, column group of 32 sampled columns, range of 128-row blocks):
