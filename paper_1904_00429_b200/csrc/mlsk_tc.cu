@@ -13,18 +13,29 @@
 //                     generated on the fly), written as hi / lo K-chunks in the
 //                     UMMA canonical K-major SWIZZLE_64B layout (16 tf32 = 64 B
 //                     per row of a K-chunk).
-//  k_gemm_tf32x3      persistent CTAs, one 128 x 256 output tile per CTA over a
-//                     strided set of samples.  warp 0: cp.async.bulk producer
-//                     (4-stage mbarrier ring, 48 KB per stage: A_hi, A_lo,
-//                     B_hi, B_lo of one K-chunk); warp 1: TMEM allocation +
-//                     single-thread tcgen05.mma (M128 N256 K8) issue into two
-//                     256-column TMEM accumulators (all 512 columns,
-//                     double-buffered across samples); warps 2-17: epilogue,
-//                     four warps per TMEM lane quadrant taking 64 columns each
-//                     (tcgen05.ld, Y^2 into fp64, running sum in 64 registers
-//                     per thread, flushed to an fp64 per-CTA partial every 32
-//                     samples).  N = 256 cuts the operand bytes per flop that
-//                     cross L2 -> SMEM by a quarter vs 128 x 128 tiles.
+//  k_gemm_tf32x3      one 128 x 256 output tile per CTA over a strided set of
+//                     samples (tile groups: Gs CTAs per tile when the grid is
+//                     smaller than the SM count), 20 warps in two register
+//                     classes (setmaxnreg): warpgroup 0 = warp 0 the
+//                     cp.async.bulk producer (4-stage mbarrier ring, 48 KB per
+//                     stage: A_hi, A_lo, B_hi, B_lo of one K-chunk), warp 1
+//                     TMEM allocation + single-thread tcgen05.mma (M128 N256 K8,
+//                     3 MMAs per K-step) into two 256-column TMEM accumulators
+//                     (all 512 columns, double-buffered across samples and
+//                     accumulation segments), warps 2-3 idle; warps 4-19 the
+//                     epilogue, four per TMEM lane quadrant taking 64 columns
+//                     each (tcgen05.ld.32x32b.x16, ||Y||^2 in fp64, the running
+//                     sum in 64 fp32 registers per thread, flushed every 32
+//                     samples by red.global.add into an fp64 CTA partial, or
+//                     -- samples longer than TC_SEG K-chunks -- each sample's Y,
+//                     summed over its segments in registers with round-to-
+//                     nearest, by red.add.f32 into an fp32 partial).  Tiles are
+//                     rasterised in groups of 16 tile rows.  N = 256 cuts the
+//                     operand bytes per flop that cross L2 -> SMEM by a quarter
+//                     vs 128 x 128 tiles.
+//  k_reduce_tiles_tc  level total += the group partials (fixed order);
+//  k_kpar_combine     one-sample levels split over two CTA groups along K;
+//  k_mirror_lower     symmetric (RFF Gram) outputs: lower blocks mirrored.
 
 #include <algorithm>
 #include <cmath>
