@@ -117,6 +117,12 @@ struct EstimatorOptions {
     int device = -1;
     int engine = MLSK_ENGINE_AUTO;
     int rank = 0, world = 1;
+    // several GPUs inside one call (mlsk_exec_opts.n_devices / device_ids; the
+    // reference's threads, parallel.hpp:18-52); deterministic: fixed virtual
+    // shards, bit-identical results for any device count dividing vshards
+    std::vector<int32_t> devices;
+    bool deterministic = false;
+    int vshards = 0;
 };
 
 namespace detail {
@@ -132,6 +138,12 @@ inline mlsk_exec_opts opts_of(const EstimatorOptions& o) {
     x.engine = o.engine;
     x.rank = o.rank;
     x.world = o.world;
+    if (!o.devices.empty()) {
+        x.n_devices = (int32_t)o.devices.size();
+        x.device_ids = o.devices.data();  // `o` outlives the call
+    }
+    x.deterministic = o.deterministic ? 1 : 0;
+    x.vshards = o.vshards;
     return x;
 }
 }  // namespace detail
@@ -216,5 +228,60 @@ inline MatrixReference reference_matmul(const Model& model, const TargetFunction
     check(mlsk_reference_matmul(&d, f.kind, f.param, (int64_t)count, seed, &o, r.value.data(), &r.std_error));
     return r;
 }
+
+// Round-based session (adaptive MLMC; no reference analogue): run_round(dN)
+// continues every level's replication index; stats() as mlmc_matmul's report;
+// checkpoint() / restore() serialise the accumulators (same run only).
+class Session {
+   public:
+    Session(const Model& model, const TargetFunction& f, std::size_t M, std::size_t L, std::uint64_t seed,
+            std::size_t c0 = 1, const EstimatorOptions& options = {})
+        : L_(L), cells_(model.rows() * model.cols()) {
+        const mlsk_model_desc d = detail::desc_of(model);
+        const mlsk_exec_opts o = detail::opts_of(options);
+        check(mlsk_session_create(&d, f.kind, f.param, (int64_t)M, (int64_t)c0, (int64_t)L, seed, &o, &s_));
+    }
+    Session(const Session&) = delete;
+    Session& operator=(const Session&) = delete;
+    ~Session() {
+        if (s_) mlsk_session_destroy(s_);
+    }
+    void run_round(const std::vector<long long>& dN) {
+        if (dN.size() != L_ + 1) throw std::invalid_argument("session: dN must have L+1 entries");
+        std::vector<int64_t> d(dN.begin(), dN.end());
+        check(mlsk_session_run_round(s_, d.data()));
+    }
+    EstimateReport<std::vector<double>> stats() {
+        const std::size_t levels = L_ + 1;
+        std::vector<double> value(cells_), est(levels * cells_), msq(levels);
+        std::vector<int64_t> cnt(levels), cost(levels);
+        mlsk_report r{};
+        r.value = value.data();
+        r.level_estimate = est.data();
+        r.level_mean_sq = msq.data();
+        r.level_count = cnt.data();
+        r.cost_units = cost.data();
+        check(mlsk_session_stats(s_, &r));
+        EstimateReport<std::vector<double>> out{value, {}, r.total_cost_units, r.wall_time_s, r.seed};
+        for (std::size_t l = 0; l < levels; ++l)
+            out.per_level.push_back({l, std::vector<double>(est.begin() + l * cells_, est.begin() + (l + 1) * cells_),
+                                     cnt[l], msq[l], cost[l]});
+        return out;
+    }
+    std::vector<unsigned char> checkpoint() {
+        int64_t n = 0;
+        check(mlsk_session_checkpoint(s_, nullptr, &n));
+        std::vector<unsigned char> img((std::size_t)n);
+        check(mlsk_session_checkpoint(s_, img.data(), &n));
+        return img;
+    }
+    void restore(const std::vector<unsigned char>& img) {
+        check(mlsk_session_restore(s_, img.data(), (int64_t)img.size()));
+    }
+
+   private:
+    mlsk_session* s_ = nullptr;
+    std::size_t L_, cells_;
+};
 
 }  // namespace mlsketch_b200

@@ -98,3 +98,5 @@ def test_cpp_wrapper_on_device(tmp_path):
     assert r.returncode == 0, r.stdout
     assert r.stdout.startswith("value 37.0 level1 0.0")
     assert "reference 19.0 22.0 43.0 50.0 se 0.0" in r.stdout
+    assert "deterministic 1 vs 2 devices identical 1" in r.stdout
+    assert "resume identical 1" in r.stdout
