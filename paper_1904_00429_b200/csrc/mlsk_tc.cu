@@ -48,6 +48,9 @@ namespace mlsk {
 
 namespace {
 
+#ifndef MLSK_PANEL_HINT
+#define MLSK_PANEL_HINT 1  // measured: config 5 -2.6%, config 3 neutral; 2 (loads too): +7% / +10% slower
+#endif
 constexpr int TBM = 128, TBN = 256, TBK = 16;       // TBK tf32 = 64 bytes per row (SWIZZLE_64B)
 constexpr int ROWB = TBK * 4;                       // bytes per K-chunk row
 #ifndef MLSK_TC_STAGES
@@ -105,9 +108,35 @@ __device__ __forceinline__ void bar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+#if MLSK_PANEL_HINT >= 2
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+#else
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
+#endif
+}
+// panel tile out of shared memory by the TMA engine; MLSK_PANEL_HINT >= 1: with
+// an L2 evict_first policy (panels stream through L2 once; the model's means
+// and the CTA partials are what should stay)
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+#if MLSK_PANEL_HINT >= 1
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+                 "r"((uint32_t)__cvta_generic_to_shared(src)), "r"(bytes), "l"(pol)
+                 : "memory");
+#else
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"((uint32_t)__cvta_generic_to_shared(src)), "r"(bytes)
+                 : "memory");
+#endif
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -399,12 +428,8 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                 const int64_t off = (((int64_t)b * nkc + kc) * (isA ? MP : PP) + rb) * TBK;
                 float* dh = (isA ? Ahi : Bhi) + off;
                 float* dl = (isA ? Alo : Blo) + off;
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dh),
-                             "r"((uint32_t)__cvta_generic_to_shared(thi)), "r"((uint32_t)TTILE)
-                             : "memory");
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dl),
-                             "r"((uint32_t)__cvta_generic_to_shared(tlo)), "r"((uint32_t)TTILE)
-                             : "memory");
+                bulk_store(dh, thi, TTILE);
+                bulk_store(dl, tlo, TTILE);
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // the other buffer is free
             }
