@@ -249,8 +249,18 @@ struct Runner {
     void run(const std::vector<Item>& items, cudaStream_t s, int64_t probe_k) {
         if (engine == MLSK_ENGINE_FUSED) {
             std::vector<FusedJob> jobs;
-            for (const auto& it : items)
-                jobs.push_back(FusedJob{it.lv, plan_segments(it.k0, it.k1, rank, world, *it.st), it.st, it.probe});
+            for (const auto& it : items) {
+                // the fused engines need only which replications run (no open
+                // 64-chunk bookkeeping): at world 1 one segment per level (per-chunk
+                // segments cost ~16 k host objects per config-1 round)
+                std::vector<Segment> segs;
+                if (world == 1) {
+                    if (it.k1 > it.k0) segs.push_back(Segment{it.k0 / 64, it.k0, it.k1 - it.k0, false, false});
+                } else {
+                    segs = plan_segments(it.k0, it.k1, rank, world, *it.st);
+                }
+                jobs.push_back(FusedJob{it.lv, std::move(segs), it.st, it.probe});
+            }
             RunArgs a{&model, target, tparam, seed, s, wsp, probe_k, nullptr};
             fused_run_round(a, jobs);
             return;

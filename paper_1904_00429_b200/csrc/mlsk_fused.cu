@@ -725,6 +725,7 @@ struct InnerPart {
     int64_t y_off;     // first output slot (parts are contiguous)
     int64_t nb;
     int64_t task_off;  // first warp task
+    int64_t k0;        // >= 0: the part's replications are k0, k0 + 1, ... (no index list read)
     int g;             // threads per replication (power of two <= INNER_G)
     double* total;
     double* total_sq;
@@ -773,7 +774,8 @@ k_fused_inner_multi(DevModel M, uint64_t seed, const int64_t* __restrict__ ks, I
         const bool live = b < q.nb;
         double acc = 0.0, pre = 0.0;
         if (live) {
-            const uint64_t key = derive_seed(seed, q.tag, (uint64_t)ks[q.ks_off + b]);
+            const int64_t k = q.k0 >= 0 ? q.k0 + b : ks[q.ks_off + b];
+            const uint64_t key = derive_seed(seed, q.tag, (uint64_t)k);
             for (int64_t tp = gl; 2 * tp < q.c; tp += g) {
                 const u32x4 ri = philox((uint32_t)tp, 0, 0, MLSK_CTR_INDEX, key);
 #pragma unroll
@@ -1180,6 +1182,8 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         auto flush = [&]() {
             if (parts.n == 0) return;
             ws.v.ensure((size_t)filled);
+            // many more CTAs than fit at once: the block scheduler then balances
+            // the tasks dynamically (a one-wave grid-stride grid was 5% slower)
             const int64_t grid = std::min<int64_t>((parts.tasks * 32 + 255) / 256, (int64_t)sms * 16);
             {
                 Prof p("fused_inner_f64", P.s_gen);
@@ -1217,8 +1221,16 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
                 if (parts.n == INNER_MAX_PARTS || filled == max_slice) flush();
                 const int64_t take = std::min(total - off, max_slice - filled);
                 const int g = inner_group(c);
-                parts.p[parts.n++] = InnerPart{job.lv.tag, c,        cc,          w_fine, w_coarse, job_off[j] + off,
-                                               filled,     take,     parts.tasks, g,      job.st->total(),
+                // contiguous replications (one run covers the part): k = k0 + b
+                int64_t k0 = -1;
+                const int64_t pos = job_off[j] + off;
+                for (const KsRun& r : runs)
+                    if (r.dst <= pos && pos + take <= r.dst + r.count) {
+                        k0 = r.k0 + (pos - r.dst);
+                        break;
+                    }
+                parts.p[parts.n++] = InnerPart{job.lv.tag, c,    cc,          w_fine, w_coarse,        job_off[j] + off,
+                                               filled,     take, parts.tasks, k0,     g,               job.st->total(),
                                                job.st->total_sq()};
                 parts.tasks += (take * g + 31) / 32;
                 filled += take;
