@@ -61,6 +61,12 @@ constexpr int TTILE = TBM * TBK * 4;                // 8 KB: one 128-row K-chunk
 constexpr int TA_BYTES = TTILE, TB_BYTES = 2 * TTILE;
 constexpr int TSTAGE_BYTES = 2 * TA_BYTES + 2 * TB_BYTES;  // A_hi, A_lo, B_hi, B_lo: 48 KB
 constexpr int EPI_WARPS = 16;                       // four per TMEM lane quadrant (64-column quarters)
+// CTA pair (cta_group::2, M = 256 over two SMs of a TPC): each CTA stages its
+// own 128 A rows and HALF of the 256 B columns, 32 KB per stage, six stages
+constexpr int PSTAGES = 6;
+constexpr int PB_BYTES = TTILE;                             // half a B tile (128 columns)
+constexpr int PSTAGE_BYTES = 2 * TA_BYTES + 2 * PB_BYTES;  // 32 KB
+static_assert(PSTAGES * PSTAGE_BYTES <= TSTAGES * TSTAGE_BYTES, "pair ring must fit the single ring's smem");
 // warpgroup 0: producer (warp 0), TMEM allocation + MMA issue (warp 1), two
 // idle warps; warpgroups 1-4: epilogue.  setmaxnreg moves registers from the
 // control warpgroup to the epilogue (24 / 112 per thread) for its 64-entry
@@ -142,6 +148,47 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+// CTA pair: the MMA completion arrives on the barrier at the same offset in both CTAs
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+        "h"((uint16_t)3)
+        : "memory");
+}
+// this CTA's shared address `a` as seen in cluster CTA `rank`
+__device__ __forceinline__ uint32_t cluster_addr(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+// (relaxed: a release arrive compiles to MEMBAR.ALL.GPU -- microseconds per
+// stage on the relay's critical path; the data it reports is already complete:
+// the stage's bulk copies have landed (observed on this CTA's barrier), the
+// TMEM reads have returned (tcgen05.wait::ld))
+__device__ __forceinline__ void bar_arrive_remote(uint32_t cluster_bar) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void bar_wait_cluster(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void tc_mma_tf32_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
 }
 __device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                             uint32_t accumulate) {
@@ -670,7 +717,13 @@ __device__ __forceinline__ int tile_index(const TcShape& sh, int tm, int tn) {
 // 3 last, partial Y in ypart); a separate instantiation for the common path.
 // SEGM: a sample's K-range runs as several TMEM accumulation segments of
 // sh.seg K-chunks (TcShape::seg) summed in registers; else one segment.
-template <bool SPLIT, bool SEGM>
+// PAIR: clusters of two CTAs on tiles (tm, tn), (tm + 1, tn): the leader
+// (rank 0) issues tcgen05.mma.cta_group::2 (M = 256) over both CTAs' shared
+// memory, each CTA loading its A rows and half of the B columns (a third less
+// shared-memory traffic per SM than the single-CTA tile, six stages); the
+// peer relays its stage arrivals to the leader, both epilogues read their
+// own TMEM lanes and release the accumulator to the leader.
+template <bool SPLIT, bool SEGM, bool PAIR>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, const float* __restrict__ Bhi,
               const float* __restrict__ Blo, TcShape sh, double* __restrict__ part, double* __restrict__ part_sq,
@@ -678,7 +731,11 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
     extern __shared__ __align__(1024) unsigned char dsm[];
     // 1024-byte aligned stage ring (SW128 atoms)
     unsigned char* ring = dsm + ((1024 - (smem_addr(dsm) & 1023)) & 1023);
-    __shared__ __align__(8) uint64_t bars[2 * TSTAGES + 5];  // full, empty, tmem_full[2], tmem_empty[2], tmem_done
+    constexpr int NST = PAIR ? PSTAGES : TSTAGES;
+    constexpr int STB = PAIR ? PSTAGE_BYTES : TSTAGE_BYTES;
+    constexpr int BB = PAIR ? PB_BYTES : TB_BYTES;  // B bytes per stage held by this CTA
+    // full[NST], empty[NST], tmem_full[2], tmem_empty[2], tmem_done, pair: peer_full[NST], pair_done
+    __shared__ __align__(8) uint64_t bars[3 * PSTAGES + 6];
     __shared__ uint32_t s_tmem;
     __shared__ double s_sq[EPI_WARPS];
 
@@ -696,28 +753,41 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
     const int64_t seg = SEGM && sh.seg > 0 && sh.seg < ke - kb ? sh.seg : ke - kb;  // K-chunks per TMEM segment
     const int nseg = (int)((ke - kb + seg - 1) / seg);                             // segments per sample
 
-    const uint32_t full0 = smem_addr(&bars[0]), empty0 = smem_addr(&bars[TSTAGES]);
-    const uint32_t tfull0 = smem_addr(&bars[2 * TSTAGES]), tempty0 = smem_addr(&bars[2 * TSTAGES + 2]);
-    const uint32_t tdone = smem_addr(&bars[2 * TSTAGES + 4]);
+    const uint32_t full0 = smem_addr(&bars[0]), empty0 = smem_addr(&bars[NST]);
+    const uint32_t tfull0 = smem_addr(&bars[2 * NST]), tempty0 = smem_addr(&bars[2 * NST + 2]);
+    const uint32_t tdone = smem_addr(&bars[2 * NST + 4]);
+    const uint32_t pfull0 = smem_addr(&bars[2 * NST + 5]), pdone = smem_addr(&bars[3 * NST + 5]);
+    uint32_t rank = 0;
+    if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
     if (threadIdx.x == 0) {
-        for (int s = 0; s < TSTAGES; ++s) {
+        for (int s = 0; s < NST; ++s) {
             bar_init(full0 + 8 * s, 1);
             bar_init(empty0 + 8 * s, 1);
+            if (PAIR) bar_init(pfull0 + 8 * s, 1);
         }
         for (int a = 0; a < 2; ++a) {
             bar_init(tfull0 + 8 * a, 1);
-            bar_init(tempty0 + 8 * a, EPI_WARPS);
+            bar_init(tempty0 + 8 * a, PAIR ? 2 * EPI_WARPS : EPI_WARPS);  // pair: both CTAs' epilogues (leader's)
         }
         bar_init(tdone, EPI_WARPS);  // every epilogue warp finished with TMEM
+        if (PAIR) bar_init(pdone, 2);  // both CTAs done with the pair's TMEM
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&s_tmem)),
-                     "r"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&s_tmem)),
+                         "r"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&s_tmem)),
+                         "r"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
     __syncthreads();
+    if (PAIR)  // both CTAs' barriers initialised before any remote arrive / multicast commit
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     tc_fence_after();
     const uint32_t tmem = s_tmem;
 
@@ -733,30 +803,46 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             uint32_t ph = 0;
             int64_t b = kpar ? 0 : grp, kc = kb;
             for (int64_t it = 0; it < iters; ++it) {
-                bar_wait(empty0 + 8 * s, ph ^ 1);
+                // (pair: freed by the leader's multicast commit)
+                if (PAIR) bar_wait_cluster(empty0 + 8 * s, ph ^ 1);
+                else bar_wait(empty0 + 8 * s, ph ^ 1);
                 const uint32_t full = full0 + 8 * s;
 #ifdef MLSK_TC_ABL_NOLD  // ablation (timing only, wrong results): no operand loads
                 bar_arrive(full);
 #else
-                bar_expect_tx(full, TSTAGE_BYTES);
+                bar_expect_tx(full, STB);
                 MLSK_DCHECK(b < (kpar ? 1 : sh.nb) && kc < sh.nkc && (int64_t)tm * TBM < sh.MP &&
                             (int64_t)tn * TBN < sh.PP);
                 const int64_t oa = ((b * sh.nkc + kc) * sh.MP + (int64_t)tm * TBM) * TBK;
-                const int64_t ob = ((b * sh.nkc + kc) * sh.PP + (int64_t)tn * TBN) * TBK;
-                const uint32_t st = smem_addr(ring + s * TSTAGE_BYTES);
+                // (pair: this CTA's half of the B tile, columns tn 256 + rank 128 ..)
+                const int64_t ob = ((b * sh.nkc + kc) * sh.PP + (int64_t)tn * TBN + (PAIR ? rank * TBM : 0)) * TBK;
+                const uint32_t st = smem_addr(ring + s * STB);
                 bulk_load(st, Ahi + oa, TA_BYTES, full);
                 bulk_load(st + TA_BYTES, Alo + oa, TA_BYTES, full);
-                bulk_load(st + 2 * TA_BYTES, Bhi + ob, TB_BYTES, full);
-                bulk_load(st + 2 * TA_BYTES + TB_BYTES, Blo + ob, TB_BYTES, full);
+                bulk_load(st + 2 * TA_BYTES, Bhi + ob, BB, full);
+                bulk_load(st + 2 * TA_BYTES + BB, Blo + ob, BB, full);
 #endif
-                if (++s == TSTAGES) { s = 0; ph ^= 1; }
+                if (++s == NST) { s = 0; ph ^= 1; }
                 if (++kc == ke) { kc = kb; b += sh.Gs; }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc = tf32_idesc(TBM, TBN);
+        if (PAIR && rank == 1) {
+            // the peer's stage arrivals relayed to the leader, which issues the
+            // pair's MMAs over both CTAs' shared memory
+            if (lane == 0) {
+                int s = 0;
+                uint32_t ph = 0;
+                const uint32_t lead_pfull0 = cluster_addr(pfull0, 0);
+                for (int64_t it = 0; it < iters; ++it) {
+                    bar_wait(full0 + 8 * s, ph);
+                    bar_arrive_remote(lead_pfull0 + 8 * s);
+                    if (++s == NST) { s = 0; ph ^= 1; }
+                }
+            }
+        } else if (lane == 0) {
+            constexpr uint32_t idesc = tf32_idesc(PAIR ? 2 * TBM : TBM, TBN);
             int s = 0;
             uint32_t ph = 0;
             int64_t kc = kb;
@@ -765,43 +851,65 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             uint32_t aph = 0;  // bit a = phase of accumulator a (no indexed local array)
             for (int64_t it = 0; it < iters; ++it) {
                 if (sgc == 0) {  // first K-chunk of a segment (kpar: this CTA's range starts at kb > 0)
-                    bar_wait(tempty0 + 8 * abuf, ((aph >> abuf) & 1u) ^ 1u);  // epilogue released this accumulator
+                    // the epilogue(s) released this accumulator
+                    if (PAIR) bar_wait_cluster(tempty0 + 8 * abuf, ((aph >> abuf) & 1u) ^ 1u);
+                    else bar_wait(tempty0 + 8 * abuf, ((aph >> abuf) & 1u) ^ 1u);
                     tc_fence_after();
                 }
                 bar_wait(full0 + 8 * s, ph);
+                if (PAIR) bar_wait_cluster(pfull0 + 8 * s, ph);  // the peer's half of the stage
                 tc_fence_after();
-                const uint32_t st = smem_addr(ring + s * TSTAGE_BYTES);
+                const uint32_t st = smem_addr(ring + s * STB);
                 const uint32_t dcol = tmem + (uint32_t)abuf * TBN;
                 const uint32_t id = sh.kc0 + kc < sh.neg_kc ? idesc | (1u << 14) : idesc;  // negate B
 #pragma unroll
                 for (int kk = 0; kk < TBK / 8; ++kk) {
                     const uint64_t ah = sw_desc(st + kk * 32), al = sw_desc(st + TA_BYTES + kk * 32);
                     const uint64_t bh = sw_desc(st + 2 * TA_BYTES + kk * 32);
-                    const uint64_t bl = sw_desc(st + 2 * TA_BYTES + TB_BYTES + kk * 32);
+                    const uint64_t bl = sw_desc(st + 2 * TA_BYTES + BB + kk * 32);
 #ifndef MLSK_TC_ABL_NOMMA  // ablation: no MMAs (commits only)
-                    tc_mma_tf32(dcol, ah, bh, id, (sgc > 0 || kk > 0) ? 1u : 0u);
-                    tc_mma_tf32(dcol, ah, bl, id, 1u);
-                    tc_mma_tf32(dcol, al, bh, id, 1u);
+                    if (PAIR) {
+                        tc_mma_tf32_pair(dcol, ah, bh, id, (sgc > 0 || kk > 0) ? 1u : 0u);
+                        tc_mma_tf32_pair(dcol, ah, bl, id, 1u);
+                        tc_mma_tf32_pair(dcol, al, bh, id, 1u);
+                    } else {
+                        tc_mma_tf32(dcol, ah, bh, id, (sgc > 0 || kk > 0) ? 1u : 0u);
+                        tc_mma_tf32(dcol, ah, bl, id, 1u);
+                        tc_mma_tf32(dcol, al, bh, id, 1u);
+                    }
 #endif
                 }
-                tc_commit(empty0 + 8 * s);  // smem stage free once these MMAs complete
-                if (++s == TSTAGES) { s = 0; ph ^= 1; }
+                // smem stage free once these MMAs complete (pair: in both CTAs)
+                if (PAIR) tc_commit_pair(empty0 + 8 * s);
+                else tc_commit(empty0 + 8 * s);
+                if (++s == NST) { s = 0; ph ^= 1; }
                 ++sgc;
                 const bool sample_end = ++kc == ke;
                 if (sample_end) kc = kb;
                 if (sample_end || sgc == seg) {
                     sgc = 0;
-                    tc_commit(tfull0 + 8 * abuf);  // accumulator segment complete
+                    if (PAIR) tc_commit_pair(tfull0 + 8 * abuf);  // accumulator segment complete
+                    else tc_commit(tfull0 + 8 * abuf);
                     aph ^= 1u << abuf;
                     abuf ^= 1;
                 }
             }
         }
         // TMEM is freed once every epilogue warp has read its last accumulator
+        // (pair: in both CTAs -- each CTA's warp 1 arrives on both pair_done)
         __syncwarp();
         bar_wait(tdone, 0);
+        if (PAIR) {
+            if (lane == 0) {
+                bar_arrive_remote(cluster_addr(pdone, 0));
+                bar_arrive_remote(cluster_addr(pdone, 1));
+            }
+            __syncwarp();
+            bar_wait_cluster(pdone, 0);
+        }
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+        if (PAIR) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+        else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
     }
     return;  // warps 2, 3: idle
     }
@@ -845,13 +953,18 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             }
         };
         auto wait_full = [&]() {
-            bar_wait(tfull0 + 8 * abuf, (aph >> abuf) & 1u);
+            if (PAIR) bar_wait_cluster(tfull0 + 8 * abuf, (aph >> abuf) & 1u);  // the leader's multicast commit
+            else bar_wait(tfull0 + 8 * abuf, (aph >> abuf) & 1u);
             tc_fence_after();
         };
+        const uint32_t lead_tempty0 = PAIR ? cluster_addr(tempty0, 0) : tempty0;
         auto release = [&]() {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) bar_arrive(tempty0 + 8 * abuf);
+            if (lane == 0) {
+                if (PAIR) bar_arrive_remote(lead_tempty0 + 8 * abuf);  // the leader issues the next MMAs
+                else bar_arrive(tempty0 + 8 * abuf);
+            }
             aph ^= 1u << abuf;
             abuf ^= 1;
         };
@@ -1112,9 +1225,16 @@ class TcEngine final : public PanelEngine {
         gen_cap_ = (int64_t)nsm_ * 8;
         rff_smem_ = RFF_SMEM;
         const int smem = smem_, rsmem = rff_smem_;
-        once_per_device((const void*)&k_gemm_tf32x3<false, false>, [smem, rsmem] {
-            for (auto f : {k_gemm_tf32x3<false, false>, k_gemm_tf32x3<false, true>, k_gemm_tf32x3<true, false>,
-                           k_gemm_tf32x3<true, true>}) {
+        // CTA pairs (cta_group::2) when the tile rows pair up (an even number of
+        // 128-row tiles; the rasterised / symmetric tile orders then put the two
+        // tiles of a pair at indices 2u, 2u + 1).  MLSK_TC_PAIR=0: single CTAs.
+        const char* pair_env = std::getenv("MLSK_TC_PAIR");
+        pair_ = (MP_ / TBM) % 2 == 0 && T_ % 2 == 0 && !(pair_env && std::strcmp(pair_env, "0") == 0);
+        once_per_device((const void*)&k_gemm_tf32x3<false, false, false>, [smem, rsmem] {
+            for (auto f : {k_gemm_tf32x3<false, false, false>, k_gemm_tf32x3<false, true, false>,
+                           k_gemm_tf32x3<true, false, false>, k_gemm_tf32x3<true, true, false>,
+                           k_gemm_tf32x3<false, false, true>, k_gemm_tf32x3<false, true, true>,
+                           k_gemm_tf32x3<true, false, true>, k_gemm_tf32x3<true, true, true>}) {
                 MLSK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
                 MLSK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
                 // setmaxnreg redistributes the launch's registers: the launch must
@@ -1197,8 +1317,8 @@ class TcEngine final : public PanelEngine {
             TcShape sh{1, k, MP_, PP_, T_, 2, tiles_n_, nullptr, M_.rows, M_.cols, 1, 0, 0, 0, 1.0f, seg_};
             {
                 Prof p("gemm_tf32x3", s);
-                (segmented(k - (k + 1) / 2) ? k_gemm_tf32x3<true, true> : k_gemm_tf32x3<true, false>)
-                    <<<2 * T_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq, 1, ws_.ypart.p);
+                launch_gemm(true, segmented(k - (k + 1) / 2), 2 * T_, s, Ahi, Alo, Bhi, Blo, sh, part, part_sq, 1,
+                            ws_.ypart.p);
             }
             {
                 Prof p("reduce_tiles_tc", s);
@@ -1222,11 +1342,9 @@ class TcEngine final : public PanelEngine {
         {
             Prof p("gemm_tf32x3", s);
             if (kr.part == 0)
-                (segmented(k) ? k_gemm_tf32x3<false, true> : k_gemm_tf32x3<false, false>)
-                    <<<T_ * Gs_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq, 0, nullptr);
+                launch_gemm(false, segmented(k), T_ * Gs_, s, Ahi, Alo, Bhi, Blo, sh, part, part_sq, 0, nullptr);
             else
-                (segmented(k) ? k_gemm_tf32x3<true, true> : k_gemm_tf32x3<true, false>)
-                    <<<T_ * Gs_, TC_THREADS, smem_, s>>>(Ahi, Alo, Bhi, Blo, sh, part, part_sq, kr.part, ypart);
+                launch_gemm(true, segmented(k), T_ * Gs_, s, Ahi, Alo, Bhi, Blo, sh, part, part_sq, kr.part, ypart);
         }
         if (!finishes) {
             launched();
@@ -1252,6 +1370,32 @@ class TcEngine final : public PanelEngine {
     }
 
    private:
+    using GemmFn = void (*)(const float*, const float*, const float*, const float*, TcShape, double*, double*, int,
+                            float*);
+    // the GEMM instantiation for (split, segmented, pair); pair launches as
+    // clusters of two CTAs
+    void launch_gemm(bool split, bool segm, int grid, cudaStream_t s, const float* Ahi, const float* Alo,
+                     const float* Bhi, const float* Blo, const TcShape& sh, double* part, double* part_sq, int split_part,
+                     float* ypart) const {
+        static const GemmFn fns[8] = {k_gemm_tf32x3<false, false, false>, k_gemm_tf32x3<false, true, false>,
+                                      k_gemm_tf32x3<true, false, false>,  k_gemm_tf32x3<true, true, false>,
+                                      k_gemm_tf32x3<false, false, true>,  k_gemm_tf32x3<false, true, true>,
+                                      k_gemm_tf32x3<true, false, true>,   k_gemm_tf32x3<true, true, true>};
+        const GemmFn f = fns[(pair_ ? 4 : 0) + (split ? 2 : 0) + (segm ? 1 : 0)];
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(TC_THREADS);
+        cfg.dynamicSmemBytes = (size_t)smem_;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = pair_ ? 2 : 1;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        MLSK_CUDA(cudaLaunchKernelEx(&cfg, f, Ahi, Alo, Bhi, Blo, sh, part, part_sq, split_part, ypart));
+    }
     static int64_t nkc(int64_t c) { return (c + TBK - 1) / TBK; }
     // a CTA K-range of `k` chunks (at least) runs as several TMEM segments
     bool segmented(int64_t k) const { return seg_ > 0 && k > seg_; }
@@ -1280,6 +1424,7 @@ class TcEngine final : public PanelEngine {
     TcModel S_{};
     int nsm_, T_, Gs_, tiles_n_, smem_, rff_smem_;
     int sym_nb_ = 0;  // symmetric output: 256-blocks per side (0 = full tile grid)
+    bool pair_ = false;  // CTA-pair GEMM (cta_group::2)
     int seg_ = TC_SEG;
     bool shared_env_ = true;
     int64_t gen_cap_;
