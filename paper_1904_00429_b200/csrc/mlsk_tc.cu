@@ -37,7 +37,7 @@
 //                     (tm, tn), (tm + 1, tn): the leader issues
 //                     tcgen05.mma.cta_group::2 (M = 256) over both CTAs' shared
 //                     memory, each CTA staging its A rows and half of the B
-//                     columns (32 KB stages, six of them) -- a third less
+//                     columns (32 KB stages, seven of them) -- a third less
 //                     shared-memory traffic per SM, 3-9% faster per level.
 //  k_reduce_tiles_tc  level total += the group partials (fixed order);
 //  k_kpar_combine     one-sample levels split over two CTA groups along K;
@@ -69,10 +69,13 @@ constexpr int TSTAGE_BYTES = 2 * TA_BYTES + 2 * TB_BYTES;  // A_hi, A_lo, B_hi, 
 constexpr int EPI_WARPS = 16;                       // four per TMEM lane quadrant (64-column quarters)
 // CTA pair (cta_group::2, M = 256 over two SMs of a TPC): each CTA stages its
 // own 128 A rows and HALF of the 256 B columns, 32 KB per stage, six stages
-constexpr int PSTAGES = 6;
+#ifndef MLSK_TC_PSTAGES
+#define MLSK_TC_PSTAGES 7  // 224 KB: measured 1.5% faster than 6 at config 3, configs 4 / 5 unchanged
+#endif
+constexpr int PSTAGES = MLSK_TC_PSTAGES;
 constexpr int PB_BYTES = TTILE;                             // half a B tile (128 columns)
 constexpr int PSTAGE_BYTES = 2 * TA_BYTES + 2 * PB_BYTES;  // 32 KB
-static_assert(PSTAGES * PSTAGE_BYTES <= TSTAGES * TSTAGE_BYTES, "pair ring must fit the single ring's smem");
+static_assert(PSTAGES * PSTAGE_BYTES + 1024 <= 226 * 1024, "pair ring exceeds the shared memory of a CTA");
 // warpgroup 0: producer (warp 0), TMEM allocation + MMA issue (warp 1), two
 // idle warps; warpgroups 1-4: epilogue.  setmaxnreg moves registers from the
 // control warpgroup to the epilogue (24 / 112 per thread) for its 64-entry
@@ -1224,7 +1227,7 @@ class TcEngine final : public PanelEngine {
         const char* seg_env = std::getenv("MLSK_TC_SEG");
         seg_ = seg_env ? std::max(0, atoi(seg_env)) : TC_SEG;
         S_.M = M.dm;
-        smem_ = TSTAGES * TSTAGE_BYTES + 1024;
+        smem_ = std::max(TSTAGES * TSTAGE_BYTES, PSTAGES * PSTAGE_BYTES) + 1024;
         ws_.partial.ensure((size_t)T_ * Gs_ * (TBM * TBN) + (size_t)T_ * Gs_);
         // generator grid cap (CTAs; grid-stride beyond it).  MLSK_TC_GEN_CTAS_PER_SM
         // (experiments): 0 = one work item per CTA
