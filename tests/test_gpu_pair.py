@@ -1,0 +1,66 @@
+"""The CTA-pair tcgen05 GEMM (cta_group::2, M = 256 over two SMs) against the
+single-CTA GEMM (MLSK_TC_PAIR=0) on the same draws: every output element is
+the same K-ordered chain of tf32 MMAs into an fp32 accumulator whichever SM
+pair computes its tile, so the level sums must agree bit for bit -- at the
+BASELINE configs' full shapes (config 3, the symmetric config-4 Gram, config
+5) and on the K-split and K-parallel paths."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+MASTER = 20260823
+
+
+def run(g, model, plan, env, opts=None):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return g.mlmc_matmul(model, g.target_identity(), plan, MASTER, opts or g.EstimatorOptions(engine="fused"))
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def same(a, b):
+    for sa, sb in zip(a.per_level, b.per_level):
+        assert sa.replication_count == sb.replication_count
+        assert np.array_equal(np.asarray(sa.sum), np.asarray(sb.sum)), sa.level
+        assert sa.sum_of_squares == sb.sum_of_squares, sa.level
+
+
+def ds(g, c):
+    return g.RngStream.derive_seed(MASTER, 0xD47A0000 + c, 0)
+
+
+@pytest.mark.parametrize("case", ["config3", "config4_sym", "config5", "ksplit", "kpar", "odd_rows"])
+def test_pair_equals_single_cta(gpu, case):
+    g = gpu
+    env = {}
+    if case == "config3":
+        model = g.gaussian_mean_matrix_model(1024, 16384, 1024, sd=1.0, data_seed=ds(g, 3), dtype=1)
+        plan = g.LevelPlan(2, 1, [6, 3], c0=64)
+    elif case == "config4_sym":
+        model = g.rff_gram_model(4096, 2 ** 16, dim=64, sigma=4.0, data_seed=ds(g, 4))
+        plan = g.LevelPlan(2, 1, [3, 2], c0=128)
+    elif case == "config5":
+        model = g.student_t_matrix_model(8192, 2 ** 20, 8192, data_seed=ds(g, 5))
+        plan = g.LevelPlan(2, 0, [2], c0=256)
+    elif case == "ksplit":  # samples split along K (forced 1 MiB batches)
+        model = g.gaussian_mean_matrix_model(512, 4096, 512, sd=1.0, data_seed=7, dtype=1)
+        plan = g.LevelPlan(2, 1, [2, 2], c0=512)
+        env = {"MLSK_SPLIT_MB": "1"}
+    elif case == "kpar":  # one sample over the full 512-tile grid: K split over two CTA groups
+        model = g.rff_gram_model(4096, 2 ** 16, dim=64, sigma=4.0, data_seed=ds(g, 4))
+        plan = g.LevelPlan(2, 0, [1], c0=512)
+        env = {"MLSK_TC_SYM": "0"}
+    else:  # an odd number of 128-row tiles: both settings run single CTAs
+        model = g.gaussian_mean_matrix_model(384, 2048, 256, sd=1.0, data_seed=9, dtype=1)
+        plan = g.LevelPlan(2, 1, [5, 3], c0=64)
+    pair = run(g, model, plan, dict(env))
+    single = run(g, model, plan, dict(env, MLSK_TC_PAIR="0"))
+    same(pair, single)
