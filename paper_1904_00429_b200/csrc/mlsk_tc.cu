@@ -682,11 +682,15 @@ struct TcShape {
 
 // tile index -> (tile row of 128, tile column of 256).  Full grids run in
 // groups of RASTER_G tile rows, column by column inside a group: the CTAs
-// resident at one time (148 of config 5's 2048 tiles) then cover about 16 x 9
+// resident at one time (148 of config 5's 2048 tiles) then cover about 8 x 18
 // tiles instead of 4.6 rows x all 32 columns, so the panel chunks they share
 // come from L2 and not once per wave from DRAM (config 5 at c = 512: 2.6 GB
-// of DRAM reads per launch for 268 MB of panels).
-constexpr int RASTER_G = 16;
+// of DRAM reads per launch for 268 MB of panels before).  The group height
+// must stay even (CTA pairs take tile rows 2u, 2u + 1).
+#ifndef MLSK_TC_RASTER_G
+#define MLSK_TC_RASTER_G 8  // config 5 (pairs): 4 / 8 / 16 / 32 rows: 382 / 369 / 381 / 400 ms per step
+#endif
+constexpr int RASTER_G = MLSK_TC_RASTER_G;
 __device__ __forceinline__ void tile_coords(const TcShape& sh, int tile, int& tm, int& tn) {
     if (sh.sym_nb == 0) {
         const int rows_t = sh.T / sh.tiles_n;
