@@ -726,6 +726,7 @@ struct InnerPart {
     int64_t nb;
     int64_t task_off;  // first warp task
     int64_t k0;        // >= 0: the part's replications are k0, k0 + 1, ... (no index list read)
+    uint64_t key_prefix;  // derive_prefix(seed, tag): one mix per replication instead of three
     int g;             // threads per replication (power of two <= INNER_G)
     double* total;
     double* total_sq;
@@ -775,7 +776,7 @@ k_fused_inner_multi(DevModel M, uint64_t seed, const int64_t* __restrict__ ks, I
         double acc = 0.0, pre = 0.0;
         if (live) {
             const int64_t k = q.k0 >= 0 ? q.k0 + b : ks[q.ks_off + b];
-            const uint64_t key = derive_seed(seed, q.tag, (uint64_t)k);
+            const uint64_t key = derive_from_prefix(q.key_prefix, (uint64_t)k);  // = derive_seed(seed, tag, k)
             for (int64_t tp = gl; 2 * tp < q.c; tp += g) {
                 const u32x4 ri = philox((uint32_t)tp, 0, 0, MLSK_CTR_INDEX, key);
 #pragma unroll
@@ -813,7 +814,10 @@ k_fused_inner_multi(DevModel M, uint64_t seed, const int64_t* __restrict__ ks, I
 // replications; the last block of a part to finish adds the INNER_RB partials
 // in block order (fixed order: bit-identical reruns).  One block per part
 // (the previous form) serialised 0.5 M replications of level 0 on one SM.
-constexpr int INNER_RB = 64;
+#ifndef MLSK_INNER_RB
+#define MLSK_INNER_RB 64
+#endif
+constexpr int INNER_RB = MLSK_INNER_RB;
 __global__ void __launch_bounds__(256)
 k_reduce_inner_multi(const double* __restrict__ y, InnerParts P, double* __restrict__ part,
                      unsigned* __restrict__ done) {
@@ -1229,9 +1233,13 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
                         k0 = r.k0 + (pos - r.dst);
                         break;
                     }
-                parts.p[parts.n++] = InnerPart{job.lv.tag, c,    cc,          w_fine, w_coarse,        job_off[j] + off,
-                                               filled,     take, parts.tasks, k0,     g,               job.st->total(),
-                                               job.st->total_sq()};
+                parts.p[parts.n++] = InnerPart{job.lv.tag, c,
+                                               cc,         w_fine,
+                                               w_coarse,   job_off[j] + off,
+                                               filled,     take,
+                                               parts.tasks, k0,
+                                               derive_prefix(a.seed, job.lv.tag), g,
+                                               job.st->total(), job.st->total_sq()};
                 parts.tasks += (take * g + 31) / 32;
                 filled += take;
                 off += take;
