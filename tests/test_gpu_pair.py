@@ -64,3 +64,27 @@ def test_pair_equals_single_cta(gpu, case):
     pair = run(g, model, plan, dict(env))
     single = run(g, model, plan, dict(env, MLSK_TC_PAIR="0"))
     same(pair, single)
+
+
+def test_pair_random_shapes_vs_single_and_exact(gpu):
+    """Seeded random shapes (m, p not multiples of the tile, c not a multiple
+    of the K-chunk, several samples per CTA group): pair == single bit for bit,
+    and both within the fp32 tolerance of the exact fp64-order engine."""
+    g = gpu
+    rng = np.random.default_rng(20261021)
+    for _ in range(8):
+        m = int(rng.integers(1, 9)) * 128 - int(rng.integers(0, 40))
+        p = int(rng.integers(1, 5)) * 256 - int(rng.integers(0, 60))
+        n = 1 << int(rng.integers(9, 13))
+        c0 = int(rng.integers(3, 40))
+        N = [int(rng.integers(1, 7)), int(rng.integers(1, 5))]
+        model = g.gaussian_mean_matrix_model(m, n, p, sd=1.0, data_seed=int(rng.integers(1, 1 << 30)), dtype=1)
+        plan = g.LevelPlan(2, 1, N, c0=c0)
+        pair = run(g, model, plan, {})
+        single = run(g, model, plan, {"MLSK_TC_PAIR": "0"})
+        same(pair, single)
+        ex = run(g, model, plan, {}, g.EstimatorOptions(engine="exact"))
+        for sf, se in zip(pair.per_level, ex.per_level):
+            a = np.asarray(sf.sum, dtype=np.float64).ravel()
+            b = np.asarray(se.sum, dtype=np.float64).ravel()
+            assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b), (m, n, p, c0, N, sf.level)
