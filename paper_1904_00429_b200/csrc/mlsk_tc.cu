@@ -410,7 +410,13 @@ __device__ __forceinline__ void student_t_phase_f32(const TcModel& S, const Tabl
 // KIND: GK_GAUSS, GK_STUDENT_T, or GK_GENERIC (per-entry loop: RFF with D > 64)
 constexpr int GK_GAUSS = 0, GK_STUDENT_T = 1, GK_GENERIC = 2;
 template <int KIND>
-__global__ void __launch_bounds__(GEN_T, KIND == GK_GAUSS ? 5 : KIND == GK_STUDENT_T ? 3 : 1)
+#ifndef MLSK_GAUSS_MINB
+#define MLSK_GAUSS_MINB 5  // gauss: 4 / 5 / 6 CTAs per SM -> config 3 16.1 / 15.6 / 16.1 ms per step
+#endif
+#ifndef MLSK_ST_MINB
+#define MLSK_ST_MINB 2  // Student-t: 2 / 3 / 4 CTAs per SM -> config 5 367 / 370 / 381 ms per step
+#endif
+__global__ void __launch_bounds__(GEN_T, KIND == GK_GAUSS ? MLSK_GAUSS_MINB : KIND == GK_STUDENT_T ? MLSK_ST_MINB : 1)
 k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
                   int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kc0,
                   float* __restrict__ Ahi, float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
