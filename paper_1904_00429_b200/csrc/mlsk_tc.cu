@@ -514,7 +514,10 @@ constexpr int RFF_RSPLIT = 4;              // work items per column group (row-b
 // 256 threads over 128-row X tiles (a 128-thread / 64-row variant small
 // enough to sit beside a GEMM CTA was measured neutral in round 1: sharing the
 // SM trades GEMM time for generator time one for one)
-constexpr int RFF_T = GEN_T, RFF_RB = TBM, RFF_MINB = 1;
+#ifndef MLSK_RFF_MINB
+#define MLSK_RFF_MINB 3  // 79 registers, 3 CTAs per SM: config 4 16.70 -> 16.37 ms per step (4: 16.70)
+#endif
+constexpr int RFF_T = GEN_T, RFF_RB = TBM, RFF_MINB = MLSK_RFF_MINB;
 constexpr int RFF_SMEM = (RFF_DMAX * RFF_RB + RFF_DMAX * RFF_COLS) * 4;  // X tile + W columns (40 KB)
 
 // work item (b, column group of 32 sampled columns, range of 128-row blocks):
