@@ -1228,11 +1228,13 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
                 // contiguous replications (one run covers the part): k = k0 + b
                 int64_t k0 = -1;
                 const int64_t pos = job_off[j] + off;
-                for (const KsRun& r : runs)
-                    if (r.dst <= pos && pos + take <= r.dst + r.count) {
-                        k0 = r.k0 + (pos - r.dst);
-                        break;
-                    }
+                // the run holding pos (runs are sorted by dst; one per owned chunk when sharded)
+                auto rit = std::upper_bound(runs.begin(), runs.end(), pos,
+                                            [](int64_t v, const KsRun& r) { return v < r.dst; });
+                if (rit != runs.begin()) {
+                    const KsRun& r = *(rit - 1);
+                    if (r.dst <= pos && pos + take <= r.dst + r.count) k0 = r.k0 + (pos - r.dst);
+                }
                 parts.p[parts.n++] = InnerPart{job.lv.tag, c,
                                                cc,         w_fine,
                                                w_coarse,   job_off[j] + off,

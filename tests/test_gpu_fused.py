@@ -96,6 +96,23 @@ def test_rank_sharding_sums(gpu):
         assert parts[0].per_level[l].replication_count + parts[1].per_level[l].replication_count == plan.N[l]
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_inner_rank_sharding_sums(gpu, world):
+    """Config-1 shape (one launch for all levels, replication lists from
+    per-chunk runs when sharded): the shards' level sums add up to the
+    unsharded run, counts exactly."""
+    model = gpu.gaussian_mean_model(4096, sd=1.0, data_seed=gpu.RngStream.derive_seed(MASTER, 0xD47A0001, 0))
+    plan = gpu.LevelPlan(2, 3, [1000, 700, 300, 130], c0=8)
+    opts = gpu.EstimatorOptions(engine="fused")
+    full = gpu.mlmc_inner(model, gpu.target_identity(), plan, MASTER, opts)
+    parts = [gpu.mlmc_inner(model, gpu.target_identity(), plan, MASTER,
+                            gpu.EstimatorOptions(engine="fused", rank=r, world=world)) for r in range(world)]
+    for l in range(4):
+        s = sum(p.per_level[l].sum for p in parts)
+        assert abs(s - full.per_level[l].sum) <= 1e-13 * abs(full.per_level[l].sum)
+        assert sum(p.per_level[l].replication_count for p in parts) == plan.N[l]
+
+
 def test_session_rounds_equal_single_run(gpu):
     model = config2_model(gpu, 128, 4096, 64)
     sess = gpu.MlmcSession(model, gpu.target_identity(), 2, 2, MASTER, c0=32)
