@@ -71,6 +71,31 @@ def alg_flops(cid, c, levels_c):
     return sum(2.0 * c["m"] * c["p"] * cl * n for cl, n in zip(levels_c, c["N"]))
 
 
+TRAFFIC_JSON = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "tc_traffic.json")
+
+
+def attach_traffic(cid, blk):
+    """roofline.traffic (DRAM bytes per launch of the dominant kernel) and the
+    step's DRAM bytes against its algorithmic bytes, from the ncu pass
+    tools/traffic_probe.py committed under profiles/ (same step, same kernels)."""
+    try:
+        import json as _json
+        t = _json.load(open(TRAFFIC_JSON))[str(cid)]
+    except (OSError, KeyError, ValueError):
+        return
+    kname = "k_fused_inner_multi" if cid == 1 else "k_gemm_tf32x3"
+    k = t["kernels"].get(kname)
+    if k and "roofline" in blk:
+        blk["roofline"]["traffic"] = k["dram_bytes_per_launch"]
+        blk["roofline"]["traffic_source"] = t["source"]
+    blk["step_traffic"] = {"dram_bytes_per_step": t["dram_bytes_per_step"],
+                           "algorithmic_bytes_per_step": t["algorithmic_bytes_per_step"], "ratio": t["ratio"],
+                           "per_kernel_dram_bytes_per_step": {
+                               n: v["dram_bytes_per_launch"] * v["launches_per_step"]
+                               for n, v in t["kernels"].items()},
+                           "source": t["source"]}
+
+
 def profile_read(L):
     name = C.create_string_buffer(64)
     nl, ms = C.c_int64(), C.c_double()
@@ -254,6 +279,7 @@ def measure(ids, steps=3, with_cpu=True, device=0):
                                               f"({peak_t:.0f} TFLOP/s) / 3",
                                "algorithmic": ("P(P+1) c + 2 P D c flops per level-sample (SYRK + features)"
                                                if cid == 4 else "2 m p c flops per level-sample")}
+        attach_traffic(cid, blk)
         if with_cpu:
             blk["cpu_baseline"] = cpu_baseline(cid, c, levels_c)
         out[str(cid)] = blk
