@@ -173,7 +173,8 @@ __device__ __forceinline__ void gen_phase(const DevModel& M, const Tables& T, ui
 __global__ void __launch_bounds__(GEN_THREADS, 4)
 k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
                  int64_t cc, double w_fine, double w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kc0,
-                 double* __restrict__ Apan, double* __restrict__ Bpan, uint32_t* __restrict__ idx_out, int64_t pcc) {
+                 double* __restrict__ Apan, double* __restrict__ Bpan, uint32_t* __restrict__ idx_out, int64_t pcc,
+                 const MkEntry* __restrict__ mk, int64_t mk_stride, const MkInfo* __restrict__ mk_info) {
     // pcc >= cc: K slots [0, pcc) hold the coarse prefix t < cc (zero padding
     // up to pcc), slots [pcc, ...) the suffix t >= cc.  pcc = cc (identity
     // target) is the plain layout; a nonlinear target pads the prefix to whole
@@ -201,7 +202,16 @@ k_gen_panels_f64(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restr
             const int64_t t = sl < pcc ? sl : sl - pcc + cc;  // column of the sample
             int j = 0;  // padding slots: column 0 with weight 0
             double w = 0.0;
-            if (sl < pcc ? t < cc : t < c) {
+            if (mk) {
+                // merged sampled columns: slot sl of the sample's (j, W_j) list
+                if (sl < mk_info[b].len) {
+                    const MkEntry e = mk[(int64_t)b * mk_stride + sl];
+                    if (e.j >= 0) {
+                        j = e.j;
+                        w = e.w;
+                    }
+                }
+            } else if (sl < pcc ? t < cc : t < c) {
                 const u32x4 r = philox((uint32_t)(t >> 1), 0, 0, MLSK_CTR_INDEX, key);
                 const uint32_t ix = index_from_u64((t & 1) ? hi64(r) : lo64(r), M.n, M.log2n, M.cum);
                 j = (int)(ix - 1);
@@ -953,7 +963,8 @@ class F64Engine final : public PanelEngine {
         double* Bpan = Apan + (size_t)nb * k * MP_ * KC;
         Prof p("gen_panels_f64", s);
         k_gen_panels_f64<<<(int)std::min<int64_t>((int64_t)nb * k, (int64_t)gen_ctas_), GEN_THREADS, GEN_DYN_SMEM, s>>>(
-            M_.dm, seed, tag, ks, nb, c, cc, w_fine, w_coarse, MP_, PP_, k, kr.kc0, Apan, Bpan, idx, pcc(cc));
+            M_.dm, seed, tag, ks, nb, c, cc, w_fine, w_coarse, MP_, PP_, k, kr.kc0, Apan, Bpan, idx, pcc(cc), kr.mk,
+            kr.mk_stride, kr.mk_info);
         launched();
     }
     void gemm(cudaStream_t s, const void* panels, int nb, int64_t c, int64_t cc, double, double, LevelState& st,
@@ -1000,6 +1011,9 @@ class F64Engine final : public PanelEngine {
         launched(2);
     }
 
+    // merged sampled columns: summed weights folded into B (identity target)
+    int merge_mode(int64_t, int64_t, double, double) const override { return nl_ ? 0 : 1; }
+
     // nonlinear targets: the coarse prefix padded to whole K-chunks
     int64_t nchunks(int64_t c, int64_t cc) const override {
         return nl_ ? (cc + KC - 1) / KC + (c - cc + KC - 1) / KC : (c + KC - 1) / KC;
@@ -1037,6 +1051,214 @@ __global__ void k_expand_ks(const KsRun* __restrict__ runs, int nruns, int64_t t
     }
 }
 
+// ------------------------------------------- merged sampled columns pre-pass
+//
+// (KRange, mlsk_internal.h.)  k_mk_count draws every index of a group of
+// samples and counts, per sample and column j, how often j falls in the coarse
+// prefix (high word) and in the suffix (low word): integer atomics, so the
+// counts -- and everything derived from them -- are the same in every run.
+// k_mk_tiles / k_mk_scan / k_mk_write turn a sample's counts into its list,
+// ordered by j (tiles of 4096 columns: counts, exclusive scan, ordered writes):
+//   mode 1: one entry per column with W_j = cnt_f w_fine + cnt_c w_coarse != 0;
+//   mode 2: columns with cnt_f != cnt_c repeated |cnt_f - cnt_c| times, the
+//           negative ones (cnt_f < cnt_c) first, padded to whole K-chunks.
+// The write pass clears the counts it read; the scan raises the job's maximum
+// chunk count, which the host reads once per round to size the launches.
+constexpr int MK_T = 256, MK_ITEMS = 16, MK_TILE = MK_T * MK_ITEMS;
+constexpr int MK_MAX_JOBS = 64;  // merged levels per round
+
+__global__ void __launch_bounds__(256)
+k_mk_count(DevModel M, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int64_t nb, int64_t c, int64_t cc,
+           unsigned long long* __restrict__ cnt) {
+    const int64_t hp = (c + 1) / 2;  // index pairs per sample (one Philox block each)
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nb * hp;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = e / hp, tp = e - b * hp;
+        const uint64_t key = derive_seed(seed, tag, (uint64_t)ks[b]);
+        const u32x4 r = philox((uint32_t)tp, 0, 0, MLSK_CTR_INDEX, key);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t t = 2 * tp + h;
+            if (t < c) {
+                const uint32_t ix = index_from_u64(h ? hi64(r) : lo64(r), M.n, M.log2n, M.cum);
+                atomicAdd(cnt + b * M.n + (ix - 1), t < cc ? (1ull << 32) : 1ull);
+            }
+        }
+    }
+}
+
+// entries column j contributes and whether they belong to the negative group
+__device__ __forceinline__ int mk_entries(unsigned long long v, int mode, double w_fine, double w_coarse, bool& neg) {
+    const int64_t cf = (int64_t)(v & 0xffffffffull), ccn = (int64_t)(v >> 32);
+    neg = false;
+    if (v == 0) return 0;
+    if (mode == 2) {  // |w_coarse| == |w_fine|, w_coarse < 0 (shared_panel)
+        neg = cf < ccn;
+        return (int)(cf > ccn ? cf - ccn : ccn - cf);
+    }
+    if (w_coarse == -w_fine) return cf != ccn ? 1 : 0;  // exact cancellation (M = 2)
+    return __fma_rn((double)cf, w_fine, __dmul_rn((double)ccn, w_coarse)) != 0.0 ? 1 : 0;
+}
+
+// (neg, pos) entry counts of this thread's MK_ITEMS consecutive columns
+__device__ __forceinline__ void mk_thread_counts(const unsigned long long* __restrict__ my, int64_t n, int64_t j0,
+                                                 int mode, double w_fine, double w_coarse,
+                                                 unsigned long long (&v)[MK_ITEMS], int (&en)[MK_ITEMS],
+                                                 bool (&ng)[MK_ITEMS], int& tn, int& tp) {
+    tn = tp = 0;
+    if (j0 + MK_ITEMS <= n) {
+#pragma unroll
+        for (int i = 0; i < MK_ITEMS; i += 2) {
+            const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(my + j0 + i);
+            v[i] = q.x;
+            v[i + 1] = q.y;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < MK_ITEMS; ++i) v[i] = j0 + i < n ? my[j0 + i] : 0ull;
+    }
+#pragma unroll
+    for (int i = 0; i < MK_ITEMS; ++i) {
+        en[i] = mk_entries(v[i], mode, w_fine, w_coarse, ng[i]);
+        if (ng[i]) tn += en[i];
+        else tp += en[i];
+    }
+}
+
+// per (tile of MK_TILE columns, sample): entry counts of the tile
+__global__ void __launch_bounds__(MK_T)
+k_mk_tiles(const unsigned long long* __restrict__ cnt, int64_t n, int mode, double w_fine, double w_coarse,
+           int2* __restrict__ tile_cnt) {
+    __shared__ int s_neg[MK_T / 32], s_pos[MK_T / 32];
+    const int tile = blockIdx.x, b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned long long v[MK_ITEMS];
+    int en[MK_ITEMS];
+    bool ng[MK_ITEMS];
+    int tn, tp;
+    mk_thread_counts(cnt + (int64_t)b * n, n, (int64_t)tile * MK_TILE + (int64_t)tid * MK_ITEMS, mode, w_fine,
+                     w_coarse, v, en, ng, tn, tp);
+    for (int o = 16; o > 0; o >>= 1) {
+        tn += __shfl_xor_sync(0xffffffffu, tn, o);
+        tp += __shfl_xor_sync(0xffffffffu, tp, o);
+    }
+    if (lane == 0) {
+        s_neg[warp] = tn;
+        s_pos[warp] = tp;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int a = 0, q = 0;
+        for (int w = 0; w < MK_T / 32; ++w) {
+            a += s_neg[w];
+            q += s_pos[w];
+        }
+        tile_cnt[(int64_t)b * gridDim.x + tile] = make_int2(a, q);
+    }
+}
+
+// per sample: exclusive scan of its tiles' counts (in place), its (len, neg_kc),
+// the padding of the negative group and the job's maximum chunk count
+__global__ void __launch_bounds__(MK_T)
+k_mk_scan(int2* __restrict__ tile_cnt, int tiles, int kcols, MkEntry* __restrict__ list, int64_t stride,
+          MkInfo* __restrict__ info, int32_t* __restrict__ job_max) {
+    __shared__ int s_neg[MK_T / 32], s_pos[MK_T / 32];
+    const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int2* my = tile_cnt + (int64_t)b * tiles;
+    int base_n = 0, base_p = 0;
+    for (int t0 = 0; t0 < tiles; t0 += MK_T) {
+        const int t = t0 + tid;
+        const int2 cv = t < tiles ? my[t] : make_int2(0, 0);
+        int xn = cv.x, xp = cv.y;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int yn = __shfl_up_sync(0xffffffffu, xn, o), yp = __shfl_up_sync(0xffffffffu, xp, o);
+            if (lane >= o) {
+                xn += yn;
+                xp += yp;
+            }
+        }
+        __syncthreads();
+        if (lane == 31) {
+            s_neg[warp] = xn;
+            s_pos[warp] = xp;
+        }
+        __syncthreads();
+        int wn = 0, wp = 0, alln = 0, allp = 0;
+        for (int w = 0; w < MK_T / 32; ++w) {
+            if (w < warp) {
+                wn += s_neg[w];
+                wp += s_pos[w];
+            }
+            alln += s_neg[w];
+            allp += s_pos[w];
+        }
+        if (t < tiles) my[t] = make_int2(base_n + wn + xn - cv.x, base_p + wp + xp - cv.y);
+        base_n += alln;
+        base_p += allp;
+    }
+    const int negpad = (base_n + kcols - 1) / kcols * kcols;
+    const int len = negpad + base_p;
+    MLSK_DCHECK((int64_t)len <= stride);
+    if (tid == 0) {
+        info[b] = MkInfo{len, negpad / kcols};
+        atomicMax(job_max, (len + kcols - 1) / kcols);
+    }
+    MkEntry* out = list + (int64_t)b * stride;
+    for (int q = base_n + tid; q < negpad; q += MK_T) out[q] = MkEntry{-1, 0, 0.0};
+}
+
+// per (tile, sample): the tile's entries, ordered by column, at their offsets;
+// the counts it read are cleared for the next group
+__global__ void __launch_bounds__(MK_T)
+k_mk_write(unsigned long long* __restrict__ cnt, int64_t n, int mode, double w_fine, double w_coarse, int kcols,
+           const int2* __restrict__ tile_off, const MkInfo* __restrict__ info, MkEntry* __restrict__ list,
+           int64_t stride) {
+    __shared__ int s_neg[MK_T / 32], s_pos[MK_T / 32];
+    const int tile = blockIdx.x, b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned long long* my = cnt + (int64_t)b * n;
+    MkEntry* out = list + (int64_t)b * stride;
+    const int64_t j0 = (int64_t)tile * MK_TILE + (int64_t)tid * MK_ITEMS;
+    unsigned long long v[MK_ITEMS];
+    int en[MK_ITEMS];
+    bool ng[MK_ITEMS];
+    int tn, tp;
+    mk_thread_counts(my, n, j0, mode, w_fine, w_coarse, v, en, ng, tn, tp);
+#pragma unroll
+    for (int i = 0; i < MK_ITEMS; ++i)
+        if (v[i]) my[j0 + i] = 0ull;
+    int xn = tn, xp = tp;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int yn = __shfl_up_sync(0xffffffffu, xn, o), yp = __shfl_up_sync(0xffffffffu, xp, o);
+        if (lane >= o) {
+            xn += yn;
+            xp += yp;
+        }
+    }
+    if (lane == 31) {
+        s_neg[warp] = xn;
+        s_pos[warp] = xp;
+    }
+    __syncthreads();
+    int wn = 0, wp = 0;
+    for (int w = 0; w < warp; ++w) {
+        wn += s_neg[w];
+        wp += s_pos[w];
+    }
+    const int2 off = tile_off[(int64_t)b * gridDim.x + tile];
+    int on = off.x + wn + xn - tn, op = info[b].neg_kc * kcols + off.y + wp + xp - tp;
+#pragma unroll
+    for (int i = 0; i < MK_ITEMS; ++i) {
+        if (en[i] == 0) continue;
+        const int64_t cf = (int64_t)(v[i] & 0xffffffffull), ccn = (int64_t)(v[i] >> 32);
+        MkEntry e;
+        e.j = (int32_t)(j0 + i);
+        e.reps = (int32_t)(cf > ccn ? cf - ccn : ccn - cf);
+        e.w = mode == 2 ? (ng[i] ? w_coarse : w_fine)
+                        : __fma_rn((double)cf, w_fine, __dmul_rn((double)ccn, w_coarse));
+        int& o = ng[i] ? on : op;
+        for (int r = 0; r < en[i]; ++r) out[o++] = e;
+    }
+}
+
 constexpr int NBUF = 3;  // panel buffers in flight (gen i+1, i+2 while GEMM i)
 
 // Engine-private pipeline state kept in the Workspace across rounds.
@@ -1055,6 +1277,15 @@ struct Pipe {
     DevArray<double> red_part;    // k_reduce_inner_multi: per-block partials
     DevArray<unsigned> red_done;  // per-part finished-block counters (self-resetting)
     bool staged_pending = false;
+    // merged sampled columns (pre-pass state)
+    DevArray<unsigned long long> mk_cnt;  // [group sample][n] packed counts, all zero between uses
+    DevArray<int2> mk_tile;               // [group sample][tile] entry counts, then offsets
+    DevArray<MkEntry> mk_list;
+    DevArray<MkInfo> mk_info;
+    DevArray<int32_t> mk_max;             // per merged job: maximum K-chunks over its samples
+    int32_t* mk_max_host = nullptr;       // pinned
+    cudaEvent_t mk_done = nullptr;
+    bool ran = false;                     // a round's end event has been recorded
 
     void ensure_inner_red() {
         if (red_done.p) return;
@@ -1071,6 +1302,8 @@ struct Pipe {
         MLSK_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
         MLSK_CUDA(cudaEventCreateWithFlags(&end, cudaEventDisableTiming));
         MLSK_CUDA(cudaEventCreateWithFlags(&staged, cudaEventDisableTiming));
+        MLSK_CUDA(cudaEventCreateWithFlags(&mk_done, cudaEventDisableTiming));
+        MLSK_CUDA(cudaMallocHost(&mk_max_host, MK_MAX_JOBS * sizeof(int32_t)));
         for (int i = 0; i < NBUF; ++i) {
             MLSK_CUDA(cudaEventCreateWithFlags(&gen_done[i], cudaEventDisableTiming));
             MLSK_CUDA(cudaEventCreateWithFlags(&mm_done[i], cudaEventDisableTiming));
@@ -1086,6 +1319,8 @@ struct Pipe {
         cudaEventDestroy(start);
         cudaEventDestroy(end);
         cudaEventDestroy(staged);
+        cudaEventDestroy(mk_done);
+        if (mk_max_host) cudaFreeHost(mk_max_host);
         if (runs_host) cudaFreeHost(runs_host);
         if (s_gen) cudaStreamDestroy(s_gen);
         if (s_mm) cudaStreamDestroy(s_mm);
@@ -1135,6 +1370,28 @@ struct Batch {
     int64_t ks_off;  // into the round's device ks array
     KRange kr;       // K-chunk range (split samples)
 };
+
+// A level of the round that runs on merged sampled columns.
+struct MergeJob {
+    int mode;
+    int64_t stride;      // list entries per sample
+    size_t list_off;     // into Pipe::mk_list / mk_info (entries / samples)
+    size_t info_off;
+    int64_t nk;          // merged K-chunks (maximum over the job's samples), from the pre-pass
+};
+
+// MLSK_MERGE=0 turns merged sampled columns off; MLSK_MERGE_MIN_DEN=d merges
+// the levels with c >= n / d (default 16: at c = n / 16 about 4.5% of the
+// columns merge or cancel, below that the pre-pass is not worth its launches)
+// (read every round: tests switch them in-process)
+bool merge_enabled() {
+    const char* e = getenv("MLSK_MERGE");
+    return !(e && e[0] == '0');
+}
+int64_t merge_min_den() {
+    const char* e = getenv("MLSK_MERGE_MIN_DEN");
+    return e ? std::max<int64_t>(1, atoll(e)) : int64_t(16);
+}
 
 }  // namespace
 
@@ -1313,10 +1570,116 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
     if (const char* e = getenv("MLSK_SPLIT_MB"))  // tests: force K-split samples at small shapes
         split_limit = std::max<int64_t>(1, atoll(e)) << 20;
 
+    // ---- merged sampled columns: the pre-pass of every level that qualifies
+    // (deepest first, within a 1 GiB budget of list memory), then ONE host
+    // synchronisation for the merged chunk counts that size the launches
+    std::vector<int> mj_of(jobs.size(), -1);
+    std::vector<MergeJob> mjs;
+    if (!nl && merge_enabled()) {
+        const int64_t KCOLS = E.chunk_cols();
+        std::vector<size_t> order(jobs.size());
+        for (size_t j = 0; j < jobs.size(); ++j) order[j] = j;
+        std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return jobs[x].lv.c > jobs[y].lv.c; });
+        const size_t list_budget = (size_t(1) << 30) / sizeof(MkEntry);
+        size_t list_used = 0, info_used = 0;
+        for (size_t j : order) {
+            const int64_t c = jobs[j].lv.c, cc = jobs[j].lv.cc;
+            if (job_cnt[j] == 0 || jobs[j].probe_host || jobs[j].lv.full || c * merge_min_den() < M.desc.n ||
+                c < 4 * KCOLS || M.desc.n > (int64_t(1) << 31) - 2 || (int)mjs.size() == MK_MAX_JOBS)
+                continue;
+            const double w_fine = n / (double)c * kRescalePerturb;
+            const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;
+            const int mode = E.merge_mode(c, cc, w_fine, w_coarse);
+            if (!mode) continue;
+            const int64_t stride = (c + KCOLS - 1) / KCOLS * KCOLS + KCOLS;
+            const size_t need = (size_t)job_cnt[j] * (size_t)stride;
+            if (list_used + need > list_budget) continue;
+            mj_of[j] = (int)mjs.size();
+            mjs.push_back({mode, stride, list_used, info_used, 0});
+            list_used += need;
+            info_used += (size_t)job_cnt[j];
+        }
+        if (!mjs.empty()) {
+            if (P.ran) MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.end, 0));  // the last round's readers of the lists
+            P.mk_list.ensure(list_used);
+            P.mk_info.ensure(info_used);
+            P.mk_max.ensure(MK_MAX_JOBS);
+            MLSK_CUDA(cudaMemsetAsync(P.mk_max.p, 0, MK_MAX_JOBS * sizeof(int32_t), P.s_gen));
+            // count scratch: groups of samples within 256 MiB
+            int64_t cnt_mb = 256;
+            if (const char* e = getenv("MLSK_MERGE_GROUP_MB")) cnt_mb = std::max<int64_t>(1, atoll(e));  // tests
+            const int64_t mk_tiles = (M.desc.n + MK_TILE - 1) / MK_TILE;
+            // (a launch's grid.y: at most 65535 samples per group)
+            const int64_t grp_cap = std::min<int64_t>(65535, std::max<int64_t>(1, (cnt_mb << 20) / (8 * M.desc.n)));
+            int64_t max_grp = 0;
+            for (size_t j = 0; j < jobs.size(); ++j)
+                if (mj_of[j] >= 0) max_grp = std::max(max_grp, std::min(grp_cap, job_cnt[j]));
+            const size_t cnt_need = (size_t)max_grp * (size_t)M.desc.n;
+            if (cnt_need > P.mk_cnt.n) {
+                P.mk_cnt.ensure(cnt_need);
+                P.mk_cnt.zero(P.s_gen);
+            }
+            P.mk_tile.ensure((size_t)max_grp * (size_t)mk_tiles);
+            Prof p("merge_columns", P.s_gen);
+            for (size_t j = 0; j < jobs.size(); ++j) {
+                if (mj_of[j] < 0) continue;
+                const MergeJob& mj = mjs[mj_of[j]];
+                const int64_t c = jobs[j].lv.c, cc = jobs[j].lv.cc;
+                const double w_fine = n / (double)c * kRescalePerturb;
+                const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;
+                for (int64_t off = 0; off < job_cnt[j]; off += grp_cap) {
+                    const int64_t g = std::min(grp_cap, job_cnt[j] - off);
+                    const int64_t work = g * ((c + 1) / 2);
+                    k_mk_count<<<(int)std::min<int64_t>((work + 255) / 256, (int64_t)sms * 16), 256, 0, P.s_gen>>>(
+                        M.dm, a.seed, jobs[j].lv.tag, P.ks.p + job_off[j] + off, g, c, cc, P.mk_cnt.p);
+                    MkEntry* list = P.mk_list.p + mj.list_off + (size_t)off * mj.stride;
+                    MkInfo* info = P.mk_info.p + mj.info_off + off;
+                    const dim3 tg((unsigned)mk_tiles, (unsigned)g);
+                    k_mk_tiles<<<tg, MK_T, 0, P.s_gen>>>(P.mk_cnt.p, M.desc.n, mj.mode, w_fine, w_coarse, P.mk_tile.p);
+                    k_mk_scan<<<(int)g, MK_T, 0, P.s_gen>>>(P.mk_tile.p, (int)mk_tiles, (int)KCOLS, list, mj.stride,
+                                                           info, P.mk_max.p + mj_of[j]);
+                    k_mk_write<<<tg, MK_T, 0, P.s_gen>>>(P.mk_cnt.p, M.desc.n, mj.mode, w_fine, w_coarse, (int)KCOLS,
+                                                         P.mk_tile.p, info, list, mj.stride);
+                    launched(4);
+                }
+            }
+            MLSK_CUDA(cudaMemcpyAsync(P.mk_max_host, P.mk_max.p, mjs.size() * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                      P.s_gen));
+            MLSK_CUDA(cudaEventRecord(P.mk_done, P.s_gen));
+            MLSK_CUDA(cudaEventSynchronize(P.mk_done));
+            for (size_t q = 0; q < mjs.size(); ++q) mjs[q].nk = std::max<int64_t>(1, P.mk_max_host[q]);
+        }
+    }
+    auto job_chunks = [&](size_t j) {
+        return mj_of[j] >= 0 ? mjs[mj_of[j]].nk : E.nchunks(jobs[j].lv.c, jobs[j].lv.cc);
+    };
+    auto with_merge = [&](KRange kr, size_t j, int64_t off) {
+        if (mj_of[j] >= 0) {
+            const MergeJob& mj = mjs[mj_of[j]];
+            if (kr.nkc < 0) kr.nkc = mj.nk;
+            kr.mk = P.mk_list.p + mj.list_off + (size_t)off * mj.stride;
+            kr.mk_stride = mj.stride;
+            kr.mk_info = P.mk_info.p + mj.info_off + off;
+        }
+        return kr;
+    };
+
+    // panel bytes a batch of nb samples needs in its buffer.  Merged chunk
+    // counts vary a little from round to round (they follow the draws), and a
+    // buffer that grew with every new maximum would be reallocated for many
+    // rounds: merged batches reserve 3% + 64 MiB of headroom, capped at the
+    // unmerged size.
+    auto reserve_bytes = [&](size_t j, int64_t nb, int64_t chunks) {
+        const int64_t need = nb * chunks * E.chunk_bytes();
+        if (mj_of[j] < 0) return need;
+        const int64_t ub = nb * E.nchunks(jobs[j].lv.c, jobs[j].lv.cc) * E.chunk_bytes();
+        const int64_t q = int64_t(64) << 20;
+        return std::min(ub, (need + need / 32 + q - 1) / q * q);
+    };
     std::vector<Batch> batches;
     int64_t max_panel = 0;
     for (size_t j = 0; j < jobs.size(); ++j) {
-        const int64_t per = E.panel_bytes(jobs[j].lv.c, jobs[j].lv.cc);
+        const int64_t per = job_chunks(j) * E.chunk_bytes();
         const int64_t total = job_cnt[j];
         if (per > split_limit && E.splits_k()) {
             if (nl)
@@ -1326,7 +1689,7 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
             // the partial Y carried between them
             if (jobs[j].probe_host)
                 throw Error(MLSK_EINVAL, "probe: not available for level-samples split along K (panels > " + std::to_string(split_limit >> 20) + " MiB)");
-            const int64_t nk = (jobs[j].lv.c + E.chunk_cols() - 1) / E.chunk_cols();
+            const int64_t nk = job_chunks(j);
             const int64_t seg = std::max<int64_t>(1, split_limit / E.chunk_bytes());  // few, large segments
             for (int64_t off = 0; off < total; ++off)
                 for (int64_t k0 = 0; k0 < nk; k0 += seg) {
@@ -1334,8 +1697,8 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
                     kr.kc0 = k0;
                     kr.nkc = std::min(seg, nk - k0);
                     kr.part = nk <= seg ? 0 : (k0 == 0 ? 1 : (k0 + kr.nkc == nk ? 3 : 2));
-                    batches.push_back({j, off, 1, job_off[j] + off, kr});
-                    max_panel = std::max(max_panel, kr.nkc * E.chunk_bytes());
+                    batches.push_back({j, off, 1, job_off[j] + off, with_merge(kr, j, off)});
+                    max_panel = std::max(max_panel, reserve_bytes(j, 1, kr.nkc));
                 }
             continue;
         }
@@ -1346,8 +1709,8 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         if (max_nb > Gs) max_nb = max_nb / Gs * Gs;
         for (int64_t off = 0; off < total; off += max_nb) {
             const int nb = (int)std::min<int64_t>(max_nb, total - off);
-            batches.push_back({j, off, nb, job_off[j] + off, KRange{}});
-            max_panel = std::max(max_panel, nb * per);
+            batches.push_back({j, off, nb, job_off[j] + off, with_merge(KRange{}, j, off)});
+            max_panel = std::max(max_panel, reserve_bytes(j, nb, job_chunks(j)));
         }
     }
     if ((size_t)(max_panel + 7) / 8 > P.panels[0].n) {
@@ -1405,6 +1768,7 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         job.st->count += cnt;
     }
     MLSK_CUDA(cudaEventRecord(P.end, P.s_mm));
+    P.ran = true;
     MLSK_CUDA(cudaStreamWaitEvent(a.stream, P.end, 0));
 }
 

@@ -257,9 +257,34 @@ struct FusedJob {
 // all).  part = 0: whole samples; otherwise the batch is ONE sample split along
 // K, part = 1 first / 2 middle / 3 last segment, with the partial Y carried
 // between segments in device memory (samples whose panels exceed a batch).
+//
+// Merged sampled columns (round 2): a level-sample's contraction is
+//     Y = sum_t w_t a_{j_t} b_{j_t}^T = sum_j W_j a_j b_j^T,  W_j = sum_{t: j_t = j} w_t,
+// because a duplicated index gathers the same drawn column (sketch.cpp:60-71)
+// -- so the K dimension can run over the DISTINCT sampled columns with summed
+// weights, and a column whose fine and coarse weights cancel (M = 2: w_coarse
+// = -w_fine, drawn once in the prefix and once in the suffix) drops out.  At
+// c = n that is 0.53 c columns instead of c.  A device pre-pass
+// (fused_run_round) builds per sample the ordered list of (j, W_j); `mk`
+// points at the batch's first sample (mk_stride entries per sample, padding
+// entries j = -1, w = 0), mk_info at its (len, neg_kc) and nkc is the merged
+// chunk count of the job (the maximum over its samples; slots >= len are
+// padding).  neg_kc (tcgen05 engine, shared RFF panel): the sample's leading
+// K-chunks that hold its negative-weight columns (columns repeated |W_j| / |w|
+// times there, so every |weight| stays the same power of two).
+struct MkEntry {
+    int32_t j, reps;  // 0-based column (-1: padding); reps = |cnt_fine - cnt_coarse| (informational)
+    double w;
+};
+struct MkInfo {
+    int32_t len, neg_kc;
+};
 struct KRange {
     int64_t kc0 = 0, nkc = -1;
     int part = 0;
+    const MkEntry* mk = nullptr;
+    int64_t mk_stride = 0;
+    const MkInfo* mk_info = nullptr;
 };
 struct PanelEngine {
     virtual ~PanelEngine() = default;
@@ -272,6 +297,13 @@ struct PanelEngine {
     }
     int64_t panel_bytes(int64_t c, int64_t cc) const { return nchunks(c, cc) * chunk_bytes(); }
     virtual bool splits_k() const { return false; }
+    // merged sampled columns: 0 = not supported for this (c, cc, weights);
+    // 1 = one group, weights summed; 2 = sign groups (negative first, each
+    // padded to whole K-chunks), columns repeated instead of weighted
+    virtual int merge_mode(int64_t c, int64_t cc, double w_fine, double w_coarse) const {
+        (void)c; (void)cc; (void)w_fine; (void)w_coarse;
+        return 0;
+    }
     virtual int64_t group_size() const = 0;   // samples per round of the CTA groups
     virtual void gen(cudaStream_t s, uint64_t seed, uint64_t tag, const int64_t* ks, int nb, int64_t c, int64_t cc,
                      double w_fine, double w_coarse, void* panels, uint32_t* idx, const KRange& kr) = 0;

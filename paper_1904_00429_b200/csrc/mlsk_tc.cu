@@ -420,7 +420,8 @@ __global__ void __launch_bounds__(GEN_T, KIND == GK_GAUSS ? MLSK_GAUSS_MINB : KI
 k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restrict__ ks, int nb, int64_t c,
                   int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kc0,
                   float* __restrict__ Ahi, float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
-                  uint32_t* __restrict__ idx_out) {
+                  uint32_t* __restrict__ idx_out, const MkEntry* __restrict__ mk, int64_t mk_stride,
+                  const MkInfo* __restrict__ mk_info) {
     __shared__ __align__(1024) unsigned char tbuf[2][2][TTILE];  // [buffer][hi / lo], double-buffered
     __shared__ __align__(16) float2 s_sc[256];  // full-circle sincos table
     __shared__ __align__(16) float2 s_lg[64];
@@ -445,7 +446,16 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
             const int64_t t = (kc0 + kc) * TBK + tid;  // column of the sample (kc0: first chunk of this K-range)
             int j = 0;  // padding columns (t >= c): column 0 with weight 0 (B = 0)
             float w = 0.f;
-            if (t < c) {
+            if (mk) {
+                // merged sampled columns (KRange): slot t of the sample's (j, W_j) list
+                if (t < mk_info[b].len) {
+                    const MkEntry e = mk[(int64_t)b * mk_stride + t];
+                    if (e.j >= 0) {
+                        j = e.j;
+                        w = (float)e.w;
+                    }
+                }
+            } else if (t < c) {
                 const u32x4 r = philox((uint32_t)(t >> 1), 0, 0, MLSK_CTR_INDEX, key);
                 const uint32_t ix = index_from_u64((t & 1) ? hi64(r) : lo64(r), M.n, M.log2n, M.cum);
                 j = (int)(ix - 1);
@@ -530,7 +540,8 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                  int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kcg,
                  int write_b, float* __restrict__ Ahi,
                  float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
-                 uint32_t* __restrict__ idx_out) {
+                 uint32_t* __restrict__ idx_out, const MkEntry* __restrict__ mk, int64_t mk_stride,
+                 const MkInfo* __restrict__ mk_info) {
     extern __shared__ __align__(1024) unsigned char rsm[];
     float* xs = reinterpret_cast<float*>(rsm);  // [D][128]
     float* wsm = xs + RFF_DMAX * RFF_RB;         // [D][RFF_COLS]
@@ -558,7 +569,14 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
             const int64_t t = (kcg + kc0) * TBK + tid;  // kcg: first chunk of this K-range
             int j = -1;
             float w = 0.f;
-            if (t < c) {
+            if (mk) {
+                // merged sampled columns (KRange); padding entries carry j = -1: a zero column
+                if (t < mk_info[b].len) {
+                    const MkEntry e = mk[(int64_t)b * mk_stride + t];
+                    j = e.j;
+                    w = (float)e.w;
+                }
+            } else if (t < c) {
                 const u32x4 r = philox((uint32_t)(t >> 1), 0, 0, MLSK_CTR_INDEX, key);
                 const uint32_t ix = index_from_u64((t & 1) ? hi64(r) : lo64(r), M.n, M.log2n, M.cum);
                 j = (int)(ix - 1);
@@ -680,6 +698,9 @@ struct TcShape {
     // the epilogue scales Y by escale = |w| -- bit-identical to B = diag(w) A^T
     int64_t neg_kc, kc0;
     float escale;
+    // merged sampled columns on the shared panel: the negated leading chunks
+    // per sample (mk_info[b].neg_kc) instead of neg_kc
+    const MkInfo* mk_info;
     // K-chunks per TMEM accumulation segment (0: a CTA's whole K-range of a
     // sample is one segment).  tcgen05's fp32 accumulation rounds the running
     // sum toward zero, so its error grows with the number of MMAs folded into
@@ -871,6 +892,8 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             int64_t sgc = 0;  // K-chunks of the current accumulation segment so far
             int abuf = 0;
             uint32_t aph = 0;  // bit a = phase of accumulator a (no indexed local array)
+            int sb = kpar ? 0 : grp;  // current sample (merged shared panel: its negated chunks)
+            int64_t neg_kc = sh.mk_info ? (sb < sh.nb ? sh.mk_info[sb].neg_kc : 0) : sh.neg_kc;
             for (int64_t it = 0; it < iters; ++it) {
                 if (sgc == 0) {  // first K-chunk of a segment (kpar: this CTA's range starts at kb > 0)
                     // the epilogue(s) released this accumulator
@@ -883,7 +906,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 tc_fence_after();
                 const uint32_t st = smem_addr(ring + s * STB);
                 const uint32_t dcol = tmem + (uint32_t)abuf * TBN;
-                const uint32_t id = sh.kc0 + kc < sh.neg_kc ? idesc | (1u << 14) : idesc;  // negate B
+                const uint32_t id = sh.kc0 + kc < neg_kc ? idesc | (1u << 14) : idesc;  // negate B
 #pragma unroll
                 for (int kk = 0; kk < TBK / 8; ++kk) {
                     const uint64_t ah = sw_desc(st + kk * 32), al = sw_desc(st + TA_BYTES + kk * 32);
@@ -907,7 +930,11 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 if (++s == NST) { s = 0; ph ^= 1; }
                 ++sgc;
                 const bool sample_end = ++kc == ke;
-                if (sample_end) kc = kb;
+                if (sample_end) {
+                    kc = kb;
+                    sb += sh.Gs;
+                    if (sh.mk_info && sb < sh.nb) neg_kc = sh.mk_info[sb].neg_kc;
+                }
                 if (sample_end || sgc == seg) {
                     sgc = 0;
                     if (PAIR) tc_commit_pair(tfull0 + 8 * abuf);  // accumulator segment complete
@@ -1276,6 +1303,12 @@ class TcEngine final : public PanelEngine {
         });
     }
     int64_t chunk_cols() const override { return TBK; }
+    // merged sampled columns: the shared RFF panel keeps every |weight| the same
+    // power of two, so its columns repeat in sign groups (mode 2); otherwise the
+    // summed weights fold into B (mode 1)
+    int merge_mode(int64_t c, int64_t cc, double w_fine, double w_coarse) const override {
+        return shared_panel(c, cc, w_fine, w_coarse) ? 2 : 1;
+    }
     int64_t chunk_bytes() const override { return (MP_ + PP_) * TBK * 8; }  // hi + lo
     bool splits_k() const override { return true; }
     int64_t group_size() const override { return Gs_; }
@@ -1290,21 +1323,21 @@ class TcEngine final : public PanelEngine {
                                                       (int64_t)nsm_ * 5),
                                RFF_T, rff_smem_, s>>>(
                 S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, kr.kc0,
-                shared_panel(c, cc, w_fine, w_coarse) ? 0 : 1, Ahi, Alo, Bhi, Blo, idx);
+                shared_panel(c, cc, w_fine, w_coarse) ? 0 : 1, Ahi, Alo, Bhi, Blo, idx, kr.mk, kr.mk_stride, kr.mk_info);
         } else {
             const int grid = (int)std::min<int64_t>((int64_t)nb * k, gen_cap_);
             if (M_.dm.kind == MLSK_MODEL_GAUSS_MEAN)
                 k_gen_panels_tf32<GK_GAUSS><<<grid, GEN_T, 0, s>>>(S_, seed, tag, ks, nb, c, cc, (float)w_fine,
                                                                   (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi,
-                                                                  Blo, idx);
+                                                                  Blo, idx, kr.mk, kr.mk_stride, kr.mk_info);
             else if (M_.dm.kind == MLSK_MODEL_STUDENT_T)
                 k_gen_panels_tf32<GK_STUDENT_T><<<grid, GEN_T, 0, s>>>(S_, seed, tag, ks, nb, c, cc, (float)w_fine,
                                                                       (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo,
-                                                                      Bhi, Blo, idx);
+                                                                      Bhi, Blo, idx, kr.mk, kr.mk_stride, kr.mk_info);
             else
                 k_gen_panels_tf32<GK_GENERIC><<<grid, GEN_T, 0, s>>>(S_, seed, tag, ks, nb, c, cc, (float)w_fine,
                                                                     (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi,
-                                                                    Blo, idx);
+                                                                    Blo, idx, kr.mk, kr.mk_stride, kr.mk_info);
         }
         launched();
     }
@@ -1321,6 +1354,8 @@ class TcEngine final : public PanelEngine {
             neg_kc = w_coarse < 0 ? cc / TBK : 0;
             escale = (float)std::fabs(w_fine);
         }
+        // merged sampled columns: sign groups only on the shared panel (mode 2)
+        const MkInfo* mk_info = kr.mk && shared_panel(c, cc, w_fine, w_coarse) ? kr.mk_info : nullptr;
         double* part = ws_.partial.p;
         double* part_sq = part + (size_t)T_ * Gs_ * (TBM * TBN);
         const bool finishes = kr.part == 0 || kr.part == 3;  // samples complete in this launch
@@ -1336,7 +1371,7 @@ class TcEngine final : public PanelEngine {
         const int64_t w1 = (T_ + nsm_ - 1) / nsm_, w2 = (2 * T_ + nsm_ - 1) / nsm_;
         if (kr.part == 0 && nb == 1 && direct && w2 < 2 * w1 && k >= 16 && !sym_nb_) {
             ws_.ypart.ensure((size_t)2 * T_ * TBM * TBN);
-            TcShape sh{1, k, MP_, PP_, T_, 2, tiles_n_, nullptr, M_.rows, M_.cols, 1, 0, 0, 0, 1.0f, seg_};
+            TcShape sh{1, k, MP_, PP_, T_, 2, tiles_n_, nullptr, M_.rows, M_.cols, 1, 0, 0, 0, 1.0f, nullptr, seg_};
             {
                 Prof p("gemm_tf32x3", s);
                 launch_gemm(true, segmented(k - (k + 1) / 2), 2 * T_, s, Ahi, Alo, Bhi, Blo, sh, part, part_sq, 1,
@@ -1360,7 +1395,7 @@ class TcEngine final : public PanelEngine {
             ypart = ws_.ypart.p;
         }
         TcShape sh{nb,      k,       MP_,     PP_,    T_,     Gs_,        tiles_n_, direct ? st.total() : nullptr,
-                   M_.rows, M_.cols, 0,       sym_nb_, neg_kc, kr.kc0, escale, seg_};
+                   M_.rows, M_.cols, 0,       sym_nb_, neg_kc, kr.kc0, escale, mk_info, seg_};
         {
             Prof p("gemm_tf32x3", s);
             if (kr.part == 0)

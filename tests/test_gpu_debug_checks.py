@@ -41,7 +41,8 @@ def test_every_engine_under_device_checks(debug_lib):
 @pytest.mark.gpu
 def test_parity_tests_under_device_checks(debug_lib):
     env = dict(os.environ, MLSK_LIB_PATH=debug_lib)
-    tests = ["tests/test_gpu_hierarchy.py", "tests/test_gpu_tc.py", "tests/test_gpu_fused.py", "tests/test_gpu_edge.py"]
+    tests = ["tests/test_gpu_hierarchy.py", "tests/test_gpu_tc.py", "tests/test_gpu_fused.py", "tests/test_gpu_edge.py",
+             "tests/test_gpu_merge.py"]
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu", *tests],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=1500)
     assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]

@@ -118,16 +118,22 @@ def test_tc_symmetric_gram(gpu, points, monkeypatch):
     re_ = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="exact"))
     check(rf, re_)
     # n / c a power of two: the GEMM reads B from the A panel (negated coarse
-    # prefix, Y scaled by |w|) -- the same bits as the separate B panel
+    # prefix, Y scaled by |w|) -- the same bits as the separate B panel.  (With
+    # merged sampled columns the two differ in how a repeated column enters --
+    # repeated vs weighted, tests/test_gpu_merge.py -- so the bit identity is a
+    # property of the unmerged contraction.)
+    monkeypatch.setenv("MLSK_MERGE", "0")
+    rsh = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
     monkeypatch.setenv("MLSK_TC_SHARED", "0")
     rsep = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
-    for a, b in zip(rf.per_level, rsep.per_level):
+    for a, b in zip(rsh.per_level, rsep.per_level):
         assert np.array_equal(np.asarray(a.sum), np.asarray(b.sum))
         assert a.sum_of_squares == b.sum_of_squares
+    check(rf, rsh)
     monkeypatch.setenv("MLSK_TC_SYM", "0")
     rfull = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
-    check(rf, rfull, tol=1e-6)
+    check(rsh, rfull, tol=1e-6)
     if points % 256 == 0:
-        for st in rf.per_level:
+        for st in list(rf.per_level) + list(rsh.per_level):
             s = np.asarray(st.sum)
             assert np.array_equal(s, s.T)

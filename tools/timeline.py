@@ -17,6 +17,11 @@ if len(sys.argv) > 1 and sys.argv[1] == "3":  # config 3 (fp32, 3xTF32 engine)
     model = g.gaussian_mean_matrix_model(1024, 16384, 1024, sd=1.0, data_seed=3, dtype=1)
     sess = g.MlmcSession(model, g.target_identity(), 2, 8, 1, c0=64, options=opts)
     STEP = [8 * 2 ** (8 - l) for l in range(9)]
+elif len(sys.argv) > 1 and sys.argv[1] in ("4", "5"):  # as tools/bench_configs.py defines them
+    import bench_configs_lib  # noqa: E402
+    cf = bench_configs_lib.configs(g)[int(sys.argv[1])]
+    model, STEP = cf["model"], cf["N"]
+    sess = g.MlmcSession(model, g.target_identity(), 2, len(STEP) - 1, 1, c0=cf["c0"], options=opts)
 else:
     model = g.gaussian_mean_matrix_model(256, 4096, 256, sd=0.5, data_seed=bench.data_seed())
     sess = g.MlmcSession(model, g.target_identity(), 2, 6, 1, c0=32, options=opts)
