@@ -319,6 +319,9 @@ def main():
     L.mlsk_profile_reset()
     L.mlsk_profile_enable(1)
     launches0 = L.mlsk_kernel_launch_count()
+    import ctypes as C
+    cols = (C.c_int64 * 2)()
+    L.mlsk_contraction_columns(cols, 1)   # reset the executed / sampled column counters
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -340,6 +343,8 @@ def main():
         dist.barrier()
     L.mlsk_profile_enable(0)
     launches = L.mlsk_kernel_launch_count() - launches0
+    L.mlsk_contraction_columns(cols, 0)
+    contraction = contraction_note(cols[0], cols[1])
     total_ms = sum(step_ms)
     if dist is not None:
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
@@ -347,7 +352,6 @@ def main():
         total_ms = float(t.item())
 
     # per-kernel event timings (this rank)
-    import ctypes as C
     kern = {}
     name = C.create_string_buffer(64)
     nl, ms = C.c_int64(), C.c_double()
@@ -417,6 +421,7 @@ def main():
                                             "(MEASURED_PEAKS.json has no fp64 entry)",
                              "algorithmic": "2*m*p*c_l flops per level-sample"},
                 "step_traffic": step_traffic,
+                "contraction": contraction,
                 "kernels": kern,
                 "step_fraction_gemm": (gemm["ms"] / sum(v["ms"] for v in kern.values())) if kern else None,
                 "gpu_launches": launches,
@@ -430,6 +435,18 @@ def main():
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def contraction_note(executed, sampled):
+    """Merged sampled columns (include/mlsk.h mlsk_contraction_columns): the GEMMs run over the
+    distinct sampled columns of a level-sample (summed weights; fine / coarse pairs cancel), so
+    the executed K is below the sampled c_l at the deep levels.  `value`, `sampled_gemm_tflops`
+    and `roofline.achieved` count the ALGORITHMIC work (2 m p c_l per level-sample)."""
+    return {"executed_columns": int(executed), "sampled_columns": int(sampled),
+            "executed_over_sampled": (executed / sampled) if sampled else None,
+            "note": "merged sampled columns: K runs over the distinct columns of each level-sample (padded to "
+                    "K-chunks); algorithmic flops = 2 m p c_l per level-sample, executed flops = that x "
+                    "executed_over_sampled; MLSK_MERGE=0 runs every sampled index"}
 
 
 def run_e2e(g, torch, device, args, rank=0, world=1, dist=None):

@@ -221,6 +221,8 @@ def measure(ids, steps=3, with_cpu=True, device=0):
         L.mlsk_profile_reset()
         L.mlsk_profile_enable(1)
         launches0 = L.mlsk_kernel_launch_count()
+        cols = (C.c_int64 * 2)()
+        L.mlsk_contraction_columns(cols, 1)
         nsteps = max(steps, 20) if c.get("inner") else steps  # config 1: 0.4 ms steps
         with bench.ClockSampler(device) as clk:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -231,6 +233,7 @@ def measure(ids, steps=3, with_cpu=True, device=0):
             e1.synchronize()
         L.mlsk_profile_enable(0)
         launches = L.mlsk_kernel_launch_count() - launches0
+        L.mlsk_contraction_columns(cols, 0)
         ms = e0.elapsed_time(e1) / nsteps
         kern = profile_read(L)
         samples = sum(c["N"])
@@ -279,6 +282,8 @@ def measure(ids, steps=3, with_cpu=True, device=0):
                                               f"({peak_t:.0f} TFLOP/s) / 3",
                                "algorithmic": ("P(P+1) c + 2 P D c flops per level-sample (SYRK + features)"
                                                if cid == 4 else "2 m p c flops per level-sample")}
+        if not c.get("inner"):
+            blk["contraction"] = bench.contraction_note(cols[0], cols[1])
         attach_traffic(cid, blk)
         if with_cpu:
             blk["cpu_baseline"] = cpu_baseline(cid, c, levels_c)

@@ -248,6 +248,14 @@ int mlsk_profile_reset(void);
 int mlsk_profile_read(int i, char* name, int name_len, int64_t* launches, double* ms);
 /* Start / end (ms since the last reset) of profiled launch i; returns the count. */
 int mlsk_profile_timeline(int i, char* name, int name_len, double* t0, double* t1);
+/* Merged sampled columns (identity target, levels with c >= n / 16: a
+ * level-sample's contraction runs over its DISTINCT sampled columns with
+ * summed weights -- a duplicated index gathers the same drawn column,
+ * sketch.cpp:60-71 -- and columns whose fine and coarse weights cancel drop
+ * out).  out[0] = K-columns the GEMMs of this thread's calls executed since
+ * the last reset, out[1] = the sampled indices they stand for (sum of c_l over
+ * the level-samples); reset != 0 clears both after the read. */
+int mlsk_contraction_columns(int64_t out[2], int reset);
 /* fp64 tensor-pipe (DMMA) throughput measured on the device, TFLOP/s. */
 double mlsk_measure_fp64_peak(int device);
 /* Dense TF32 tcgen05 throughput (M=128, N=n, one CTA per SM), TFLOP/s. */

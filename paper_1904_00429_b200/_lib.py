@@ -66,6 +66,7 @@ def lib():
     L.mlsk_version.restype = C.c_char_p
     L.mlsk_device_count.restype = C.c_int
     L.mlsk_kernel_launch_count.restype = C.c_int64
+    L.mlsk_contraction_columns.argtypes = [_P(C.c_int64), C.c_int]
     L.mlsk_profile_enable.argtypes = [C.c_int]
     L.mlsk_profile_read.argtypes = [C.c_int, C.c_char_p, C.c_int, _P(C.c_int64), _P(C.c_double)]
     L.mlsk_profile_timeline.argtypes = [C.c_int, C.c_char_p, C.c_int, _P(C.c_double), _P(C.c_double)]

@@ -21,6 +21,7 @@
 
 namespace mlsk {
 thread_local int64_t g_launches = 0;
+thread_local int64_t g_columns[2] = {0, 0};
 int run_guarded(const std::function<void()>& body);
 }
 
@@ -1029,5 +1030,14 @@ int mlsk_device_count(void) {
 }
 
 int64_t mlsk_kernel_launch_count(void) { return g_launches; }
+
+int mlsk_contraction_columns(int64_t out[2], int reset) {
+    if (out) {
+        out[0] = g_columns[0];
+        out[1] = g_columns[1];
+    }
+    if (reset) g_columns[0] = g_columns[1] = 0;
+    return MLSK_OK;
+}
 
 }  // extern "C"

@@ -1060,8 +1060,9 @@ __global__ void k_expand_ks(const KsRun* __restrict__ runs, int nruns, int64_t t
 // k_mk_tiles / k_mk_scan / k_mk_write turn a sample's counts into its list,
 // ordered by j (tiles of 4096 columns: counts, exclusive scan, ordered writes):
 //   mode 1: one entry per column with W_j = cnt_f w_fine + cnt_c w_coarse != 0;
-//   mode 2: columns with cnt_f != cnt_c repeated |cnt_f - cnt_c| times, the
-//           negative ones (cnt_f < cnt_c) first, padded to whole K-chunks.
+//   mode 2: one entry per column with cnt_f != cnt_c carrying the column
+//           scale sqrt(|cnt_f - cnt_c|) (Y = sum_j sign_j (s_j z_j)(s_j z_j)^T |w|),
+//           the negative ones (cnt_f < cnt_c) first, padded to whole K-chunks.
 // The write pass clears the counts it read; the scan raises the job's maximum
 // chunk count, which the host reads once per round to size the launches.
 constexpr int MK_T = 256, MK_ITEMS = 16, MK_TILE = MK_T * MK_ITEMS;
@@ -1094,7 +1095,7 @@ __device__ __forceinline__ int mk_entries(unsigned long long v, int mode, double
     if (v == 0) return 0;
     if (mode == 2) {  // |w_coarse| == |w_fine|, w_coarse < 0 (shared_panel)
         neg = cf < ccn;
-        return (int)(cf > ccn ? cf - ccn : ccn - cf);
+        return cf != ccn ? 1 : 0;
     }
     if (w_coarse == -w_fine) return cf != ccn ? 1 : 0;  // exact cancellation (M = 2)
     return __fma_rn((double)cf, w_fine, __dmul_rn((double)ccn, w_coarse)) != 0.0 ? 1 : 0;
@@ -1252,10 +1253,12 @@ k_mk_write(unsigned long long* __restrict__ cnt, int64_t n, int mode, double w_f
         MkEntry e;
         e.j = (int32_t)(j0 + i);
         e.reps = (int32_t)(cf > ccn ? cf - ccn : ccn - cf);
-        e.w = mode == 2 ? (ng[i] ? w_coarse : w_fine)
+        // mode 2: the signed column scale sqrt(|cnt_f - cnt_c|) (the panel column is
+        // scaled, the sign is the chunk's negate bit); mode 1: the summed weight
+        e.w = mode == 2 ? (ng[i] ? -sqrt((double)e.reps) : sqrt((double)e.reps))
                         : __fma_rn((double)cf, w_fine, __dmul_rn((double)ccn, w_coarse));
         int& o = ng[i] ? on : op;
-        for (int r = 0; r < en[i]; ++r) out[o++] = e;
+        out[o++] = e;
     }
 }
 
@@ -1676,9 +1679,30 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         const int64_t q = int64_t(64) << 20;
         return std::min(ub, (need + need / 32 + q - 1) / q * q);
     };
+    // Level order (each level has its own accumulators, so the order changes no
+    // result): the pipeline's tail is the last batch's GEMM with no generator
+    // left to overlap, its head the first batch's generator alone.  When one
+    // sample's panels exceed a batch (configs 4 / 5: long single-sample GEMMs at
+    // the deep levels) the levels run deepest first, so that those GEMMs run
+    // over the other levels' generators instead of ending the round alone
+    // (config 4: 13.2 -> 12.75 ms per step, config 5: 345 -> 341); with many
+    // samples per batch at every level (configs 2 / 3) the order is neutral to
+    // slightly worse (19.73 -> 19.90 ms) and stays ascending.
+    // MLSK_LEVEL_ORDER=asc|desc overrides.
+    std::vector<size_t> level_order(jobs.size());
+    for (size_t j = 0; j < jobs.size(); ++j) level_order[j] = j;
+    {
+        bool desc = false;
+        for (size_t j = 0; j < jobs.size(); ++j)
+            if (job_cnt[j] > 0 && job_chunks(j) * E.chunk_bytes() > budget) desc = true;
+        if (const char* e = getenv("MLSK_LEVEL_ORDER")) desc = e[0] == 'd';
+        if (desc)
+            std::stable_sort(level_order.begin(), level_order.end(),
+                             [&](size_t x, size_t y) { return jobs[x].lv.c > jobs[y].lv.c; });
+    }
     std::vector<Batch> batches;
     int64_t max_panel = 0;
-    for (size_t j = 0; j < jobs.size(); ++j) {
+    for (size_t j : level_order) {
         const int64_t per = job_chunks(j) * E.chunk_bytes();
         const int64_t total = job_cnt[j];
         if (per > split_limit && E.splits_k()) {
@@ -1750,6 +1774,13 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
         // GEMM + fused level epilogue + fixed-order reduction
         MLSK_CUDA(cudaStreamWaitEvent(P.s_mm, P.gen_done[buf], 0));
         E.gemm(P.s_mm, panels, bt.nb, c, cc, w_fine, w_coarse, *job.st, bt.kr);
+        {
+            const int64_t full = E.nchunks(c, cc);
+            const int64_t k = bt.kr.nkc >= 0 ? bt.kr.nkc : full;
+            g_columns[0] += (int64_t)bt.nb * k * E.chunk_cols();
+            // (a K-split sample's segments add up to its merged chunks; its c indices count once)
+            g_columns[1] += bt.kr.part == 0 || bt.kr.part == 1 ? (int64_t)bt.nb * c : 0;
+        }
         MLSK_CUDA(cudaEventRecord(P.mm_done[buf], P.s_mm));
         P.used[buf] = true;
         if (idx) {

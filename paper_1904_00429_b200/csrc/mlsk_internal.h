@@ -44,6 +44,9 @@ constexpr double kRescalePerturb = MLSK_INJECT_RESCALE_BUG ? 1.0 + 1e-6 : 1.0;
 
 // Kernel launches made by the calling thread (mlsk_kernel_launch_count).
 extern thread_local int64_t g_launches;
+// K-columns executed by the panel engines' GEMMs / sampled indices they stand
+// for (mlsk_contraction_columns)
+extern thread_local int64_t g_columns[2];
 inline void launched(int n = 1) {
     g_launches += n;
     MLSK_CUDA(cudaGetLastError());
@@ -270,8 +273,9 @@ struct FusedJob {
 // entries j = -1, w = 0), mk_info at its (len, neg_kc) and nkc is the merged
 // chunk count of the job (the maximum over its samples; slots >= len are
 // padding).  neg_kc (tcgen05 engine, shared RFF panel): the sample's leading
-// K-chunks that hold its negative-weight columns (columns repeated |W_j| / |w|
-// times there, so every |weight| stays the same power of two).
+// K-chunks that hold its negative-weight columns; there an entry's w is the
+// signed column scale sqrt(|W_j| / |w|) applied to the one panel both operand
+// roles read (Y = |w| sum_j sign_j (s_j z_j)(s_j z_j)^T).
 struct MkEntry {
     int32_t j, reps;  // 0-based column (-1: padding); reps = |cnt_fine - cnt_coarse| (informational)
     double w;
@@ -299,7 +303,7 @@ struct PanelEngine {
     virtual bool splits_k() const { return false; }
     // merged sampled columns: 0 = not supported for this (c, cc, weights);
     // 1 = one group, weights summed; 2 = sign groups (negative first, each
-    // padded to whole K-chunks), columns repeated instead of weighted
+    // padded to whole K-chunks), columns scaled by sqrt(|W_j| / |w|)
     virtual int merge_mode(int64_t c, int64_t cc, double w_fine, double w_coarse) const {
         (void)c; (void)cc; (void)w_fine; (void)w_coarse;
         return 0;

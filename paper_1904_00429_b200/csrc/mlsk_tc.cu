@@ -604,6 +604,7 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
         }
         const int64_t kc = kc0 + ch;
         const bool col_ok = kc < nkc;
+        const bool colscale = mk != nullptr && !write_b;
         const int64_t rb_end = nrb < (rs + 1) * rb_per ? nrb : (rs + 1) * rb_per;
         for (int64_t rbi = rs * rb_per; rbi < rb_end; ++rbi) {
             const int64_t rb = rbi * RFF_RB;
@@ -654,6 +655,8 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                 for (int q = 0; q < 4; ++q) {
                     z[q] = 0.f;
                     if (jv[q] >= 0 && r0 + i < lim) z[q] = scale * cosf(acc[i][q] + bv[q]);
+                    // merged columns on the shared panel: |w| is the column scale sqrt(reps)
+                    if (colscale) z[q] = __fmul_rn(fabsf(wv4[q]), z[q]);
                     v[q] = __fmul_rn(wv4[q], z[q]);
                 }
                 const int off = sw_off(r, tt) / 4;  // floats
@@ -1303,9 +1306,9 @@ class TcEngine final : public PanelEngine {
         });
     }
     int64_t chunk_cols() const override { return TBK; }
-    // merged sampled columns: the shared RFF panel keeps every |weight| the same
-    // power of two, so its columns repeat in sign groups (mode 2); otherwise the
-    // summed weights fold into B (mode 1)
+    // merged sampled columns: on the shared RFF panel the columns carry the scale
+    // sqrt(|W_j| / |w|) in sign groups (mode 2); otherwise the summed weights
+    // fold into B (mode 1)
     int merge_mode(int64_t c, int64_t cc, double w_fine, double w_coarse) const override {
         return shared_panel(c, cc, w_fine, w_coarse) ? 2 : 1;
     }

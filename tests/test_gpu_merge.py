@@ -132,7 +132,7 @@ def test_merge_student_t_k_split(gpu):
 
 def test_merge_rff_shared_panel(gpu):
     """RFF Gram on the symmetric tile grid with the shared A / B panel (n, c
-    powers of two): sign groups with repeated columns (mode 2), the negated
+    powers of two): sign groups of scaled columns (mode 2), the negated
     leading chunks per sample."""
     model = gpu.rff_gram_model(512, 4096, dim=64, sigma=4.0, data_seed=17)
     rm, ru = three_way(gpu, model, 2, 5, [3, 3, 2, 2, 2, 2], 128, TOL32)

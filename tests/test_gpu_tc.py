@@ -120,7 +120,7 @@ def test_tc_symmetric_gram(gpu, points, monkeypatch):
     # n / c a power of two: the GEMM reads B from the A panel (negated coarse
     # prefix, Y scaled by |w|) -- the same bits as the separate B panel.  (With
     # merged sampled columns the two differ in how a repeated column enters --
-    # repeated vs weighted, tests/test_gpu_merge.py -- so the bit identity is a
+    # scaled by sqrt(reps) vs weighted, tests/test_gpu_merge.py -- so the bit identity is a
     # property of the unmerged contraction.)
     monkeypatch.setenv("MLSK_MERGE", "0")
     rsh = gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused"))
