@@ -23,6 +23,7 @@
 //  k_reduce_tiles    deterministic (fixed-order) sum of the per-CTA partials
 //                    into the level accumulators.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -1284,11 +1285,16 @@ struct Pipe {
     DevArray<unsigned long long> mk_cnt;  // [group sample][n] packed counts, all zero between uses
     DevArray<int2> mk_tile;               // [group sample][tile] entry counts, then offsets
     DevArray<MkEntry> mk_list;
-    DevArray<MkInfo> mk_info;
+    DevArray<MkInfo> mk_info[2];          // by round parity: the last round's GEMMs may still read theirs
+    int mk_parity = 0;
+    cudaEvent_t mk_info_done[2] = {};     // end of the last round that used mk_info[parity]
+    bool mk_info_used[2] = {};
+    uint64_t last_serial = 0;             // model of the last matrix round (cross-round overlap)
     DevArray<int32_t> mk_max;             // per merged job: maximum K-chunks over its samples
     int32_t* mk_max_host = nullptr;       // pinned
     cudaEvent_t mk_done = nullptr;
     bool ran = false;                     // a round's end event has been recorded
+    uint64_t batch_seq = 0;               // batches launched so far (panel buffer rotation)
 
     void ensure_inner_red() {
         if (red_done.p) return;
@@ -1306,6 +1312,7 @@ struct Pipe {
         MLSK_CUDA(cudaEventCreateWithFlags(&end, cudaEventDisableTiming));
         MLSK_CUDA(cudaEventCreateWithFlags(&staged, cudaEventDisableTiming));
         MLSK_CUDA(cudaEventCreateWithFlags(&mk_done, cudaEventDisableTiming));
+        for (int i = 0; i < 2; ++i) MLSK_CUDA(cudaEventCreateWithFlags(&mk_info_done[i], cudaEventDisableTiming));
         MLSK_CUDA(cudaMallocHost(&mk_max_host, MK_MAX_JOBS * sizeof(int32_t)));
         for (int i = 0; i < NBUF; ++i) {
             MLSK_CUDA(cudaEventCreateWithFlags(&gen_done[i], cudaEventDisableTiming));
@@ -1323,6 +1330,7 @@ struct Pipe {
         cudaEventDestroy(end);
         cudaEventDestroy(staged);
         cudaEventDestroy(mk_done);
+        for (int i = 0; i < 2; ++i) cudaEventDestroy(mk_info_done[i]);
         if (mk_max_host) cudaFreeHost(mk_max_host);
         if (runs_host) cudaFreeHost(runs_host);
         if (s_gen) cudaStreamDestroy(s_gen);
@@ -1434,8 +1442,20 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
             for (const auto& sg : jobs[j].segs)
                 for (int64_t k = 0; k < sg.count; ++k) jks[j].push_back(sg.k0 + k);
     MLSK_CUDA(cudaEventRecord(P.start, a.stream));
-    MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.start, 0));
+    // Cross-round overlap (matrix path): the generator stream reads only the
+    // model and its own scratch (replication lists, merged-column lists, panel
+    // buffers guarded by the GEMMs' events), so when the last round on this
+    // pipeline ran the same model -- which waited for the caller's stream
+    // after the model was built -- it need not wait for the caller's stream
+    // again: the pre-pass and first generators of this round then run under the
+    // last round's GEMM tail (config 2: 0.7 ms of a 19.7 ms round, config 3:
+    // 0.7 of 14.5).  The GEMM stream (level accumulators) always waits.
+    // MLSK_ROUND_OVERLAP=0 restores the full dependency.
+    const char* ov_env = getenv("MLSK_ROUND_OVERLAP");
+    const bool overlap_rounds = !M.vector && P.ran && P.last_serial == M.serial && !(ov_env && ov_env[0] == '0');
+    if (!overlap_rounds) MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.start, 0));
     MLSK_CUDA(cudaStreamWaitEvent(P.s_mm, P.start, 0));
+    P.last_serial = M.vector ? 0 : M.serial;
     P.stage_ks(runs, all, P.s_gen);
     if (M.vector && !any_probe) {
         // config-1 shape: every level of the round in one launch (+ one reduction
@@ -1573,226 +1593,268 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
     if (const char* e = getenv("MLSK_SPLIT_MB"))  // tests: force K-split samples at small shapes
         split_limit = std::max<int64_t>(1, atoll(e)) << 20;
 
-    // ---- merged sampled columns: the pre-pass of every level that qualifies
-    // (deepest first, within a 1 GiB budget of list memory), then ONE host
-    // synchronisation for the merged chunk counts that size the launches
-    std::vector<int> mj_of(jobs.size(), -1);
-    std::vector<MergeJob> mjs;
-    if (!nl && merge_enabled()) {
-        const int64_t KCOLS = E.chunk_cols();
-        std::vector<size_t> order(jobs.size());
-        for (size_t j = 0; j < jobs.size(); ++j) order[j] = j;
-        std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return jobs[x].lv.c > jobs[y].lv.c; });
-        const size_t list_budget = (size_t(1) << 30) / sizeof(MkEntry);
-        size_t list_used = 0, info_used = 0;
-        for (size_t j : order) {
-            const int64_t c = jobs[j].lv.c, cc = jobs[j].lv.cc;
-            if (job_cnt[j] == 0 || jobs[j].probe_host || jobs[j].lv.full || c * merge_min_den() < M.desc.n ||
-                c < 4 * KCOLS || M.desc.n > (int64_t(1) << 31) - 2 || (int)mjs.size() == MK_MAX_JOBS)
+    // ---- passes.  The merged-column lists of a round (16 bytes per sampled
+    // index) must fit their budget (1 GiB; MLSK_MERGE_LIST_MB): a round with more
+    // (the adaptive driver's large rounds: millions of samples per level) runs
+    // as several passes over slices of every level's samples, each with its own
+    // pre-pass and synchronisation.
+    const int64_t KCOLS = E.chunk_cols();
+    auto merge_stride = [&](int64_t c) { return (c + KCOLS - 1) / KCOLS * KCOLS + KCOLS; };
+    auto merge_mode_of = [&](size_t j) {
+        const int64_t c = jobs[j].lv.c, cc = jobs[j].lv.cc;
+        if (nl || !merge_enabled() || jobs[j].probe_host || jobs[j].lv.full || c * merge_min_den() < M.desc.n ||
+            c < 4 * KCOLS || M.desc.n > (int64_t(1) << 31) - 2)
+            return 0;
+        const double w_fine = n / (double)c * kRescalePerturb;
+        const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;
+        return E.merge_mode(c, cc, w_fine, w_coarse);
+    };
+    int64_t list_mb = 1024;
+    if (const char* e = getenv("MLSK_MERGE_LIST_MB")) list_mb = std::max<int64_t>(1, atoll(e));  // tests
+    const size_t list_budget = (size_t)(list_mb << 20) / sizeof(MkEntry);
+    int64_t npass = 1;
+    {
+        double entries = 0;
+        for (size_t j = 0; j < jobs.size(); ++j)
+            if (job_cnt[j] > 0 && merge_mode_of(j)) entries += (double)job_cnt[j] * (double)merge_stride(jobs[j].lv.c);
+        npass = std::max<int64_t>(1, (int64_t)std::ceil(entries / (0.95 * (double)list_budget)));
+    }
+    std::vector<int64_t> plo(jobs.size(), 0), pcnt(jobs.size(), 0);
+    for (int64_t pass = 0; pass < npass; ++pass) {
+        for (size_t j = 0; j < jobs.size(); ++j) {
+            // slice boundaries on multiples of the engine's sample group
+            auto cut = [&](int64_t q) {
+                if (q >= npass) return job_cnt[j];
+                const int64_t v = (int64_t)((double)job_cnt[j] * (double)q / (double)npass);
+                return std::min(job_cnt[j], v / Gs * Gs);
+            };
+            plo[j] = cut(pass);
+            pcnt[j] = cut(pass + 1) - plo[j];
+        }
+        // ---- merged sampled columns: the pre-pass of every level that qualifies
+        // (deepest first, within the pass's budget of list memory), then ONE host
+        // synchronisation for the merged chunk counts that size the launches
+        std::vector<int> mj_of(jobs.size(), -1);
+        std::vector<MergeJob> mjs;
+        if (!nl && merge_enabled()) {
+            std::vector<size_t> order(jobs.size());
+            for (size_t j = 0; j < jobs.size(); ++j) order[j] = j;
+            std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return jobs[x].lv.c > jobs[y].lv.c; });
+            size_t list_used = 0, info_used = 0;
+            for (size_t j : order) {
+                if (pcnt[j] == 0 || (int)mjs.size() == MK_MAX_JOBS) continue;
+                const int mode = merge_mode_of(j);
+                if (!mode) continue;
+                const int64_t stride = merge_stride(jobs[j].lv.c);
+                const size_t need = (size_t)pcnt[j] * (size_t)stride;
+                if (list_used + need > list_budget) continue;
+                mj_of[j] = (int)mjs.size();
+                mjs.push_back({mode, stride, list_used, info_used, 0});
+                list_used += need;
+                info_used += (size_t)pcnt[j];
+            }
+            if (!mjs.empty()) {
+                // (the lists are read by the generators only, in order on this stream;
+                // the per-sample info also by the GEMMs: double-buffered by round)
+                P.mk_parity ^= 1;
+                if (P.mk_info_used[P.mk_parity])
+                    MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.mk_info_done[P.mk_parity], 0));
+                P.mk_list.ensure(list_used);
+                P.mk_info[P.mk_parity].ensure(info_used);
+                P.mk_max.ensure(MK_MAX_JOBS);
+                MLSK_CUDA(cudaMemsetAsync(P.mk_max.p, 0, MK_MAX_JOBS * sizeof(int32_t), P.s_gen));
+                // count scratch: groups of samples within 256 MiB
+                int64_t cnt_mb = 256;
+                if (const char* e = getenv("MLSK_MERGE_GROUP_MB")) cnt_mb = std::max<int64_t>(1, atoll(e));  // tests
+                const int64_t mk_tiles = (M.desc.n + MK_TILE - 1) / MK_TILE;
+                // (a launch's grid.y: at most 65535 samples per group)
+                const int64_t grp_cap = std::min<int64_t>(65535, std::max<int64_t>(1, (cnt_mb << 20) / (8 * M.desc.n)));
+                int64_t max_grp = 0;
+                for (size_t j = 0; j < jobs.size(); ++j)
+                    if (mj_of[j] >= 0) max_grp = std::max(max_grp, std::min(grp_cap, pcnt[j]));
+                const size_t cnt_need = (size_t)max_grp * (size_t)M.desc.n;
+                if (cnt_need > P.mk_cnt.n) {
+                    P.mk_cnt.ensure(cnt_need);
+                    P.mk_cnt.zero(P.s_gen);
+                }
+                P.mk_tile.ensure((size_t)max_grp * (size_t)mk_tiles);
+                Prof p("merge_columns", P.s_gen);
+                for (size_t j = 0; j < jobs.size(); ++j) {
+                    if (mj_of[j] < 0) continue;
+                    const MergeJob& mj = mjs[mj_of[j]];
+                    const int64_t c = jobs[j].lv.c, cc = jobs[j].lv.cc;
+                    const double w_fine = n / (double)c * kRescalePerturb;
+                    const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;
+                    for (int64_t off = 0; off < pcnt[j]; off += grp_cap) {
+                        const int64_t g = std::min(grp_cap, pcnt[j] - off);
+                        const int64_t work = g * ((c + 1) / 2);
+                        k_mk_count<<<(int)std::min<int64_t>((work + 255) / 256, (int64_t)sms * 16), 256, 0, P.s_gen>>>(
+                            M.dm, a.seed, jobs[j].lv.tag, P.ks.p + job_off[j] + plo[j] + off, g, c, cc, P.mk_cnt.p);
+                        MkEntry* list = P.mk_list.p + mj.list_off + (size_t)off * mj.stride;
+                        MkInfo* info = P.mk_info[P.mk_parity].p + mj.info_off + off;
+                        const dim3 tg((unsigned)mk_tiles, (unsigned)g);
+                        k_mk_tiles<<<tg, MK_T, 0, P.s_gen>>>(P.mk_cnt.p, M.desc.n, mj.mode, w_fine, w_coarse, P.mk_tile.p);
+                        k_mk_scan<<<(int)g, MK_T, 0, P.s_gen>>>(P.mk_tile.p, (int)mk_tiles, (int)KCOLS, list, mj.stride,
+                                                               info, P.mk_max.p + mj_of[j]);
+                        k_mk_write<<<tg, MK_T, 0, P.s_gen>>>(P.mk_cnt.p, M.desc.n, mj.mode, w_fine, w_coarse, (int)KCOLS,
+                                                             P.mk_tile.p, info, list, mj.stride);
+                        launched(4);
+                    }
+                }
+                MLSK_CUDA(cudaMemcpyAsync(P.mk_max_host, P.mk_max.p, mjs.size() * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                          P.s_gen));
+                MLSK_CUDA(cudaEventRecord(P.mk_done, P.s_gen));
+                MLSK_CUDA(cudaEventSynchronize(P.mk_done));
+                for (size_t q = 0; q < mjs.size(); ++q) mjs[q].nk = std::max<int64_t>(1, P.mk_max_host[q]);
+            }
+        }
+        auto job_chunks = [&](size_t j) {
+            return mj_of[j] >= 0 ? mjs[mj_of[j]].nk : E.nchunks(jobs[j].lv.c, jobs[j].lv.cc);
+        };
+        auto with_merge = [&](KRange kr, size_t j, int64_t off) {
+            if (mj_of[j] >= 0) {
+                const MergeJob& mj = mjs[mj_of[j]];
+                if (kr.nkc < 0) kr.nkc = mj.nk;
+                kr.mk = P.mk_list.p + mj.list_off + (size_t)off * mj.stride;
+                kr.mk_stride = mj.stride;
+                kr.mk_info = P.mk_info[P.mk_parity].p + mj.info_off + off;
+            }
+            return kr;
+        };
+
+        // panel bytes a batch of nb samples needs in its buffer.  Merged chunk
+        // counts vary a little from round to round (they follow the draws), and a
+        // buffer that grew with every new maximum would be reallocated for many
+        // rounds: merged batches reserve 3% + 64 MiB of headroom, capped at the
+        // unmerged size.
+        auto reserve_bytes = [&](size_t j, int64_t nb, int64_t chunks) {
+            const int64_t need = nb * chunks * E.chunk_bytes();
+            if (mj_of[j] < 0) return need;
+            const int64_t ub = nb * E.nchunks(jobs[j].lv.c, jobs[j].lv.cc) * E.chunk_bytes();
+            const int64_t q = int64_t(64) << 20;
+            return std::min(ub, (need + need / 32 + q - 1) / q * q);
+        };
+        // Level order (each level has its own accumulators, so the order changes no
+        // result): the pipeline's tail is the last batch's GEMM with no generator
+        // left to overlap, its head the first batch's generator alone.  When one
+        // sample's panels exceed a batch (configs 4 / 5: long single-sample GEMMs at
+        // the deep levels) the levels run deepest first, so that those GEMMs run
+        // over the other levels' generators instead of ending the round alone
+        // (config 4: 13.2 -> 12.75 ms per step, config 5: 345 -> 341); with many
+        // samples per batch at every level (configs 2 / 3) the order is neutral to
+        // slightly worse (19.73 -> 19.90 ms) and stays ascending.
+        // MLSK_LEVEL_ORDER=asc|desc overrides.
+        std::vector<size_t> level_order(jobs.size());
+        for (size_t j = 0; j < jobs.size(); ++j) level_order[j] = j;
+        {
+            bool desc = false;
+            for (size_t j = 0; j < jobs.size(); ++j)
+                if (pcnt[j] > 0 && job_chunks(j) * E.chunk_bytes() > budget) desc = true;
+            if (const char* e = getenv("MLSK_LEVEL_ORDER")) desc = e[0] == 'd';
+            if (desc)
+                std::stable_sort(level_order.begin(), level_order.end(),
+                                 [&](size_t x, size_t y) { return jobs[x].lv.c > jobs[y].lv.c; });
+        }
+        std::vector<Batch> batches;
+        int64_t max_panel = 0;
+        for (size_t j : level_order) {
+            const int64_t per = job_chunks(j) * E.chunk_bytes();
+            const int64_t total = pcnt[j];  // this pass's samples of the level: [plo, plo + total)
+            if (per > split_limit && E.splits_k()) {
+                if (nl)
+                    throw Error(MLSK_EINVAL, "fused engine: nonlinear targets need a level-sample's panels within one "
+                                             "batch (" + std::to_string(split_limit >> 20) + " MiB)");
+                // one sample's panels exceed a batch: K-segments of one sample each,
+                // the partial Y carried between them
+                if (jobs[j].probe_host)
+                    throw Error(MLSK_EINVAL, "probe: not available for level-samples split along K (panels > " + std::to_string(split_limit >> 20) + " MiB)");
+                const int64_t nk = job_chunks(j);
+                const int64_t seg = std::max<int64_t>(1, split_limit / E.chunk_bytes());  // few, large segments
+                for (int64_t off = 0; off < total; ++off)
+                    for (int64_t k0 = 0; k0 < nk; k0 += seg) {
+                        KRange kr;
+                        kr.kc0 = k0;
+                        kr.nkc = std::min(seg, nk - k0);
+                        kr.part = nk <= seg ? 0 : (k0 == 0 ? 1 : (k0 + kr.nkc == nk ? 3 : 2));
+                        batches.push_back({j, plo[j] + off, 1, job_off[j] + plo[j] + off, with_merge(kr, j, off)});
+                        max_panel = std::max(max_panel, reserve_bytes(j, 1, kr.nkc));
+                    }
                 continue;
-            const double w_fine = n / (double)c * kRescalePerturb;
-            const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;
-            const int mode = E.merge_mode(c, cc, w_fine, w_coarse);
-            if (!mode) continue;
-            const int64_t stride = (c + KCOLS - 1) / KCOLS * KCOLS + KCOLS;
-            const size_t need = (size_t)job_cnt[j] * (size_t)stride;
-            if (list_used + need > list_budget) continue;
-            mj_of[j] = (int)mjs.size();
-            mjs.push_back({mode, stride, list_used, info_used, 0});
-            list_used += need;
-            info_used += (size_t)job_cnt[j];
+            }
+            int64_t max_nb = std::max<int64_t>(1, budget / per);
+            // every CTA group needs a sample: stretch the batch (up to 4x the budget)
+            // rather than leave groups idle (config 3's deepest level: 268 MB samples)
+            if (max_nb < Gs && Gs * per <= 4 * budget) max_nb = Gs;
+            if (max_nb > Gs) max_nb = max_nb / Gs * Gs;
+            for (int64_t off = 0; off < total; off += max_nb) {
+                const int nb = (int)std::min<int64_t>(max_nb, total - off);
+                batches.push_back({j, plo[j] + off, nb, job_off[j] + plo[j] + off, with_merge(KRange{}, j, off)});
+                max_panel = std::max(max_panel, reserve_bytes(j, nb, job_chunks(j)));
+            }
+        }
+        if ((size_t)(max_panel + 7) / 8 > P.panels[0].n) {
+            // the buffers must grow: one level-sample's panels must fit a buffer;
+            // fail with a clear message instead of an opaque allocation error
+            // (queried only when growing: cudaMemGetInfo on every round stalled
+            // the launching thread for milliseconds now and then)
+            size_t free_b = 0, total_b = 0;
+            MLSK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            size_t held = 0;
+            for (int i = 0; i < NBUF; ++i) held += P.panels[i].n * sizeof(double);
+            if ((double)NBUF * (double)max_panel > (double)(free_b + held))
+                throw Error(MLSK_ERUNTIME, "fused engine: the sampled panels of one batch (" +
+                                               std::to_string(max_panel >> 20) + " MiB x " + std::to_string(NBUF) +
+                                               " buffers) exceed free device memory; use a smaller c_l or m, p");
+        }
+        for (int i = 0; i < NBUF; ++i) P.panels[i].ensure((size_t)(max_panel + 7) / 8);
+
+        for (size_t bi = 0; bi < batches.size(); ++bi, ++P.batch_seq) {
+            const size_t i = (size_t)P.batch_seq;  // buffers rotate across passes and rounds
+            const Batch& bt = batches[bi];
+            FusedJob& job = jobs[bt.job];
+            const int64_t c = job.lv.c, cc = job.lv.cc;
+            const double w_fine = n / (double)c * kRescalePerturb;                                        // n/c
+            const double w_coarse = cc > 0 && !nl ? w_fine - n / (double)cc : w_fine;  // n/c - n/cc on the prefix
+            const int buf = (int)(i % NBUF);
+            void* panels = P.panels[buf].p;
+            uint32_t* idx = nullptr;
+            if (job.probe_host) {
+                P.idx[buf].ensure((size_t)bt.nb * c);
+                idx = P.idx[buf].p;
+            }
+            // generator: wait until the GEMM that last used this buffer is done
+            if (P.used[buf]) MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.mm_done[buf], 0));
+            if (serial_mode() && P.used[(i + NBUF - 1) % NBUF])
+                MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.mm_done[(i + NBUF - 1) % NBUF], 0));
+            E.gen(P.s_gen, a.seed, job.lv.tag, P.ks.p + bt.ks_off, bt.nb, c, cc, w_fine, w_coarse, panels, idx, bt.kr);
+            MLSK_CUDA(cudaEventRecord(P.gen_done[buf], P.s_gen));
+            // GEMM + fused level epilogue + fixed-order reduction
+            MLSK_CUDA(cudaStreamWaitEvent(P.s_mm, P.gen_done[buf], 0));
+            E.gemm(P.s_mm, panels, bt.nb, c, cc, w_fine, w_coarse, *job.st, bt.kr);
+            {
+                const int64_t full = E.nchunks(c, cc);
+                const int64_t k = bt.kr.nkc >= 0 ? bt.kr.nkc : full;
+                g_columns[0] += (int64_t)bt.nb * k * E.chunk_cols();
+                // (a K-split sample's segments add up to its merged chunks; its c indices count once)
+                g_columns[1] += bt.kr.part == 0 || bt.kr.part == 1 ? (int64_t)bt.nb * c : 0;
+            }
+            MLSK_CUDA(cudaEventRecord(P.mm_done[buf], P.s_mm));
+            P.used[buf] = true;
+            if (idx) {
+                MLSK_CUDA(cudaStreamSynchronize(P.s_gen));
+                for (int b = 0; b < bt.nb; ++b) {
+                    const int64_t k = jks[bt.job][bt.off + b];
+                    if (k < a.probe_k)
+                        MLSK_CUDA(cudaMemcpy(job.probe_host + k * c, idx + (int64_t)b * c, sizeof(uint32_t) * c,
+                                             cudaMemcpyDeviceToHost));
+                }
+            }
         }
         if (!mjs.empty()) {
-            if (P.ran) MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.end, 0));  // the last round's readers of the lists
-            P.mk_list.ensure(list_used);
-            P.mk_info.ensure(info_used);
-            P.mk_max.ensure(MK_MAX_JOBS);
-            MLSK_CUDA(cudaMemsetAsync(P.mk_max.p, 0, MK_MAX_JOBS * sizeof(int32_t), P.s_gen));
-            // count scratch: groups of samples within 256 MiB
-            int64_t cnt_mb = 256;
-            if (const char* e = getenv("MLSK_MERGE_GROUP_MB")) cnt_mb = std::max<int64_t>(1, atoll(e));  // tests
-            const int64_t mk_tiles = (M.desc.n + MK_TILE - 1) / MK_TILE;
-            // (a launch's grid.y: at most 65535 samples per group)
-            const int64_t grp_cap = std::min<int64_t>(65535, std::max<int64_t>(1, (cnt_mb << 20) / (8 * M.desc.n)));
-            int64_t max_grp = 0;
-            for (size_t j = 0; j < jobs.size(); ++j)
-                if (mj_of[j] >= 0) max_grp = std::max(max_grp, std::min(grp_cap, job_cnt[j]));
-            const size_t cnt_need = (size_t)max_grp * (size_t)M.desc.n;
-            if (cnt_need > P.mk_cnt.n) {
-                P.mk_cnt.ensure(cnt_need);
-                P.mk_cnt.zero(P.s_gen);
-            }
-            P.mk_tile.ensure((size_t)max_grp * (size_t)mk_tiles);
-            Prof p("merge_columns", P.s_gen);
-            for (size_t j = 0; j < jobs.size(); ++j) {
-                if (mj_of[j] < 0) continue;
-                const MergeJob& mj = mjs[mj_of[j]];
-                const int64_t c = jobs[j].lv.c, cc = jobs[j].lv.cc;
-                const double w_fine = n / (double)c * kRescalePerturb;
-                const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;
-                for (int64_t off = 0; off < job_cnt[j]; off += grp_cap) {
-                    const int64_t g = std::min(grp_cap, job_cnt[j] - off);
-                    const int64_t work = g * ((c + 1) / 2);
-                    k_mk_count<<<(int)std::min<int64_t>((work + 255) / 256, (int64_t)sms * 16), 256, 0, P.s_gen>>>(
-                        M.dm, a.seed, jobs[j].lv.tag, P.ks.p + job_off[j] + off, g, c, cc, P.mk_cnt.p);
-                    MkEntry* list = P.mk_list.p + mj.list_off + (size_t)off * mj.stride;
-                    MkInfo* info = P.mk_info.p + mj.info_off + off;
-                    const dim3 tg((unsigned)mk_tiles, (unsigned)g);
-                    k_mk_tiles<<<tg, MK_T, 0, P.s_gen>>>(P.mk_cnt.p, M.desc.n, mj.mode, w_fine, w_coarse, P.mk_tile.p);
-                    k_mk_scan<<<(int)g, MK_T, 0, P.s_gen>>>(P.mk_tile.p, (int)mk_tiles, (int)KCOLS, list, mj.stride,
-                                                           info, P.mk_max.p + mj_of[j]);
-                    k_mk_write<<<tg, MK_T, 0, P.s_gen>>>(P.mk_cnt.p, M.desc.n, mj.mode, w_fine, w_coarse, (int)KCOLS,
-                                                         P.mk_tile.p, info, list, mj.stride);
-                    launched(4);
-                }
-            }
-            MLSK_CUDA(cudaMemcpyAsync(P.mk_max_host, P.mk_max.p, mjs.size() * sizeof(int32_t), cudaMemcpyDeviceToHost,
-                                      P.s_gen));
-            MLSK_CUDA(cudaEventRecord(P.mk_done, P.s_gen));
-            MLSK_CUDA(cudaEventSynchronize(P.mk_done));
-            for (size_t q = 0; q < mjs.size(); ++q) mjs[q].nk = std::max<int64_t>(1, P.mk_max_host[q]);
+            MLSK_CUDA(cudaEventRecord(P.mk_info_done[P.mk_parity], P.s_mm));
+            P.mk_info_used[P.mk_parity] = true;
         }
-    }
-    auto job_chunks = [&](size_t j) {
-        return mj_of[j] >= 0 ? mjs[mj_of[j]].nk : E.nchunks(jobs[j].lv.c, jobs[j].lv.cc);
-    };
-    auto with_merge = [&](KRange kr, size_t j, int64_t off) {
-        if (mj_of[j] >= 0) {
-            const MergeJob& mj = mjs[mj_of[j]];
-            if (kr.nkc < 0) kr.nkc = mj.nk;
-            kr.mk = P.mk_list.p + mj.list_off + (size_t)off * mj.stride;
-            kr.mk_stride = mj.stride;
-            kr.mk_info = P.mk_info.p + mj.info_off + off;
-        }
-        return kr;
-    };
-
-    // panel bytes a batch of nb samples needs in its buffer.  Merged chunk
-    // counts vary a little from round to round (they follow the draws), and a
-    // buffer that grew with every new maximum would be reallocated for many
-    // rounds: merged batches reserve 3% + 64 MiB of headroom, capped at the
-    // unmerged size.
-    auto reserve_bytes = [&](size_t j, int64_t nb, int64_t chunks) {
-        const int64_t need = nb * chunks * E.chunk_bytes();
-        if (mj_of[j] < 0) return need;
-        const int64_t ub = nb * E.nchunks(jobs[j].lv.c, jobs[j].lv.cc) * E.chunk_bytes();
-        const int64_t q = int64_t(64) << 20;
-        return std::min(ub, (need + need / 32 + q - 1) / q * q);
-    };
-    // Level order (each level has its own accumulators, so the order changes no
-    // result): the pipeline's tail is the last batch's GEMM with no generator
-    // left to overlap, its head the first batch's generator alone.  When one
-    // sample's panels exceed a batch (configs 4 / 5: long single-sample GEMMs at
-    // the deep levels) the levels run deepest first, so that those GEMMs run
-    // over the other levels' generators instead of ending the round alone
-    // (config 4: 13.2 -> 12.75 ms per step, config 5: 345 -> 341); with many
-    // samples per batch at every level (configs 2 / 3) the order is neutral to
-    // slightly worse (19.73 -> 19.90 ms) and stays ascending.
-    // MLSK_LEVEL_ORDER=asc|desc overrides.
-    std::vector<size_t> level_order(jobs.size());
-    for (size_t j = 0; j < jobs.size(); ++j) level_order[j] = j;
-    {
-        bool desc = false;
-        for (size_t j = 0; j < jobs.size(); ++j)
-            if (job_cnt[j] > 0 && job_chunks(j) * E.chunk_bytes() > budget) desc = true;
-        if (const char* e = getenv("MLSK_LEVEL_ORDER")) desc = e[0] == 'd';
-        if (desc)
-            std::stable_sort(level_order.begin(), level_order.end(),
-                             [&](size_t x, size_t y) { return jobs[x].lv.c > jobs[y].lv.c; });
-    }
-    std::vector<Batch> batches;
-    int64_t max_panel = 0;
-    for (size_t j : level_order) {
-        const int64_t per = job_chunks(j) * E.chunk_bytes();
-        const int64_t total = job_cnt[j];
-        if (per > split_limit && E.splits_k()) {
-            if (nl)
-                throw Error(MLSK_EINVAL, "fused engine: nonlinear targets need a level-sample's panels within one "
-                                         "batch (" + std::to_string(split_limit >> 20) + " MiB)");
-            // one sample's panels exceed a batch: K-segments of one sample each,
-            // the partial Y carried between them
-            if (jobs[j].probe_host)
-                throw Error(MLSK_EINVAL, "probe: not available for level-samples split along K (panels > " + std::to_string(split_limit >> 20) + " MiB)");
-            const int64_t nk = job_chunks(j);
-            const int64_t seg = std::max<int64_t>(1, split_limit / E.chunk_bytes());  // few, large segments
-            for (int64_t off = 0; off < total; ++off)
-                for (int64_t k0 = 0; k0 < nk; k0 += seg) {
-                    KRange kr;
-                    kr.kc0 = k0;
-                    kr.nkc = std::min(seg, nk - k0);
-                    kr.part = nk <= seg ? 0 : (k0 == 0 ? 1 : (k0 + kr.nkc == nk ? 3 : 2));
-                    batches.push_back({j, off, 1, job_off[j] + off, with_merge(kr, j, off)});
-                    max_panel = std::max(max_panel, reserve_bytes(j, 1, kr.nkc));
-                }
-            continue;
-        }
-        int64_t max_nb = std::max<int64_t>(1, budget / per);
-        // every CTA group needs a sample: stretch the batch (up to 4x the budget)
-        // rather than leave groups idle (config 3's deepest level: 268 MB samples)
-        if (max_nb < Gs && Gs * per <= 4 * budget) max_nb = Gs;
-        if (max_nb > Gs) max_nb = max_nb / Gs * Gs;
-        for (int64_t off = 0; off < total; off += max_nb) {
-            const int nb = (int)std::min<int64_t>(max_nb, total - off);
-            batches.push_back({j, off, nb, job_off[j] + off, with_merge(KRange{}, j, off)});
-            max_panel = std::max(max_panel, reserve_bytes(j, nb, job_chunks(j)));
-        }
-    }
-    if ((size_t)(max_panel + 7) / 8 > P.panels[0].n) {
-        // the buffers must grow: one level-sample's panels must fit a buffer;
-        // fail with a clear message instead of an opaque allocation error
-        // (queried only when growing: cudaMemGetInfo on every round stalled
-        // the launching thread for milliseconds now and then)
-        size_t free_b = 0, total_b = 0;
-        MLSK_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        size_t held = 0;
-        for (int i = 0; i < NBUF; ++i) held += P.panels[i].n * sizeof(double);
-        if ((double)NBUF * (double)max_panel > (double)(free_b + held))
-            throw Error(MLSK_ERUNTIME, "fused engine: the sampled panels of one batch (" +
-                                           std::to_string(max_panel >> 20) + " MiB x " + std::to_string(NBUF) +
-                                           " buffers) exceed free device memory; use a smaller c_l or m, p");
-    }
-    for (int i = 0; i < NBUF; ++i) P.panels[i].ensure((size_t)(max_panel + 7) / 8);
-
-    for (size_t i = 0; i < batches.size(); ++i) {
-        const Batch& bt = batches[i];
-        FusedJob& job = jobs[bt.job];
-        const int64_t c = job.lv.c, cc = job.lv.cc;
-        const double w_fine = n / (double)c * kRescalePerturb;                                        // n/c
-        const double w_coarse = cc > 0 && !nl ? w_fine - n / (double)cc : w_fine;  // n/c - n/cc on the prefix
-        const int buf = (int)(i % NBUF);
-        void* panels = P.panels[buf].p;
-        uint32_t* idx = nullptr;
-        if (job.probe_host) {
-            P.idx[buf].ensure((size_t)bt.nb * c);
-            idx = P.idx[buf].p;
-        }
-        // generator: wait until the GEMM that last used this buffer is done
-        if (P.used[buf]) MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.mm_done[buf], 0));
-        if (serial_mode() && i > 0) MLSK_CUDA(cudaStreamWaitEvent(P.s_gen, P.mm_done[(i - 1) % NBUF], 0));
-        E.gen(P.s_gen, a.seed, job.lv.tag, P.ks.p + bt.ks_off, bt.nb, c, cc, w_fine, w_coarse, panels, idx, bt.kr);
-        MLSK_CUDA(cudaEventRecord(P.gen_done[buf], P.s_gen));
-        // GEMM + fused level epilogue + fixed-order reduction
-        MLSK_CUDA(cudaStreamWaitEvent(P.s_mm, P.gen_done[buf], 0));
-        E.gemm(P.s_mm, panels, bt.nb, c, cc, w_fine, w_coarse, *job.st, bt.kr);
-        {
-            const int64_t full = E.nchunks(c, cc);
-            const int64_t k = bt.kr.nkc >= 0 ? bt.kr.nkc : full;
-            g_columns[0] += (int64_t)bt.nb * k * E.chunk_cols();
-            // (a K-split sample's segments add up to its merged chunks; its c indices count once)
-            g_columns[1] += bt.kr.part == 0 || bt.kr.part == 1 ? (int64_t)bt.nb * c : 0;
-        }
-        MLSK_CUDA(cudaEventRecord(P.mm_done[buf], P.s_mm));
-        P.used[buf] = true;
-        if (idx) {
-            MLSK_CUDA(cudaStreamSynchronize(P.s_gen));
-            for (int b = 0; b < bt.nb; ++b) {
-                const int64_t k = jks[bt.job][bt.off + b];
-                if (k < a.probe_k)
-                    MLSK_CUDA(cudaMemcpy(job.probe_host + k * c, idx + (int64_t)b * c, sizeof(uint32_t) * c,
-                                         cudaMemcpyDeviceToHost));
-            }
-        }
-    }
+    }  // passes
     for (auto& job : jobs) {
         int64_t cnt = 0;
         for (const auto& sg : job.segs) cnt += sg.count;

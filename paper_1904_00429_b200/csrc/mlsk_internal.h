@@ -134,6 +134,7 @@ void once_per_device(const void* tag, F&& f) {
 }
 
 struct Model {
+    uint64_t serial = 0;  // unique per built model (build_model): "same model as the last round"
     mlsk_model_desc desc{};
     DevModel dm{};
     bool vector = false;

@@ -4,6 +4,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <atomic>
+
 #include "mlsk_internal.h"
 
 namespace mlsk {
@@ -130,6 +132,8 @@ bool model_is_vector(const mlsk_model_desc* d) {
 
 void build_model(Model& M, const mlsk_model_desc* d, cudaStream_t st) {
     if (!d) invalid("model: null descriptor");
+    static std::atomic<uint64_t> next_serial{1};
+    M.serial = next_serial.fetch_add(1);
     M.desc = *d;
     mlsk_model_desc& D = M.desc;
     const int k = D.kind;

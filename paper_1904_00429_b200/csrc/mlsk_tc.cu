@@ -528,7 +528,25 @@ constexpr int RFF_RSPLIT = 4;              // work items per column group (row-b
 #define MLSK_RFF_MINB 3  // 79 registers, 3 CTAs per SM: config 4 16.70 -> 16.37 ms per step (4: 16.70)
 #endif
 constexpr int RFF_T = GEN_T, RFF_RB = TBM, RFF_MINB = MLSK_RFF_MINB;
-constexpr int RFF_SMEM = (RFF_DMAX * RFF_RB + RFF_DMAX * RFF_COLS) * 4;  // X tile + W columns (40 KB)
+// MLSK_RFF_MMA (default): the 128 x 32 x D phase products of a row block run on
+// the tensor cores as 3xTF32 mma.sync (m16n8k8, one 16-row slab x four 8-column
+// tiles per warp; hi x hi in one accumulator, the two cross terms in another,
+// summed at the end: the large accumulator sees 8 MMAs, not 24) instead of 64
+// FFMAs per entry: 0.38 k instead of 1.15 k instructions per thread and row
+// block ahead of the cos / split / store epilogue.  The X and W tiles are
+// padded by 8 floats per row so the fragment loads are conflict-free.
+#ifndef MLSK_RFF_MMA
+#define MLSK_RFF_MMA 1
+#endif
+constexpr int RFF_XS = MLSK_RFF_MMA ? RFF_RB + 8 : RFF_RB;      // X tile row stride (floats)
+constexpr int RFF_WS = MLSK_RFF_MMA ? RFF_COLS + 8 : RFF_COLS;  // W tile row stride
+constexpr int RFF_SMEM = (RFF_DMAX * RFF_XS + RFF_DMAX * RFF_WS) * 4;  // X tile + W columns (40 / 44 KB)
+
+__device__ __forceinline__ void mma_tf32_16x8x8(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
 
 // work item (b, column group of 32 sampled columns, range of 128-row blocks):
 // W columns and (per row block) the X tile in shared memory; each thread
@@ -543,12 +561,13 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                  uint32_t* __restrict__ idx_out, const MkEntry* __restrict__ mk, int64_t mk_stride,
                  const MkInfo* __restrict__ mk_info) {
     extern __shared__ __align__(1024) unsigned char rsm[];
-    float* xs = reinterpret_cast<float*>(rsm);  // [D][128]
-    float* wsm = xs + RFF_DMAX * RFF_RB;         // [D][RFF_COLS]
+    float* xs = reinterpret_cast<float*>(rsm);  // [D][RFF_XS]
+    float* wsm = xs + RFF_DMAX * RFF_XS;         // [D][RFF_WS]
     __shared__ int s_j[RFF_COLS];
     __shared__ float s_w[RFF_COLS], s_b[RFF_COLS];
     const DevModel& M = S.M;
     const int D = (int)M.rff_dim;
+    const int D8 = MLSK_RFF_MMA ? (D + 7) & ~7 : D;
     const int tid = threadIdx.x;
     const float scale = (float)M.rff_scale;
     const int64_t ngrp = (nkc + RFF_CH - 1) / RFF_CH;  // column groups of RFF_CH K-chunks
@@ -556,8 +575,10 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
     const int64_t rb_per = (nrb + RFF_RSPLIT - 1) / RFF_RSPLIT;
     const int64_t items = (int64_t)nb * ngrp * RFF_RSPLIT;
     static_assert(RFF_COLS == 32 && RFF_T == 2 * RFF_RB && TBM % RFF_RB == 0, "4 x 4 thread tile map");
+#if !MLSK_RFF_MMA
     const int t0 = 4 * (tid & 7), r0 = 4 * (tid >> 3);
     const int ch = t0 / TBK, tt = t0 % TBK;
+#endif
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const int64_t cgi = it / RFF_RSPLIT;
         const int rs = (int)(it - cgi * RFF_RSPLIT);
@@ -588,11 +609,13 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
             s_b[tid] = j >= 0 ? M.rff_b[j] : 0.f;
         }
         __syncthreads();
-        for (int e = tid; e < D * RFF_COLS; e += RFF_T) {
+        for (int e = tid; e < D8 * RFF_COLS; e += RFF_T) {  // (rows D .. D8: zero K padding of the MMAs)
             const int d = e / RFF_COLS, t = e - d * RFF_COLS;
             const int j = s_j[t];
-            wsm[d * RFF_COLS + t] = j >= 0 ? M.rff_w[(int64_t)d * M.n + j] : 0.f;
+            wsm[d * RFF_WS + t] = j >= 0 && d < D ? M.rff_w[(int64_t)d * M.n + j] : 0.f;
         }
+        const bool colscale = mk != nullptr && !write_b;
+#if !MLSK_RFF_MMA
         // this thread's columns: index, phase and weight are fixed over the item
         int jv[4];
         float bv[4], wv4[4];
@@ -604,7 +627,7 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
         }
         const int64_t kc = kc0 + ch;
         const bool col_ok = kc < nkc;
-        const bool colscale = mk != nullptr && !write_b;
+#endif
         const int64_t rb_end = nrb < (rs + 1) * rb_per ? nrb : (rs + 1) * rb_per;
         for (int64_t rbi = rs * rb_per; rbi < rb_end; ++rbi) {
             const int64_t rb = rbi * RFF_RB;
@@ -612,19 +635,86 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
             __syncthreads();  // previous X tile consumed
             // X tile from the transposed copy: rows contiguous per dimension, so
             // the global reads coalesce and the shared stores are conflict-free
-            if (lim >= RFF_RB && (M.m & 3) == 0) {
+            if (lim >= RFF_RB && (M.m & 3) == 0 && D8 == D) {
                 for (int e = tid; e < RFF_RB / 4 * D; e += RFF_T) {
                     const int d = e / (RFF_RB / 4), r4 = e - d * (RFF_RB / 4);
-                    reinterpret_cast<float4*>(xs + d * RFF_RB)[r4] =
+                    reinterpret_cast<float4*>(xs + d * RFF_XS)[r4] =
                         __ldg(reinterpret_cast<const float4*>(M.rff_xt + (int64_t)d * M.m + rb) + r4);
                 }
             } else {
-                for (int e = tid; e < RFF_RB * D; e += RFF_T) {
+                for (int e = tid; e < RFF_RB * D8; e += RFF_T) {
                     const int d = e / RFF_RB, r = e - d * RFF_RB;
-                    xs[d * RFF_RB + r] = r < lim ? M.rff_xt[(int64_t)d * M.m + rb + r] : 0.f;
+                    xs[d * RFF_XS + r] = r < lim && d < D ? M.rff_xt[(int64_t)d * M.m + rb + r] : 0.f;
                 }
             }
             __syncthreads();
+#if MLSK_RFF_MMA
+            // warp = rows 16 warp .. +15 of the block x the item's 32 columns
+            const int lane = tid & 31, wrp = tid >> 5, g = lane >> 2, tq = lane & 3;
+            float cm[4][4], cx[4][4];  // [n8 tile][fragment]: hi x hi, and the cross terms
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) cm[nt][q] = cx[nt][q] = 0.f;
+            const float* xa = xs + 16 * wrp + g;
+            const float* wb = wsm + g;
+            for (int k0 = 0; k0 < D8; k0 += 8) {
+                // A fragment (rows g, g + 8; k = tq, tq + 4): the mma reads the
+                // TF32 part of the fp32 word (hi); lo = x - tf32(x)
+                uint32_t ah[4], al[4];
+                const float a0 = xa[(k0 + tq) * RFF_XS], a1 = xa[(k0 + tq) * RFF_XS + 8];
+                const float a2 = xa[(k0 + tq + 4) * RFF_XS], a3 = xa[(k0 + tq + 4) * RFF_XS + 8];
+                ah[0] = __float_as_uint(a0); ah[1] = __float_as_uint(a1);
+                ah[2] = __float_as_uint(a2); ah[3] = __float_as_uint(a3);
+                al[0] = __float_as_uint(tf32_lo(a0)); al[1] = __float_as_uint(tf32_lo(a1));
+                al[2] = __float_as_uint(tf32_lo(a2)); al[3] = __float_as_uint(tf32_lo(a3));
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                    const float b0 = wb[(k0 + tq) * RFF_WS + 8 * nt], b1 = wb[(k0 + tq + 4) * RFF_WS + 8 * nt];
+                    const uint32_t bh[2] = {__float_as_uint(b0), __float_as_uint(b1)};
+                    const uint32_t bl[2] = {__float_as_uint(tf32_lo(b0)), __float_as_uint(tf32_lo(b1))};
+                    mma_tf32_16x8x8(cm[nt], ah, bh);
+                    mma_tf32_16x8x8(cx[nt], ah, bl);
+                    mma_tf32_16x8x8(cx[nt], al, bh);
+                }
+            }
+            const int64_t rt = rb & ~(int64_t)(TBM - 1);  // the 128-row panel tile holding this block
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+                const int cl = 8 * nt + 2 * tq;  // this thread's two adjacent columns of the item
+                const int64_t kcn = kc0 + cl / TBK;
+                if (kcn >= nkc) continue;
+                const int ttn = cl % TBK;
+                const int j0 = s_j[cl], j1 = s_j[cl + 1];
+                const float b0 = s_b[cl], b1 = s_b[cl + 1], w0 = s_w[cl], w1 = s_w[cl + 1];
+                const int64_t oa = ((b * nkc + kcn) * MP + rt) * TBK;
+                const int64_t ob = ((b * nkc + kcn) * PP + rt) * TBK;  // B panels are padded to 256
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int rr = 16 * wrp + g + 8 * h;  // row within the block
+                    float z0 = 0.f, z1 = 0.f;
+                    if (rr < lim) {
+                        if (j0 >= 0) z0 = scale * cosf(__fadd_rn(cm[nt][2 * h], cx[nt][2 * h]) + b0);
+                        if (j1 >= 0) z1 = scale * cosf(__fadd_rn(cm[nt][2 * h + 1], cx[nt][2 * h + 1]) + b1);
+                    }
+                    // merged columns on the shared panel: |w| is the column scale sqrt(reps)
+                    if (colscale) {
+                        z0 = __fmul_rn(fabsf(w0), z0);
+                        z1 = __fmul_rn(fabsf(w1), z1);
+                    }
+                    const int off = sw_off((int)(rb - rt) + rr, ttn) / 4;  // floats
+                    if (rb < MP) {
+                        *reinterpret_cast<float2*>(Ahi + oa + off) = make_float2(z0, z1);
+                        *reinterpret_cast<float2*>(Alo + oa + off) = make_float2(tf32_lo(z0), tf32_lo(z1));
+                    }
+                    if (write_b && rb < PP) {
+                        const float v0 = __fmul_rn(w0, z0), v1 = __fmul_rn(w1, z1);
+                        *reinterpret_cast<float2*>(Bhi + ob + off) = make_float2(v0, v1);
+                        *reinterpret_cast<float2*>(Blo + ob + off) = make_float2(tf32_lo(v0), tf32_lo(v1));
+                    }
+                }
+            }
+#else
             // per dimension one 16-byte W read and one 16-byte X read (both
             // broadcast within the warp) feed 16 FMAs; each entry sums over d
             // in order (rff_entry)
@@ -635,8 +725,8 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                 for (int q = 0; q < 4; ++q) acc[i][q] = 0.f;
 #pragma unroll 4
             for (int d = 0; d < D; ++d) {
-                const float4 wv = *reinterpret_cast<const float4*>(wsm + d * RFF_COLS + t0);
-                const float4 xv = *reinterpret_cast<const float4*>(xs + d * RFF_RB + r0);
+                const float4 wv = *reinterpret_cast<const float4*>(wsm + d * RFF_WS + t0);
+                const float4 xv = *reinterpret_cast<const float4*>(xs + d * RFF_XS + r0);
                 const float xa[4] = {xv.x, xv.y, xv.z, xv.w}, wa[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
@@ -671,6 +761,7 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                         make_float4(tf32_lo(v[0]), tf32_lo(v[1]), tf32_lo(v[2]), tf32_lo(v[3]));
                 }
             }
+#endif
         }
     }
 }

@@ -114,6 +114,14 @@ def test_merge_fp64_sample_groups(gpu):
     three_way(gpu, model, 2, 2, [70, 40, 33], 256, TOL64, extra_env={"MLSK_MERGE_GROUP_MB": 1}, exact=False)
 
 
+def test_merge_passes(gpu):
+    """the lists bounded to 1 MiB: the round runs as several passes over slices of every level's samples"""
+    model = gpu.gaussian_mean_matrix_model(64, 4096, 64, sd=0.5, data_seed=13)
+    three_way(gpu, model, 2, 2, [150, 90, 77], 256, TOL64, extra_env={"MLSK_MERGE_LIST_MB": 1}, exact=False)
+    model32 = gpu.gaussian_mean_matrix_model(256, 2048, 256, sd=1.0, data_seed=14, dtype=abi.F32)
+    three_way(gpu, model32, 2, 3, [40, 30, 20, 10], 256, TOL32, extra_env={"MLSK_MERGE_LIST_MB": 1}, exact=False)
+
+
 def test_merge_fp32_gauss(gpu):
     model = gpu.gaussian_mean_matrix_model(256, 2048, 512, sd=1.0, data_seed=14, dtype=abi.F32)
     three_way(gpu, model, 2, 4, [4, 3, 3, 2, 2], 128, TOL32)
