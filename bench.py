@@ -376,11 +376,16 @@ def main():
         try:
             pj = json.load(open(prof_json))
             ratio = pj.get("dram_over_algorithmic")
-            traffic = ratio * args.steps * panel_bytes_of(STEP_N) / gemm["launches"] if ratio else None
+            traffic = (ratio * (contraction["executed_over_sampled"] or 1.0) * args.steps * panel_bytes_of(STEP_N)
+                       / gemm["launches"]) if ratio else None
             sr = pj.get("step_dram_over_algorithmic")
             if sr:  # generator + GEMM DRAM bytes of a whole step (not the GEMM's reads alone)
-                step_traffic = {"dram_bytes_per_step": sr * panel_bytes_of(STEP_N),
-                                "algorithmic_bytes_per_step": panel_bytes_of(STEP_N), "ratio": sr,
+                # the captured ratio is per batch of panels; with merged sampled columns the step
+                # generates and reads panels for the executed columns only
+                ex = contraction["executed_over_sampled"] or 1.0
+                step_traffic = {"dram_bytes_per_step": sr * ex * panel_bytes_of(STEP_N),
+                                "algorithmic_bytes_per_step": panel_bytes_of(STEP_N), "ratio": sr * ex,
+                                "per_batch_ratio": sr, "executed_over_sampled_columns": ex,
                                 "source": pj.get("source")}
         except Exception:
             traffic = None

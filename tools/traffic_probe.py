@@ -27,7 +27,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 KERNELS = "k_gemm_tf32x3|k_gen_panels|k_reduce_tiles_tc|k_mirror_lower|k_kpar_combine|k_sum_sq|" \
-          "k_fused_inner|k_reduce_inner|k_expand_ks"
+          "k_fused_inner|k_reduce_inner|k_expand_ks|k_mk_"
 METRICS = "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum"
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "nsecond": 1e-3, "us": 1.0,
          "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
