@@ -1807,6 +1807,14 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
                                                " buffers) exceed free device memory; use a smaller c_l or m, p");
         }
         for (int i = 0; i < NBUF; ++i) P.panels[i].ensure((size_t)(max_panel + 7) / 8);
+        {
+            // KRange::finish: only a level's last batch of the pass
+            std::vector<char> seen(jobs.size(), 0);
+            for (size_t q = batches.size(); q-- > 0;) {
+                batches[q].kr.finish = !seen[batches[q].job];
+                seen[batches[q].job] = 1;
+            }
+        }
 
         for (size_t bi = 0; bi < batches.size(); ++bi, ++P.batch_seq) {
             const size_t i = (size_t)P.batch_seq;  // buffers rotate across passes and rounds

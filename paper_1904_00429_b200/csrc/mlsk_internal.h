@@ -287,6 +287,7 @@ struct MkInfo {
 struct KRange {
     int64_t kc0 = 0, nkc = -1;
     int part = 0;
+    bool finish = true;  // the level's last batch of this pass (symmetric outputs are mirrored then)
     const MkEntry* mk = nullptr;
     int64_t mk_stride = 0;
     const MkInfo* mk_info = nullptr;

@@ -1509,15 +1509,19 @@ class TcEngine final : public PanelEngine {
                                 dim3(32, 8), 0, s>>>(part, part_sq, sh, direct ? 0 : M_.rows, M_.cols, st.total(),
                                                      st.total_sq(), segmented(k) ? 1 : 0);
         }
-        if (sym_nb_) {
+        launched(2);
+        // symmetric output: the lower blocks are copied from the upper ones once
+        // per level and pass (KRange::finish), after the level's last reduction
+        // (a per-batch reduction stream with double-buffered partials was measured
+        // too: config 3 14.4 -> 15.3 ms -- the generator fills the SMs during the
+        // reductions, so taking them off the GEMM stream only starves it)
+        if (sym_nb_ && kr.finish) {
             Prof p("mirror_tc", s);
             const int64_t n = M_.rows;
             k_mirror_lower<<<(int)std::min<int64_t>((n / 32) * (n / 32), (int64_t)nsm_ * 8), dim3(32, 8), 0, s>>>(
                 st.total(), n);
-            launched(3);
-            return;
+            launched();
         }
-        launched(2);
     }
 
    private:
