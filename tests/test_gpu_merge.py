@@ -175,3 +175,37 @@ def test_merge_default_threshold(gpu):
     for l in (1, 2):
         assert frob_rel(rm.per_level[l].sum, ru.per_level[l].sum) <= TOL64
         assert not np.array_equal(np.asarray(rm.per_level[l].sum), np.asarray(ru.per_level[l].sum))
+
+
+def test_merge_rank_shards_add_up(gpu):
+    """64-replication chunk sharding (rank / world) with merged columns: the two ranks'
+    level sums add up to the single-rank run (each sample's list depends on (seed, l, k) only)."""
+    model = gpu.gaussian_mean_matrix_model(96, 2048, 80, sd=0.5, data_seed=21)
+    N = [200, 150, 130]
+    plan = gpu.LevelPlan(2, 2, N, c0=256)
+    with env(MLSK_MERGE=None, MLSK_MERGE_MIN_DEN=1 << 30):
+        one, names = profiled_names(
+            lambda: gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER, gpu.EstimatorOptions(engine="fused")))
+        parts = [gpu.mlmc_matmul(model, gpu.target_identity(), plan, MASTER,
+                                 gpu.EstimatorOptions(engine="fused", rank=r, world=2)) for r in range(2)]
+    assert "merge_columns" in names
+    for l in range(3):
+        assert parts[0].per_level[l].replication_count + parts[1].per_level[l].replication_count == N[l]
+        s = np.asarray(parts[0].per_level[l].sum) + np.asarray(parts[1].per_level[l].sum)
+        assert frob_rel(s, one.per_level[l].sum) <= TOL64
+        sq = parts[0].per_level[l].sum_of_squares + parts[1].per_level[l].sum_of_squares
+        assert abs(sq - one.per_level[l].sum_of_squares) <= TOL64 * one.per_level[l].sum_of_squares
+
+
+def test_merge_single_level_mc(gpu):
+    """the single-level MC baseline (no coarse prefix: duplicates merge, nothing cancels)"""
+    model = gpu.gaussian_mean_matrix_model(128, 1024, 128, sd=0.5, data_seed=22)
+    kw = dict(L=3, N=12, M=2, seed=MASTER, c0=128)  # s = 128 * 2^3 = 1024 = n
+    with env(MLSK_MERGE=None, MLSK_MERGE_MIN_DEN=None):
+        rm, names = profiled_names(lambda: gpu.mc_matmul(model, gpu.target_identity(), options=gpu.EstimatorOptions(engine="fused"), **kw))
+    assert "merge_columns" in names
+    with env(MLSK_MERGE=0):
+        ru = gpu.mc_matmul(model, gpu.target_identity(), options=gpu.EstimatorOptions(engine="fused"), **kw)
+    re_ = gpu.mc_matmul(model, gpu.target_identity(), options=gpu.EstimatorOptions(engine="exact"), **kw)
+    assert frob_rel(rm.value, ru.value) <= TOL64 and frob_rel(rm.value, re_.value) <= TOL64
+    assert not np.array_equal(np.asarray(rm.value), np.asarray(ru.value))
