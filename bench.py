@@ -57,6 +57,11 @@ def flops_of(N):
     return sum(2.0 * M_ * P_ * C0 * 2 ** l * n for l, n in enumerate(N))
 
 
+def ref_convention_flops_of(N):
+    """The reference's own cost convention (two passes, estimators.cpp:137-147): 2 m p (c_l + c_{l-1})."""
+    return sum(2.0 * M_ * P_ * (C0 * 2 ** l + (C0 * 2 ** (l - 1) if l > 0 else 0)) * n for l, n in enumerate(N))
+
+
 def panel_bytes_of(N):
     """Algorithmic bytes the GEMM reads: the sampled columns of A and rows of B (fp64)."""
     return sum(8.0 * (M_ + P_) * C0 * 2 ** l * n for l, n in enumerate(N))
@@ -419,6 +424,10 @@ def main():
                                       warm=f"{GPU_WARM_S} s of device memory writes and DMMA work before the "
                                            f"{args.warmup} warm-up steps"),
                 "sampled_gemm_tflops": flops_total / (total_ms * 1e-3) / 1e12,
+                # roofline_time / measured_time of the whole step (flops-bound), and the
+                # reference-convention rate (fine and coarse as two passes: 2 m p (c_l + c_{l-1}))
+                "step_frac_of_peak": (flops_total / world / (total_ms * 1e-3) / 1e12 / peak) if peak > 0 else None,
+                "reference_convention_tflops": args.steps * ref_convention_flops_of(dN) / (total_ms * 1e-3) / 1e12,
                 "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                              "frac": (achieved / peak) if achieved and peak > 0 else None,
                              "traffic": traffic, "kernel": "k_gemm_f64 (DMMA m8n8k4, fp64)",

@@ -276,6 +276,9 @@ def measure(ids, steps=3, with_cpu=True, device=0):
             which = f"sustained: {sus_note}" if long_region else "burst"
             blk["sampled_gemm_tflops"] = sum(2.0 * c["m"] * c["p"] * cl * n for cl, n in zip(levels_c, c["N"])) \
                 / (ms * 1e-3) / 1e12
+            blk["reference_convention_tflops"] = sum(
+                2.0 * c["m"] * c["p"] * (cl + (levels_c[l - 1] if l > 0 else 0)) * n
+                for l, (cl, n) in enumerate(zip(levels_c, c["N"]))) / (ms * 1e-3) / 1e12
             blk["algorithmic_tflops"] = flops / (ms * 1e-3) / 1e12
             blk["step_frac_of_peak"] = blk["algorithmic_tflops"] / (peak_t / 3)
             blk["peaks_tf32"] = {"burst": tf32, "sustained": tf32_sus, "used": which}

@@ -409,6 +409,9 @@ __device__ __forceinline__ void student_t_phase_f32(const TcModel& S, const Tabl
 // by the TMA engine.
 // KIND: GK_GAUSS, GK_STUDENT_T, or GK_GENERIC (per-entry loop: RFF with D > 64)
 constexpr int GK_GAUSS = 0, GK_STUDENT_T = 1, GK_GENERIC = 2;
+#ifndef MLSK_GEN_CHUNK_MAJOR
+#define MLSK_GEN_CHUNK_MAJOR 1
+#endif
 template <int KIND>
 #ifndef MLSK_GAUSS_MINB
 #define MLSK_GAUSS_MINB 5  // gauss: 4 / 5 / 6 CTAs per SM -> config 3 16.1 / 15.6 / 16.1 ms per step
@@ -438,8 +441,11 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
     const int a_ph = (int)(MP / TBM), b_ph = (int)(PP / TBM);  // 128-row phases (a B tile is two)
     int buf = 0;
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int b = (int)(it / nkc);
-        const int64_t kc = it - (int64_t)b * nkc;
+        // merged lists are ordered by column, so chunk kc of every sample covers about
+        // the same columns: chunk-major item order lets the CTAs running at one time
+        // gather the same mean rows (L2 hits); draw-order lists run sample-major
+        const int b = (int)(MLSK_GEN_CHUNK_MAJOR && mk ? it % nb : it / nkc);
+        const int64_t kc = MLSK_GEN_CHUNK_MAJOR && mk ? it / nb : it - (int64_t)b * nkc;
         const uint64_t key = derive_seed(seed, tag, (uint64_t)ks[b]);
         __syncthreads();
         if (tid < TBK) {
