@@ -248,7 +248,8 @@ int mlsk_profile_reset(void);
 int mlsk_profile_read(int i, char* name, int name_len, int64_t* launches, double* ms);
 /* Start / end (ms since the last reset) of profiled launch i; returns the count. */
 int mlsk_profile_timeline(int i, char* name, int name_len, double* t0, double* t1);
-/* Merged sampled columns (identity target, levels with c >= n / 16: a
+/* Merged sampled columns (identity target, the deep levels -- c >= n / 16 or
+ * so -- where it saves K-chunks: a
  * level-sample's contraction runs over its DISTINCT sampled columns with
  * summed weights -- a duplicated index gathers the same drawn column,
  * sketch.cpp:60-71 -- and columns whose fine and coarse weights cancel drop

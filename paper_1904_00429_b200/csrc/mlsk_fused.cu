@@ -1392,8 +1392,7 @@ struct MergeJob {
 };
 
 // MLSK_MERGE=0 turns merged sampled columns off; MLSK_MERGE_MIN_DEN=d merges
-// the levels with c >= n / d (default 16: at c = n / 16 about 4.5% of the
-// columns merge or cancel, below that the pre-pass is not worth its launches)
+// the levels with c >= n / d instead of the levels where it pays (merge_pays)
 // (read every round: tests switch them in-process)
 bool merge_enabled() {
     const char* e = getenv("MLSK_MERGE");
@@ -1402,6 +1401,37 @@ bool merge_enabled() {
 int64_t merge_min_den() {
     const char* e = getenv("MLSK_MERGE_MIN_DEN");
     return e ? std::max<int64_t>(1, atoll(e)) : int64_t(16);
+}
+// Is merging worth its pre-pass for a level of c draws (coarse prefix cc) from n
+// columns, K-chunks of kcols?  The expected number of surviving columns is
+// n (1 - e^{-l} I_0(l)), l = c / n, when the prefix is half the draws with the
+// opposite weight (Skellam(l/2, l/2) multiplicity != 0), n (1 - e^{-l}) when
+// only duplicates merge; the launches are sized by the maximum over the level's
+// samples (~ mean + 3 sigma, sigma^2 <= the merged-away count) in whole chunks
+// (+ one chunk of padding per sign group).  Merge when that saves at least 3%
+// of the chunks: at config 2's c = 256 (16 chunks, 244.5 expected columns) it
+// saves none and the pre-pass is a net loss.  MLSK_MERGE_MIN_DEN set: the plain
+// c >= n / d rule (tests force merging with a large d).
+bool merge_pays(int64_t c, int64_t cc, int64_t n, int64_t kcols, bool cancels, int groups) {
+    if (getenv("MLSK_MERGE_MIN_DEN")) return c * merge_min_den() >= n;
+    if (c * 64 < n) return false;
+    const double l = (double)c / (double)n;
+    double keep;
+    if (cc > 0 && cancels && 2 * cc == c) {
+        double i0 = 0.0, term = 1.0;  // I_0(l) = sum (l/2)^{2k} / (k!)^2
+        for (int k = 1; k < 40; ++k) {
+            i0 += term;
+            term *= (l / 2) * (l / 2) / ((double)k * (double)k);
+        }
+        keep = (double)n * (1.0 - std::exp(-l) * i0);
+    } else {
+        keep = (double)n * (1.0 - std::exp(-l));  // distinct columns
+    }
+    const double away = std::max(0.0, (double)c - keep);
+    const double worst = keep + 3.0 * std::sqrt(away);
+    const double chunks = std::ceil(worst / (double)kcols) + (groups - 1);
+    const double full = (double)((c + kcols - 1) / kcols);
+    return chunks <= 0.97 * full && chunks <= full - 1.0;
 }
 
 }  // namespace
@@ -1602,12 +1632,14 @@ void fused_run_round(const RunArgs& a, std::vector<FusedJob>& jobs) {
     auto merge_stride = [&](int64_t c) { return (c + KCOLS - 1) / KCOLS * KCOLS + KCOLS; };
     auto merge_mode_of = [&](size_t j) {
         const int64_t c = jobs[j].lv.c, cc = jobs[j].lv.cc;
-        if (nl || !merge_enabled() || jobs[j].probe_host || jobs[j].lv.full || c * merge_min_den() < M.desc.n ||
-            c < 4 * KCOLS || M.desc.n > (int64_t(1) << 31) - 2)
+        if (nl || !merge_enabled() || jobs[j].probe_host || jobs[j].lv.full || c < 4 * KCOLS ||
+            M.desc.n > (int64_t(1) << 31) - 2)
             return 0;
         const double w_fine = n / (double)c * kRescalePerturb;
         const double w_coarse = cc > 0 ? w_fine - n / (double)cc : w_fine;
-        return E.merge_mode(c, cc, w_fine, w_coarse);
+        const int mode = E.merge_mode(c, cc, w_fine, w_coarse);
+        if (!mode || !merge_pays(c, cc, M.desc.n, KCOLS, w_coarse == -w_fine, mode == 2 ? 2 : 1)) return 0;
+        return mode;
     };
     int64_t list_mb = 1024;
     if (const char* e = getenv("MLSK_MERGE_LIST_MB")) list_mb = std::max<int64_t>(1, atoll(e));  // tests

@@ -163,18 +163,20 @@ def test_merge_rff_full_grid(gpu):
 
 
 def test_merge_default_threshold(gpu):
-    """default: only levels with c >= n / 16 merge; shallower levels are untouched bit for bit"""
+    """default: only the levels where merging saves K-chunks merge (mlsk_fused.cu merge_pays: at
+    c = 256 of n = 4096 the ~244 surviving columns still take 16 chunks, at c = 512 the ~467
+    take 30-31 of 32); the other levels are untouched bit for bit"""
     model = gpu.gaussian_mean_matrix_model(128, 4096, 128, sd=0.5, data_seed=19)
     N = [3, 3, 2]
     with env(MLSK_MERGE=None, MLSK_MERGE_MIN_DEN=None):
-        rm, names = profiled_names(lambda: run(gpu, model, 2, 2, N, 128))  # c = 128, 256, 512: only 256, 512
+        rm, names = profiled_names(lambda: run(gpu, model, 2, 2, N, 128))  # c = 128, 256, 512: only 512
     assert "merge_columns" in names
     with env(MLSK_MERGE=0):
         ru = run(gpu, model, 2, 2, N, 128)
-    assert np.array_equal(np.asarray(rm.per_level[0].sum), np.asarray(ru.per_level[0].sum))
-    for l in (1, 2):
-        assert frob_rel(rm.per_level[l].sum, ru.per_level[l].sum) <= TOL64
-        assert not np.array_equal(np.asarray(rm.per_level[l].sum), np.asarray(ru.per_level[l].sum))
+    for l in (0, 1):
+        assert np.array_equal(np.asarray(rm.per_level[l].sum), np.asarray(ru.per_level[l].sum))
+    assert frob_rel(rm.per_level[2].sum, ru.per_level[2].sum) <= TOL64
+    assert not np.array_equal(np.asarray(rm.per_level[2].sum), np.asarray(ru.per_level[2].sum))
 
 
 def test_merge_rank_shards_add_up(gpu):
