@@ -211,3 +211,32 @@ def test_merge_single_level_mc(gpu):
     re_ = gpu.mc_matmul(model, gpu.target_identity(), options=gpu.EstimatorOptions(engine="exact"), **kw)
     assert frob_rel(rm.value, ru.value) <= TOL64 and frob_rel(rm.value, re_.value) <= TOL64
     assert not np.array_equal(np.asarray(rm.value), np.asarray(ru.value))
+
+
+def test_contraction_columns_counter(gpu):
+    """mlsk_contraction_columns: executed K-columns (whole chunks) vs sampled indices of this
+    thread's GEMMs -- equal to the chunk-padded sampled count when merging is off, the expected
+    fraction n (1 - e^-l I_0(l)) / c (here c = n: 0.534) when it is on."""
+    L = _lib.lib()
+    model = gpu.gaussian_mean_matrix_model(64, 1024, 64, sd=0.5, data_seed=23)
+    N, c0 = [0, 0, 0, 0, 6], 64  # only level 4: c = 1024 = n
+    cols = (C.c_int64 * 2)()
+
+    def one_round():
+        s = gpu.MlmcSession(model, gpu.target_identity(), 2, 4, MASTER, c0=c0,
+                            options=gpu.EstimatorOptions(engine="fused"))
+        s.run_round(N)
+        s.stats()
+        s.close()
+
+    with env(MLSK_MERGE=0):
+        L.mlsk_contraction_columns(cols, 1)
+        one_round()
+        L.mlsk_contraction_columns(cols, 1)
+    assert cols[0] == cols[1] == 6 * 1024
+    with env(MLSK_MERGE=None, MLSK_MERGE_MIN_DEN=None):
+        one_round()
+        L.mlsk_contraction_columns(cols, 1)
+    assert cols[1] == 6 * 1024
+    frac = cols[0] / cols[1]
+    assert 0.50 < frac < 0.60, frac  # 0.534 expected, + chunk padding and the maximum over 6 samples
