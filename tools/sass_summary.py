@@ -23,8 +23,8 @@ for line in out.splitlines():
     if m:
         name = m.group(1)
         f = subprocess.run(["c++filt", name], capture_output=True, text=True).stdout.strip() or name
-        short = re.sub(r"\(.*", "", f).split("::")[-1]
-        short = re.sub(r"^void ", "", short)
+        mm = re.search(r"\b(k_\w+)", f)
+        short = mm.group(1) if mm else f
         cur = kern.setdefault(short, collections.Counter())
         continue
     if cur is None:
