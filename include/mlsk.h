@@ -102,7 +102,10 @@ typedef struct mlsk_exec_opts {
     void* stream;        /* cudaStream_t to order the work on; NULL = a library stream
                             and every call returns only when its work is done.  With
                             a caller stream, mlsk_session_run_round returns once the
-                            round is enqueued (results ordered on that stream). */
+                            round is enqueued (results ordered on that stream); a
+                            round whose deep levels run on merged sampled columns
+                            (mlsk_contraction_columns) waits once for a small device
+                            pre-pass before it enqueues the rest (MLSK_MERGE=0: never). */
     int32_t rank;        /* sample sharding: 64-sample chunk q runs on rank q % world */
     int32_t world;       /* 1 for a single GPU */
     int64_t probe_k;     /* coupling probe: dump index sets of the first probe_k
