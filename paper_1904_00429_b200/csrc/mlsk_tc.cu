@@ -208,6 +208,16 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uin
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// BF16 cross terms (TcShape::bfx): kind::f16 MMAs with BF16 operands, K = 16
+__device__ __forceinline__ void tc_mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 // 32 lanes x 16 consecutive 32-bit columns: lane i of the warp gets row
 // (quadrant*32 + i), columns [col, col + 16)
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
@@ -255,10 +265,59 @@ __device__ __forceinline__ int sw_off(int r, int k) {
     return r * ROWB + ((((k >> 2) ^ ((r * ROWB >> 7) & (ROWB / 16 - 1))) << 4) | ((k & 3) << 2));
 }
 
+// ---- BF16 cross terms (bfx).  a b ~= tf32(a) tf32(b) + a b_lo + a_lo b: the
+// two cross terms are 2^-11 of the product, so BF16 operands (8 bits, rounded
+// to nearest) leave them accurate to 2^-9 of themselves, 2^-20 of the product
+// (1.3e-6 relative on a level-sample's Y, emulated on the CPU; the TF32 form
+// leaves 3.5e-7, and the accumulation's own error is 2-5e-6).  A BF16 MMA is
+// K = 16 at twice the TF32 rate: a K-chunk costs 2 TF32 + 2 BF16 MMAs instead
+// of 6 TF32 ones (a third less tensor time) and reads 32 KB instead of 48 KB of
+// operands from shared memory.  The lo tile of a 128-row K-chunk (8 KB) then
+// holds two BF16 tiles of 4 KB, K-major SWIZZLE_32B (32-byte rows): bf16(x)
+// and bf16(x - tf32(x)); the hi tile is unchanged, so panels, stages and bulk
+// copies keep their sizes.  CTA pairs only (a single CTA's 256-column B tile
+// would need its two halves' BF16 tiles contiguous); MLSK_TC_BF16X=0 keeps
+// the three TF32 MMAs.
+constexpr int BROWB = TBK * 2;       // bytes per BF16 K-chunk row
+constexpr int BTILE = TBM * BROWB;   // 4 KB: 128 rows
+static_assert(2 * BTILE == TTILE, "the two BF16 tiles fill the lo tile");
+__device__ __forceinline__ int sw_off_b(int r, int k) {  // byte offset of BF16 element (r, k), SWIZZLE_32B
+    return r * BROWB + ((((k >> 3) ^ ((r * BROWB >> 7) & 1)) << 4) | ((k & 7) << 1));
+}
+__device__ __forceinline__ uint64_t sw_desc_b(uint32_t saddr) {
+    uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+    d |= (uint64_t)1 << 16;                   // LBO (unused for swizzled K-major)
+    d |= (uint64_t)((8 * BROWB) >> 4) << 32;  // SBO: 8-row groups
+    d |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
+    d |= (uint64_t)6 << 61;                   // SWIZZLE_32B
+    return d;
+}
+// kind::f16 instruction descriptor: F32 accumulate, BF16 A / B, K-major, M x N
+__host__ __device__ constexpr uint32_t bf16_idesc(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// two floats -> packed BF16 pair (round to nearest even), x0 in the low half
+__device__ __forceinline__ uint32_t bf16x2_rn(float x0, float x1) {
+    uint32_t d;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(x1), "f"(x0));
+    return d;
+}
+
 // ---------------------------------------------------------------- entries
 
 __device__ __forceinline__ float tf32_lo(float x) {
     return __fsub_rn(x, __uint_as_float(__float_as_uint(x) & 0xFFFFE000u));
+}
+// chunk columns k, k + 1 (k even) of row r into the lo tile: TF32 lo words, or
+// (bfx) the BF16 pair of the values and of their lo parts
+__device__ __forceinline__ void store_lo_pair(unsigned char* tlo, int r, int k, float v0, float v1, bool bfx) {
+    if (bfx) {
+        const int ob = sw_off_b(r, k);
+        *reinterpret_cast<uint32_t*>(tlo + ob) = bf16x2_rn(v0, v1);
+        *reinterpret_cast<uint32_t*>(tlo + BTILE + ob) = bf16x2_rn(tf32_lo(v0), tf32_lo(v1));
+    } else {
+        *reinterpret_cast<float2*>(tlo + sw_off(r, k)) = make_float2(tf32_lo(v0), tf32_lo(v1));
+    }
 }
 
 struct TcModel {
@@ -299,7 +358,7 @@ static_assert(GEN_T == 256 && TBK == 16 && TBM == 128, "gauss_phase_f32 thread m
 template <bool IS_A>
 __device__ __forceinline__ void gauss_phase_f32(const DevModel& M, const Tables& T, uint64_t key, int64_t rb,
                                                 const int* s_j, const float* s_w, unsigned char* thi,
-                                                unsigned char* tlo, int tid) {
+                                                unsigned char* tlo, int tid, bool bfx) {
     const int cp = tid & 7, qq = tid >> 3;
     const int r0 = 4 * qq;
     const int64_t dim = IS_A ? M.m : M.p;
@@ -360,7 +419,7 @@ __device__ __forceinline__ void gauss_phase_f32(const DevModel& M, const Tables&
     for (int e = 0; e < 4; ++e) {
         const int off = sw_off(r0 + e, 2 * cp);  // chunk columns 2cp, 2cp+1: adjacent words
         *reinterpret_cast<float2*>(thi + off) = make_float2(v[0][e], v[1][e]);
-        *reinterpret_cast<float2*>(tlo + off) = make_float2(tf32_lo(v[0][e]), tf32_lo(v[1][e]));
+        store_lo_pair(tlo, r0 + e, 2 * cp, v[0][e], v[1][e], bfx);
     }
 }
 
@@ -372,7 +431,7 @@ __device__ __forceinline__ void gauss_phase_f32(const DevModel& M, const Tables&
 template <bool IS_A>
 __device__ __forceinline__ void student_t_phase_f32(const TcModel& S, const Tables& T, uint64_t key, int64_t rb,
                                                     const int* s_j, const float* s_w, unsigned char* thi,
-                                                    unsigned char* tlo, int tid) {
+                                                    unsigned char* tlo, int tid, bool bfx) {
     const int cp = tid & 7, qq = tid >> 3;
     const int r0 = 4 * qq;
     const int64_t lim = (IS_A ? S.M.m : S.M.p) - rb;
@@ -400,7 +459,7 @@ __device__ __forceinline__ void student_t_phase_f32(const TcModel& S, const Tabl
     for (int e = 0; e < 4; ++e) {
         const int off = sw_off(r0 + e, 2 * cp);
         *reinterpret_cast<float2*>(thi + off) = make_float2(v[0][e], v[1][e]);
-        *reinterpret_cast<float2*>(tlo + off) = make_float2(tf32_lo(v[0][e]), tf32_lo(v[1][e]));
+        store_lo_pair(tlo, r0 + e, 2 * cp, v[0][e], v[1][e], bfx);
     }
 }
 
@@ -424,7 +483,8 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                   int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kc0,
                   float* __restrict__ Ahi, float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
                   uint32_t* __restrict__ idx_out, const MkEntry* __restrict__ mk, int64_t mk_stride,
-                  const MkInfo* __restrict__ mk_info) {
+                  const MkInfo* __restrict__ mk_info, int bfx_i) {
+    const bool bfx = bfx_i != 0;  // lo tiles as two BF16 tiles (BF16 cross terms)
     __shared__ __align__(1024) unsigned char tbuf[2][2][TTILE];  // [buffer][hi / lo], double-buffered
     __shared__ __align__(16) float2 s_sc[256];  // full-circle sincos table
     __shared__ __align__(16) float2 s_lg[64];
@@ -479,11 +539,11 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
             unsigned char* thi = tbuf[buf][0];
             unsigned char* tlo = tbuf[buf][1];
             if (KIND == GK_GAUSS) {
-                if (isA) gauss_phase_f32<true>(M, T, key, rb, s_j, s_w, thi, tlo, tid);
-                else gauss_phase_f32<false>(M, T, key, rb, s_j, s_w, thi, tlo, tid);
+                if (isA) gauss_phase_f32<true>(M, T, key, rb, s_j, s_w, thi, tlo, tid, bfx);
+                else gauss_phase_f32<false>(M, T, key, rb, s_j, s_w, thi, tlo, tid, bfx);
             } else if (KIND == GK_STUDENT_T) {
-                if (isA) student_t_phase_f32<true>(S, T, key, rb, s_j, s_w, thi, tlo, tid);
-                else student_t_phase_f32<false>(S, T, key, rb, s_j, s_w, thi, tlo, tid);
+                if (isA) student_t_phase_f32<true>(S, T, key, rb, s_j, s_w, thi, tlo, tid, bfx);
+                else student_t_phase_f32<false>(S, T, key, rb, s_j, s_w, thi, tlo, tid, bfx);
             } else {
                 for (int item = tid; item < TBM * TBK; item += GEN_T) {
                     const int tt = item & (TBK - 1), rr = item / TBK;
@@ -496,7 +556,14 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                         v = isA ? x : __fmul_rn(s_w[tt], x);
                     }
                     *reinterpret_cast<float*>(thi + sw_off(rr, tt)) = v;
-                    *reinterpret_cast<float*>(tlo + sw_off(rr, tt)) = tf32_lo(v);
+                    if (bfx) {
+                        const int ob = sw_off_b(rr, tt);
+                        *reinterpret_cast<unsigned short*>(tlo + ob) = (unsigned short)(bf16x2_rn(v, 0.f) & 0xffffu);
+                        *reinterpret_cast<unsigned short*>(tlo + BTILE + ob) =
+                            (unsigned short)(bf16x2_rn(tf32_lo(v), 0.f) & 0xffffu);
+                    } else {
+                        *reinterpret_cast<float*>(tlo + sw_off(rr, tt)) = tf32_lo(v);
+                    }
                 }
             }
             // both tiles leave by bulk copies (TMA engine), not by the threads
@@ -565,7 +632,8 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                  int write_b, float* __restrict__ Ahi,
                  float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
                  uint32_t* __restrict__ idx_out, const MkEntry* __restrict__ mk, int64_t mk_stride,
-                 const MkInfo* __restrict__ mk_info) {
+                 const MkInfo* __restrict__ mk_info, int bfx_i) {
+    const bool bfx = bfx_i != 0;  // lo tiles as two BF16 tiles (BF16 cross terms)
     extern __shared__ __align__(1024) unsigned char rsm[];
     float* xs = reinterpret_cast<float*>(rsm);  // [D][RFF_XS]
     float* wsm = xs + RFF_DMAX * RFF_XS;         // [D][RFF_WS]
@@ -708,15 +776,16 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                         z0 = __fmul_rn(fabsf(w0), z0);
                         z1 = __fmul_rn(fabsf(w1), z1);
                     }
-                    const int off = sw_off((int)(rb - rt) + rr, ttn) / 4;  // floats
+                    const int rti = (int)(rb - rt) + rr;  // row within the 128-row panel tile
+                    const int off = sw_off(rti, ttn) / 4;  // floats
                     if (rb < MP) {
                         *reinterpret_cast<float2*>(Ahi + oa + off) = make_float2(z0, z1);
-                        *reinterpret_cast<float2*>(Alo + oa + off) = make_float2(tf32_lo(z0), tf32_lo(z1));
+                        store_lo_pair(reinterpret_cast<unsigned char*>(Alo + oa), rti, ttn, z0, z1, bfx);
                     }
                     if (write_b && rb < PP) {
                         const float v0 = __fmul_rn(w0, z0), v1 = __fmul_rn(w1, z1);
                         *reinterpret_cast<float2*>(Bhi + ob + off) = make_float2(v0, v1);
-                        *reinterpret_cast<float2*>(Blo + ob + off) = make_float2(tf32_lo(v0), tf32_lo(v1));
+                        store_lo_pair(reinterpret_cast<unsigned char*>(Blo + ob), rti, ttn, v0, v1, bfx);
                     }
                 }
             }
@@ -758,13 +827,23 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                 const int off = sw_off(r, tt) / 4;  // floats
                 if (rb < MP) {
                     *reinterpret_cast<float4*>(Ahi + oa + off) = make_float4(z[0], z[1], z[2], z[3]);
-                    *reinterpret_cast<float4*>(Alo + oa + off) =
-                        make_float4(tf32_lo(z[0]), tf32_lo(z[1]), tf32_lo(z[2]), tf32_lo(z[3]));
+                    if (bfx) {
+                        store_lo_pair(reinterpret_cast<unsigned char*>(Alo + oa), r, tt, z[0], z[1], true);
+                        store_lo_pair(reinterpret_cast<unsigned char*>(Alo + oa), r, tt + 2, z[2], z[3], true);
+                    } else {
+                        *reinterpret_cast<float4*>(Alo + oa + off) =
+                            make_float4(tf32_lo(z[0]), tf32_lo(z[1]), tf32_lo(z[2]), tf32_lo(z[3]));
+                    }
                 }
                 if (write_b && rb < PP) {
                     *reinterpret_cast<float4*>(Bhi + ob + off) = make_float4(v[0], v[1], v[2], v[3]);
-                    *reinterpret_cast<float4*>(Blo + ob + off) =
-                        make_float4(tf32_lo(v[0]), tf32_lo(v[1]), tf32_lo(v[2]), tf32_lo(v[3]));
+                    if (bfx) {
+                        store_lo_pair(reinterpret_cast<unsigned char*>(Blo + ob), r, tt, v[0], v[1], true);
+                        store_lo_pair(reinterpret_cast<unsigned char*>(Blo + ob), r, tt + 2, v[2], v[3], true);
+                    } else {
+                        *reinterpret_cast<float4*>(Blo + ob + off) =
+                            make_float4(tf32_lo(v[0]), tf32_lo(v[1]), tf32_lo(v[2]), tf32_lo(v[3]));
+                    }
                 }
             }
 #endif
@@ -801,6 +880,8 @@ struct TcShape {
     // merged sampled columns on the shared panel: the negated leading chunks
     // per sample (mk_info[b].neg_kc) instead of neg_kc
     const MkInfo* mk_info;
+    // BF16 cross terms (CTA pairs): the lo tiles hold bf16(x) | bf16(x - tf32(x))
+    int bfx;
     // K-chunks per TMEM accumulation segment (0: a CTA's whole K-range of a
     // sample is one segment).  tcgen05's fp32 accumulation rounds the running
     // sum toward zero, so its error grows with the number of MMAs folded into
@@ -1007,6 +1088,18 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 const uint32_t st = smem_addr(ring + s * STB);
                 const uint32_t dcol = tmem + (uint32_t)abuf * TBN;
                 const uint32_t id = sh.kc0 + kc < neg_kc ? idesc | (1u << 14) : idesc;  // negate B
+                if (PAIR && sh.bfx) {
+                    // hi x hi as two TF32 MMAs (K = 8 each), the cross terms a b_lo and
+                    // a_lo b as two BF16 MMAs (K = 16) over the lo tiles' BF16 halves
+                    constexpr uint32_t idb0 = bf16_idesc(2 * TBM, TBN);
+                    const uint32_t idb = sh.kc0 + kc < neg_kc ? idb0 | (1u << 14) : idb0;
+#ifndef MLSK_TC_ABL_NOMMA
+                    tc_mma_tf32_pair(dcol, sw_desc(st), sw_desc(st + 2 * TA_BYTES), id, sgc > 0 ? 1u : 0u);
+                    tc_mma_tf32_pair(dcol, sw_desc(st + 32), sw_desc(st + 2 * TA_BYTES + 32), id, 1u);
+                    tc_mma_bf16_pair(dcol, sw_desc_b(st + TA_BYTES), sw_desc_b(st + 2 * TA_BYTES + BB + BTILE), idb, 1u);
+                    tc_mma_bf16_pair(dcol, sw_desc_b(st + TA_BYTES + BTILE), sw_desc_b(st + 2 * TA_BYTES + BB), idb, 1u);
+#endif
+                } else
 #pragma unroll
                 for (int kk = 0; kk < TBK / 8; ++kk) {
                     const uint64_t ah = sw_desc(st + kk * 32), al = sw_desc(st + TA_BYTES + kk * 32);
@@ -1379,6 +1472,9 @@ class TcEngine final : public PanelEngine {
         // tiles of a pair at indices 2u, 2u + 1).  MLSK_TC_PAIR=0: single CTAs.
         const char* pair_env = std::getenv("MLSK_TC_PAIR");
         pair_ = (MP_ / TBM) % 2 == 0 && T_ % 2 == 0 && !(pair_env && std::strcmp(pair_env, "0") == 0);
+        // BF16 cross terms (CTA pairs only).  MLSK_TC_BF16X=0: three TF32 MMAs per K-step
+        const char* bfx_env = std::getenv("MLSK_TC_BF16X");
+        bfx_ = pair_ && !(bfx_env && std::strcmp(bfx_env, "0") == 0) ? 1 : 0;
         once_per_device((const void*)&k_gemm_tf32x3<false, false, false>, [smem, rsmem] {
             for (auto f : {k_gemm_tf32x3<false, false, false>, k_gemm_tf32x3<false, true, false>,
                            k_gemm_tf32x3<true, false, false>, k_gemm_tf32x3<true, true, false>,
@@ -1423,21 +1519,21 @@ class TcEngine final : public PanelEngine {
                                                       (int64_t)nsm_ * 5),
                                RFF_T, rff_smem_, s>>>(
                 S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, kr.kc0,
-                shared_panel(c, cc, w_fine, w_coarse) ? 0 : 1, Ahi, Alo, Bhi, Blo, idx, kr.mk, kr.mk_stride, kr.mk_info);
+                shared_panel(c, cc, w_fine, w_coarse) ? 0 : 1, Ahi, Alo, Bhi, Blo, idx, kr.mk, kr.mk_stride, kr.mk_info, bfx_);
         } else {
             const int grid = (int)std::min<int64_t>((int64_t)nb * k, gen_cap_);
             if (M_.dm.kind == MLSK_MODEL_GAUSS_MEAN)
                 k_gen_panels_tf32<GK_GAUSS><<<grid, GEN_T, 0, s>>>(S_, seed, tag, ks, nb, c, cc, (float)w_fine,
                                                                   (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi,
-                                                                  Blo, idx, kr.mk, kr.mk_stride, kr.mk_info);
+                                                                  Blo, idx, kr.mk, kr.mk_stride, kr.mk_info, bfx_);
             else if (M_.dm.kind == MLSK_MODEL_STUDENT_T)
                 k_gen_panels_tf32<GK_STUDENT_T><<<grid, GEN_T, 0, s>>>(S_, seed, tag, ks, nb, c, cc, (float)w_fine,
                                                                       (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo,
-                                                                      Bhi, Blo, idx, kr.mk, kr.mk_stride, kr.mk_info);
+                                                                      Bhi, Blo, idx, kr.mk, kr.mk_stride, kr.mk_info, bfx_);
             else
                 k_gen_panels_tf32<GK_GENERIC><<<grid, GEN_T, 0, s>>>(S_, seed, tag, ks, nb, c, cc, (float)w_fine,
                                                                     (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi,
-                                                                    Blo, idx, kr.mk, kr.mk_stride, kr.mk_info);
+                                                                    Blo, idx, kr.mk, kr.mk_stride, kr.mk_info, bfx_);
         }
         launched();
     }
@@ -1471,7 +1567,7 @@ class TcEngine final : public PanelEngine {
         const int64_t w1 = (T_ + nsm_ - 1) / nsm_, w2 = (2 * T_ + nsm_ - 1) / nsm_;
         if (kr.part == 0 && nb == 1 && direct && w2 < 2 * w1 && k >= 16 && !sym_nb_) {
             ws_.ypart.ensure((size_t)2 * T_ * TBM * TBN);
-            TcShape sh{1, k, MP_, PP_, T_, 2, tiles_n_, nullptr, M_.rows, M_.cols, 1, 0, 0, 0, 1.0f, nullptr, seg_};
+            TcShape sh{1, k, MP_, PP_, T_, 2, tiles_n_, nullptr, M_.rows, M_.cols, 1, 0, 0, 0, 1.0f, nullptr, bfx_, seg_};
             {
                 Prof p("gemm_tf32x3", s);
                 launch_gemm(true, segmented(k - (k + 1) / 2), 2 * T_, s, Ahi, Alo, Bhi, Blo, sh, part, part_sq, 1,
@@ -1495,7 +1591,7 @@ class TcEngine final : public PanelEngine {
             ypart = ws_.ypart.p;
         }
         TcShape sh{nb,      k,       MP_,     PP_,    T_,     Gs_,        tiles_n_, direct ? st.total() : nullptr,
-                   M_.rows, M_.cols, 0,       sym_nb_, neg_kc, kr.kc0, escale, mk_info, seg_};
+                   M_.rows, M_.cols, 0,       sym_nb_, neg_kc, kr.kc0, escale, mk_info, bfx_, seg_};
         {
             Prof p("gemm_tf32x3", s);
             if (kr.part == 0)
@@ -1586,6 +1682,7 @@ class TcEngine final : public PanelEngine {
     int nsm_, T_, Gs_, tiles_n_, smem_, rff_smem_;
     int sym_nb_ = 0;  // symmetric output: 256-blocks per side (0 = full tile grid)
     bool pair_ = false;  // CTA-pair GEMM (cta_group::2)
+    int bfx_ = 0;        // BF16 cross terms (lo tiles as BF16 pairs)
     int seg_ = TC_SEG;
     bool shared_env_ = true;
     int64_t gen_cap_;
