@@ -282,11 +282,19 @@ def measure(ids, steps=3, with_cpu=True, device=0):
             blk["algorithmic_tflops"] = flops / (ms * 1e-3) / 1e12
             blk["step_frac_of_peak"] = blk["algorithmic_tflops"] / (peak_t / 3)
             blk["peaks_tf32"] = {"burst": tf32, "sustained": tf32_sus, "used": which}
+            bfx = os.environ.get("MLSK_TC_BF16X", "1") != "0" and os.environ.get("MLSK_TC_PAIR", "1") != "0"
             blk["roofline"] = {"bound": "tensor", "achieved": ach, "peak": peak_t / 3, "unit": "TFLOP/s",
                                "frac": ach / (peak_t / 3) if ach else None, "traffic": None,
-                               "kernel": "k_gemm_tf32x3 (tcgen05.mma kind::tf32, 3 MMAs per K-step)",
+                               "kernel": ("k_gemm_tf32x3 (tcgen05.mma cta_group::2: per 16-column K-chunk 2 kind::tf32 "
+                                          "MMAs for hi x hi + 2 kind::f16 BF16 MMAs for the cross terms)" if bfx else
+                                          "k_gemm_tf32x3 (tcgen05.mma kind::tf32, 3 MMAs per K-step)"),
                                "peak_source": f"dense TF32 tcgen05 measured in this run, {which} "
                                               f"({peak_t:.0f} TFLOP/s) / 3",
+                               # SURVEY 8(d)'s fp32 peak is TF32 / 3 (3xTF32).  With BF16 cross terms a K-chunk
+                               # costs 4 MMA slots instead of 6, so the kernel's own ceiling is TF32 / 2 and
+                               # `frac` can approach 1.5 x (tensor time) -- both fractions are given.
+                               "frac_of_own_ceiling": (ach / (peak_t / 2) if ach and bfx else
+                                                       (ach / (peak_t / 3) if ach else None)),
                                "algorithmic": ("P(P+1) c + 2 P D c flops per level-sample (SYRK + features)"
                                                if cid == 4 else "2 m p c flops per level-sample")}
         if not c.get("inner"):
