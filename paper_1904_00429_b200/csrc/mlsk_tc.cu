@@ -8,6 +8,11 @@
 // a_hi = a (the MMA reads the fp32 word and uses its TF32 part), a_lo = a -
 // tf32(a) (exact in fp32) -- three MMAs per K-step into one fp32 accumulator.
 //
+// CTA pairs run the two cross terms as BF16 MMAs (kind::f16, K = 16) over BF16
+// copies of the values and of their lo parts -- see "BF16 cross terms" below:
+// 2 TF32 + 2 BF16 MMAs per 16-column K-chunk instead of 6 TF32 ones, the same
+// fp32-level accuracy (the cross terms are 2^-11 of the product).
+//
 //  k_gen_panels_tf32  sampled indices + the sampled columns of A / rows of B
 //                     (gauss f32, Student-t or random-Fourier features,
 //                     generated on the fly), written as hi / lo K-chunks in the
