@@ -8,7 +8,7 @@
 // a_hi = a (the MMA reads the fp32 word and uses its TF32 part), a_lo = a -
 // tf32(a) (exact in fp32) -- three MMAs per K-step into one fp32 accumulator.
 //
-// CTA pairs run the two cross terms as BF16 MMAs (kind::f16, K = 16) over BF16
+// The two cross terms run as BF16 MMAs (kind::f16, K = 16) over BF16
 // copies of the values and of their lo parts -- see "BF16 cross terms" below:
 // 2 TF32 + 2 BF16 MMAs per 16-column K-chunk instead of 6 TF32 ones, the same
 // fp32-level accuracy (the cross terms are 2^-11 of the product).
@@ -223,6 +223,15 @@ __device__ __forceinline__ void tc_mma_bf16_pair(uint32_t tmem_d, uint64_t adesc
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+__device__ __forceinline__ void tc_mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 // 32 lanes x 16 consecutive 32-bit columns: lane i of the warp gets row
 // (quadrant*32 + i), columns [col, col + 16)
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
@@ -278,24 +287,19 @@ __device__ __forceinline__ int sw_off(int r, int k) {
 // K = 16 at twice the TF32 rate: a K-chunk costs 2 TF32 + 2 BF16 MMAs instead
 // of 6 TF32 ones (a third less tensor time) and reads 32 KB instead of 48 KB of
 // operands from shared memory.  The lo tile of a 128-row K-chunk (8 KB) then
-// holds two BF16 tiles of 4 KB, K-major SWIZZLE_32B (32-byte rows): bf16(x)
-// and bf16(x - tf32(x)); the hi tile is unchanged, so panels, stages and bulk
-// copies keep their sizes.  CTA pairs only (a single CTA's 256-column B tile
-// would need its two halves' BF16 tiles contiguous); MLSK_TC_BF16X=0 keeps
-// the three TF32 MMAs.
-constexpr int BROWB = TBK * 2;       // bytes per BF16 K-chunk row
-constexpr int BTILE = TBM * BROWB;   // 4 KB: 128 rows
-static_assert(2 * BTILE == TTILE, "the two BF16 tiles fill the lo tile");
-__device__ __forceinline__ int sw_off_b(int r, int k) {  // byte offset of BF16 element (r, k), SWIZZLE_32B
-    return r * BROWB + ((((k >> 3) ^ ((r * BROWB >> 7) & 1)) << 4) | ((k & 7) << 1));
-}
-__device__ __forceinline__ uint64_t sw_desc_b(uint32_t saddr) {
-    uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
-    d |= (uint64_t)1 << 16;                   // LBO (unused for swizzled K-major)
-    d |= (uint64_t)((8 * BROWB) >> 4) << 32;  // SBO: 8-row groups
-    d |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
-    d |= (uint64_t)6 << 61;                   // SWIZZLE_32B
-    return d;
+// holds ONE BF16 tile in the same K-major SWIZZLE_64B layout (64-byte rows):
+// row r = [bf16(x)(r, 0..15) | bf16(x - tf32(x))(r, 0..15)], i.e. the values are
+// BF16 columns 0..15 and their lo parts columns 16..31 of a 32-column tile, and
+// the two K = 16 operands are the row halves (descriptor start + 0 / + 32 bytes,
+// as the TF32 K = 8 steps of the hi tile).  The hi tile is unchanged, so panels,
+// stages and bulk copies keep their sizes.  (Two separate 32-byte-row tiles in
+// SWIZZLE_32B were measured first: correct, but their MMAs ran ~1.6x slower than
+// the 64-byte-row form.)  MLSK_TC_BF16X=0 keeps the three TF32 MMAs.
+static_assert(TBK * 2 * 2 == ROWB, "values and lo parts as BF16 fill a 64-byte row");
+// byte offset of BF16 element (r, k) of the values (which = 0) or the lo parts (1)
+__device__ __forceinline__ int sw_off_b(int r, int k, int which) {
+    const int kp = k + TBK * which;
+    return r * ROWB + ((((kp >> 3) ^ ((r * ROWB >> 7) & (ROWB / 16 - 1))) << 4) | ((kp & 7) << 1));
 }
 // kind::f16 instruction descriptor: F32 accumulate, BF16 A / B, K-major, M x N
 __host__ __device__ constexpr uint32_t bf16_idesc(int M, int N) {
@@ -317,9 +321,8 @@ __device__ __forceinline__ float tf32_lo(float x) {
 // (bfx) the BF16 pair of the values and of their lo parts
 __device__ __forceinline__ void store_lo_pair(unsigned char* tlo, int r, int k, float v0, float v1, bool bfx) {
     if (bfx) {
-        const int ob = sw_off_b(r, k);
-        *reinterpret_cast<uint32_t*>(tlo + ob) = bf16x2_rn(v0, v1);
-        *reinterpret_cast<uint32_t*>(tlo + BTILE + ob) = bf16x2_rn(tf32_lo(v0), tf32_lo(v1));
+        *reinterpret_cast<uint32_t*>(tlo + sw_off_b(r, k, 0)) = bf16x2_rn(v0, v1);
+        *reinterpret_cast<uint32_t*>(tlo + sw_off_b(r, k, 1)) = bf16x2_rn(tf32_lo(v0), tf32_lo(v1));
     } else {
         *reinterpret_cast<float2*>(tlo + sw_off(r, k)) = make_float2(tf32_lo(v0), tf32_lo(v1));
     }
@@ -562,9 +565,9 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                     }
                     *reinterpret_cast<float*>(thi + sw_off(rr, tt)) = v;
                     if (bfx) {
-                        const int ob = sw_off_b(rr, tt);
-                        *reinterpret_cast<unsigned short*>(tlo + ob) = (unsigned short)(bf16x2_rn(v, 0.f) & 0xffffu);
-                        *reinterpret_cast<unsigned short*>(tlo + BTILE + ob) =
+                        *reinterpret_cast<unsigned short*>(tlo + sw_off_b(rr, tt, 0)) =
+                            (unsigned short)(bf16x2_rn(v, 0.f) & 0xffffu);
+                        *reinterpret_cast<unsigned short*>(tlo + sw_off_b(rr, tt, 1)) =
                             (unsigned short)(bf16x2_rn(tf32_lo(v), 0.f) & 0xffffu);
                     } else {
                         *reinterpret_cast<float*>(tlo + sw_off(rr, tt)) = tf32_lo(v);
@@ -885,7 +888,7 @@ struct TcShape {
     // merged sampled columns on the shared panel: the negated leading chunks
     // per sample (mk_info[b].neg_kc) instead of neg_kc
     const MkInfo* mk_info;
-    // BF16 cross terms (CTA pairs): the lo tiles hold bf16(x) | bf16(x - tf32(x))
+    // BF16 cross terms: the lo tiles' rows hold bf16(x) | bf16(x - tf32(x))
     int bfx;
     // K-chunks per TMEM accumulation segment (0: a CTA's whole K-range of a
     // sample is one segment).  tcgen05's fp32 accumulation rounds the running
@@ -1093,16 +1096,24 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 const uint32_t st = smem_addr(ring + s * STB);
                 const uint32_t dcol = tmem + (uint32_t)abuf * TBN;
                 const uint32_t id = sh.kc0 + kc < neg_kc ? idesc | (1u << 14) : idesc;  // negate B
-                if (PAIR && sh.bfx) {
+                if (sh.bfx) {
                     // hi x hi as two TF32 MMAs (K = 8 each), the cross terms a b_lo and
-                    // a_lo b as two BF16 MMAs (K = 16) over the lo tiles' BF16 halves
-                    constexpr uint32_t idb0 = bf16_idesc(2 * TBM, TBN);
+                    // a_lo b as two BF16 MMAs (K = 16) over the row halves of the lo tiles
+                    constexpr uint32_t idb0 = bf16_idesc(PAIR ? 2 * TBM : TBM, TBN);
                     const uint32_t idb = sh.kc0 + kc < neg_kc ? idb0 | (1u << 14) : idb0;
+                    const uint32_t sal = st + TA_BYTES, sbh = st + 2 * TA_BYTES, sbl = sbh + BB;
 #ifndef MLSK_TC_ABL_NOMMA
-                    tc_mma_tf32_pair(dcol, sw_desc(st), sw_desc(st + 2 * TA_BYTES), id, sgc > 0 ? 1u : 0u);
-                    tc_mma_tf32_pair(dcol, sw_desc(st + 32), sw_desc(st + 2 * TA_BYTES + 32), id, 1u);
-                    tc_mma_bf16_pair(dcol, sw_desc_b(st + TA_BYTES), sw_desc_b(st + 2 * TA_BYTES + BB + BTILE), idb, 1u);
-                    tc_mma_bf16_pair(dcol, sw_desc_b(st + TA_BYTES + BTILE), sw_desc_b(st + 2 * TA_BYTES + BB), idb, 1u);
+                    if (PAIR) {
+                        tc_mma_tf32_pair(dcol, sw_desc(st), sw_desc(sbh), id, sgc > 0 ? 1u : 0u);
+                        tc_mma_tf32_pair(dcol, sw_desc(st + 32), sw_desc(sbh + 32), id, 1u);
+                        tc_mma_bf16_pair(dcol, sw_desc(sal), sw_desc(sbl + 32), idb, 1u);   // a b_lo
+                        tc_mma_bf16_pair(dcol, sw_desc(sal + 32), sw_desc(sbl), idb, 1u);   // a_lo b
+                    } else {
+                        tc_mma_tf32(dcol, sw_desc(st), sw_desc(sbh), id, sgc > 0 ? 1u : 0u);
+                        tc_mma_tf32(dcol, sw_desc(st + 32), sw_desc(sbh + 32), id, 1u);
+                        tc_mma_bf16(dcol, sw_desc(sal), sw_desc(sbl + 32), idb, 1u);
+                        tc_mma_bf16(dcol, sw_desc(sal + 32), sw_desc(sbl), idb, 1u);
+                    }
 #endif
                 } else
 #pragma unroll
@@ -1477,9 +1488,9 @@ class TcEngine final : public PanelEngine {
         // tiles of a pair at indices 2u, 2u + 1).  MLSK_TC_PAIR=0: single CTAs.
         const char* pair_env = std::getenv("MLSK_TC_PAIR");
         pair_ = (MP_ / TBM) % 2 == 0 && T_ % 2 == 0 && !(pair_env && std::strcmp(pair_env, "0") == 0);
-        // BF16 cross terms (CTA pairs only).  MLSK_TC_BF16X=0: three TF32 MMAs per K-step
+        // BF16 cross terms.  MLSK_TC_BF16X=0: three TF32 MMAs per K-step
         const char* bfx_env = std::getenv("MLSK_TC_BF16X");
-        bfx_ = pair_ && !(bfx_env && std::strcmp(bfx_env, "0") == 0) ? 1 : 0;
+        bfx_ = !(bfx_env && std::strcmp(bfx_env, "0") == 0) ? 1 : 0;
         once_per_device((const void*)&k_gemm_tf32x3<false, false, false>, [smem, rsmem] {
             for (auto f : {k_gemm_tf32x3<false, false, false>, k_gemm_tf32x3<false, true, false>,
                            k_gemm_tf32x3<true, false, false>, k_gemm_tf32x3<true, true, false>,

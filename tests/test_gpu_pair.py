@@ -1,8 +1,9 @@
 """The CTA-pair tcgen05 GEMM (cta_group::2, M = 256 over two SMs) against the
 single-CTA GEMM (MLSK_TC_PAIR=0) on the same draws: every output element is
 the same K-ordered chain of tf32 MMAs into an fp32 accumulator whichever SM
-pair computes its tile (with the pair's BF16 cross terms off, MLSK_TC_BF16X=0),
-so the level sums must agree bit for bit -- at the
+pair computes its tile (with BF16 cross terms, the default, and with three
+TF32 MMAs per K-step, MLSK_TC_BF16X=0), so the level sums must agree bit for
+bit -- at the
 BASELINE configs' full shapes (config 3, the symmetric config-4 Gram, config
 5) and on the K-split and K-parallel paths."""
 import os
@@ -62,22 +63,20 @@ def test_pair_equals_single_cta(gpu, case):
     else:  # an odd number of 128-row tiles: both settings run single CTAs
         model = g.gaussian_mean_matrix_model(384, 2048, 256, sd=1.0, data_seed=9, dtype=1)
         plan = g.LevelPlan(2, 1, [5, 3], c0=64)
-    # (the pair's BF16 cross terms off: the same three TF32 MMAs per K-step as single CTAs)
-    pair = run(g, model, plan, dict(env, MLSK_TC_BF16X="0"))
+    # default (cross terms a b_lo + a_lo b as BF16 MMAs) and with three TF32 MMAs per K-step
+    pair = run(g, model, plan, dict(env))
     single = run(g, model, plan, dict(env, MLSK_TC_PAIR="0"))
     same(pair, single)
-    # default pairs (cross terms a b_lo + a_lo b as BF16 MMAs): the same sums within the
-    # fp32 tolerance, and -- when the shape pairs up -- not the same bits
-    bfx = run(g, model, plan, dict(env))
-    for sa, sb in zip(bfx.per_level, single.per_level):
+    pair3 = run(g, model, plan, dict(env, MLSK_TC_BF16X="0"))
+    single3 = run(g, model, plan, dict(env, MLSK_TC_PAIR="0", MLSK_TC_BF16X="0"))
+    same(pair3, single3)
+    # the two forms: the same sums within the fp32 tolerance, not the same bits
+    for sa, sb in zip(pair.per_level, pair3.per_level):
         a = np.asarray(sa.sum, dtype=np.float64).ravel()
         b = np.asarray(sb.sum, dtype=np.float64).ravel()
         assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b), sa.level
         assert abs(sa.sum_of_squares - sb.sum_of_squares) <= 1e-5 * sb.sum_of_squares
-    if case != "odd_rows":
-        assert not np.array_equal(np.asarray(bfx.per_level[0].sum), np.asarray(single.per_level[0].sum))
-    else:
-        same(bfx, single)
+    assert not np.array_equal(np.asarray(pair.per_level[0].sum), np.asarray(pair3.per_level[0].sum))
 
 
 def test_pair_random_shapes_vs_single_and_exact(gpu):
@@ -94,12 +93,13 @@ def test_pair_random_shapes_vs_single_and_exact(gpu):
         N = [int(rng.integers(1, 7)), int(rng.integers(1, 5))]
         model = g.gaussian_mean_matrix_model(m, n, p, sd=1.0, data_seed=int(rng.integers(1, 1 << 30)), dtype=1)
         plan = g.LevelPlan(2, 1, N, c0=c0)
-        pair = run(g, model, plan, {"MLSK_TC_BF16X": "0"})
+        pair = run(g, model, plan, {})
         single = run(g, model, plan, {"MLSK_TC_PAIR": "0"})
         same(pair, single)
-        bfx = run(g, model, plan, {})  # default: BF16 cross terms when the shape pairs up
+        pair3 = run(g, model, plan, {"MLSK_TC_BF16X": "0"})  # three TF32 MMAs per K-step
+        same(pair3, run(g, model, plan, {"MLSK_TC_PAIR": "0", "MLSK_TC_BF16X": "0"}))
         ex = run(g, model, plan, {}, g.EstimatorOptions(engine="exact"))
-        for r in (pair, bfx):
+        for r in (pair, pair3):
             for sf, se in zip(r.per_level, ex.per_level):
                 a = np.asarray(sf.sum, dtype=np.float64).ravel()
                 b = np.asarray(se.sum, dtype=np.float64).ravel()
