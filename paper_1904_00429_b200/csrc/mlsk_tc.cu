@@ -311,6 +311,43 @@ __device__ __forceinline__ uint32_t bf16x2_rn(float x0, float x1) {
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(x1), "f"(x0));
     return d;
 }
+// two floats -> packed FP16 pair (round to nearest even, saturating), x0 in the low half
+__device__ __forceinline__ uint32_t f16x2_rn(float x0, float x1) {
+    uint32_t d;
+    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(x1), "f"(x0));
+    return d;
+}
+
+// ---- FP16 pairs (TcShape::bfx == 2, models whose entries are bounded: fp32
+// Gaussian draws -- the 24-bit Box-Muller radius is at most 5.77 -- and random
+// Fourier features).  An entry is stored as TWO halves, hi = fp16(x) (11 bits,
+// round to nearest) and lo = fp16(x - hi): 4 bytes per entry instead of 8, in
+// ONE K-major SWIZZLE_64B tile per 128 rows of a K-chunk whose 64-byte rows are
+// hi(r, 0..15) | lo(r, 0..15), and a K-chunk is three FP16 MMAs (K = 16): hi x
+// hi, hi x lo, lo x hi over the row halves.  Half the panel bytes for the
+// generators to write and the GEMM to read, three MMAs instead of four.
+// (Mixed FP16 x BF16 operands in one MMA are an illegal instruction, so
+// unbounded models -- Student-t: fp16 would saturate in the tails -- keep the
+// TF32 + BF16 form.)  Entries below 2^-14 keep an absolute accuracy of 2^-25 in
+// each half; the models' panel scale (a power of two, undone exactly in the
+// epilogue) keeps typical entries near 1.
+__device__ __forceinline__ void f16x2_unpack(uint32_t h, float& x0, float& x1) {
+    asm("{\n\t.reg .b16 l, u;\n\tmov.b32 {l, u}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, u;\n\t}"
+        : "=f"(x0), "=f"(x1)
+        : "r"(h));
+}
+// chunk columns k, k + 1 (k even) of row r into the (only) tile of FP16 pairs
+__device__ __forceinline__ void store_h16_pair(unsigned char* t, int r, int k, float v0, float v1) {
+    const uint32_t h = f16x2_rn(v0, v1);
+    float h0, h1;
+    f16x2_unpack(h, h0, h1);
+    *reinterpret_cast<uint32_t*>(t + sw_off_b(r, k, 0)) = h;
+    *reinterpret_cast<uint32_t*>(t + sw_off_b(r, k, 1)) = f16x2_rn(__fsub_rn(v0, h0), __fsub_rn(v1, h1));
+}
+// kind::f16 instruction descriptor: F32 accumulate, FP16 A / B, K-major, M x N
+__host__ __device__ constexpr uint32_t f16_idesc(int M, int N) {
+    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
 
 // ---------------------------------------------------------------- entries
 
@@ -366,7 +403,7 @@ static_assert(GEN_T == 256 && TBK == 16 && TBM == 128, "gauss_phase_f32 thread m
 template <bool IS_A>
 __device__ __forceinline__ void gauss_phase_f32(const DevModel& M, const Tables& T, uint64_t key, int64_t rb,
                                                 const int* s_j, const float* s_w, unsigned char* thi,
-                                                unsigned char* tlo, int tid, bool bfx) {
+                                                unsigned char* tlo, int tid, int bfx) {
     const int cp = tid & 7, qq = tid >> 3;
     const int r0 = 4 * qq;
     const int64_t dim = IS_A ? M.m : M.p;
@@ -425,9 +462,13 @@ __device__ __forceinline__ void gauss_phase_f32(const DevModel& M, const Tables&
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
+        if (bfx == 2) {  // FP16 pairs: one tile
+            store_h16_pair(thi, r0 + e, 2 * cp, v[0][e], v[1][e]);
+            continue;
+        }
         const int off = sw_off(r0 + e, 2 * cp);  // chunk columns 2cp, 2cp+1: adjacent words
         *reinterpret_cast<float2*>(thi + off) = make_float2(v[0][e], v[1][e]);
-        store_lo_pair(tlo, r0 + e, 2 * cp, v[0][e], v[1][e], bfx);
+        store_lo_pair(tlo, r0 + e, 2 * cp, v[0][e], v[1][e], bfx != 0);
     }
 }
 
@@ -439,7 +480,7 @@ __device__ __forceinline__ void gauss_phase_f32(const DevModel& M, const Tables&
 template <bool IS_A>
 __device__ __forceinline__ void student_t_phase_f32(const TcModel& S, const Tables& T, uint64_t key, int64_t rb,
                                                     const int* s_j, const float* s_w, unsigned char* thi,
-                                                    unsigned char* tlo, int tid, bool bfx) {
+                                                    unsigned char* tlo, int tid, int bfx) {
     const int cp = tid & 7, qq = tid >> 3;
     const int r0 = 4 * qq;
     const int64_t lim = (IS_A ? S.M.m : S.M.p) - rb;
@@ -465,9 +506,13 @@ __device__ __forceinline__ void student_t_phase_f32(const TcModel& S, const Tabl
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
+        if (bfx == 2) {
+            store_h16_pair(thi, r0 + e, 2 * cp, v[0][e], v[1][e]);
+            continue;
+        }
         const int off = sw_off(r0 + e, 2 * cp);
         *reinterpret_cast<float2*>(thi + off) = make_float2(v[0][e], v[1][e]);
-        store_lo_pair(tlo, r0 + e, 2 * cp, v[0][e], v[1][e], bfx);
+        store_lo_pair(tlo, r0 + e, 2 * cp, v[0][e], v[1][e], bfx != 0);
     }
 }
 
@@ -492,7 +537,7 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                   float* __restrict__ Ahi, float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
                   uint32_t* __restrict__ idx_out, const MkEntry* __restrict__ mk, int64_t mk_stride,
                   const MkInfo* __restrict__ mk_info, int bfx_i) {
-    const bool bfx = bfx_i != 0;  // lo tiles as two BF16 tiles (BF16 cross terms)
+    const int bfx = bfx_i;  // 0: TF32 lo tiles; 1: BF16 cross-term tiles; 2: FP16 pairs (one tile)
     __shared__ __align__(1024) unsigned char tbuf[2][2][TTILE];  // [buffer][hi / lo], double-buffered
     __shared__ __align__(16) float2 s_sc[256];  // full-circle sincos table
     __shared__ __align__(16) float2 s_lg[64];
@@ -563,6 +608,15 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                         else x = rff_entry(M, j, rb + rr);  // RFF (D > 64): B = A^T
                         v = isA ? x : __fmul_rn(s_w[tt], x);
                     }
+                    if (bfx == 2) {
+                        const uint32_t h = f16x2_rn(v, 0.f);
+                        float h0, h1;
+                        f16x2_unpack(h, h0, h1);
+                        *reinterpret_cast<unsigned short*>(thi + sw_off_b(rr, tt, 0)) = (unsigned short)(h & 0xffffu);
+                        *reinterpret_cast<unsigned short*>(thi + sw_off_b(rr, tt, 1)) =
+                            (unsigned short)(f16x2_rn(__fsub_rn(v, h0), 0.f) & 0xffffu);
+                        continue;
+                    }
                     *reinterpret_cast<float*>(thi + sw_off(rr, tt)) = v;
                     if (bfx) {
                         *reinterpret_cast<unsigned short*>(tlo + sw_off_b(rr, tt, 0)) =
@@ -582,7 +636,7 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                 float* dh = (isA ? Ahi : Bhi) + off;
                 float* dl = (isA ? Alo : Blo) + off;
                 bulk_store(dh, thi, TTILE);
-                bulk_store(dl, tlo, TTILE);
+                if (bfx != 2) bulk_store(dl, tlo, TTILE);
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // the other buffer is free
             }
@@ -640,8 +694,8 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                  int write_b, float* __restrict__ Ahi,
                  float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
                  uint32_t* __restrict__ idx_out, const MkEntry* __restrict__ mk, int64_t mk_stride,
-                 const MkInfo* __restrict__ mk_info, int bfx_i) {
-    const bool bfx = bfx_i != 0;  // lo tiles as two BF16 tiles (BF16 cross terms)
+                 const MkInfo* __restrict__ mk_info, int bfx_i, float pscale) {
+    const int bfx = bfx_i;  // 0: TF32 lo tiles; 1: BF16 cross-term tiles; 2: FP16 pairs (one tile)
     extern __shared__ __align__(1024) unsigned char rsm[];
     float* xs = reinterpret_cast<float*>(rsm);  // [D][RFF_XS]
     float* wsm = xs + RFF_DMAX * RFF_XS;         // [D][RFF_WS]
@@ -651,7 +705,8 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
     const int D = (int)M.rff_dim;
     const int D8 = MLSK_RFF_MMA ? (D + 7) & ~7 : D;
     const int tid = threadIdx.x;
-    const float scale = (float)M.rff_scale;
+    // (FP16 pairs: the features carry the model's power-of-two panel scale, undone in the GEMM's epilogue)
+    const float scale = (float)M.rff_scale * pscale;
     const int64_t ngrp = (nkc + RFF_CH - 1) / RFF_CH;  // column groups of RFF_CH K-chunks
     const int64_t nrb = (MP > PP ? MP : PP) / RFF_RB;  // row blocks (A rows / B columns, m == p)
     const int64_t rb_per = (nrb + RFF_RSPLIT - 1) / RFF_RSPLIT;
@@ -786,14 +841,21 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                     }
                     const int rti = (int)(rb - rt) + rr;  // row within the 128-row panel tile
                     const int off = sw_off(rti, ttn) / 4;  // floats
+                    if (bfx == 2) {  // FP16 pairs: one tile per operand
+                        if (rb < MP) store_h16_pair(reinterpret_cast<unsigned char*>(Ahi + oa), rti, ttn, z0, z1);
+                        if (write_b && rb < PP)
+                            store_h16_pair(reinterpret_cast<unsigned char*>(Bhi + ob), rti, ttn, __fmul_rn(w0, z0),
+                                           __fmul_rn(w1, z1));
+                        continue;
+                    }
                     if (rb < MP) {
                         *reinterpret_cast<float2*>(Ahi + oa + off) = make_float2(z0, z1);
-                        store_lo_pair(reinterpret_cast<unsigned char*>(Alo + oa), rti, ttn, z0, z1, bfx);
+                        store_lo_pair(reinterpret_cast<unsigned char*>(Alo + oa), rti, ttn, z0, z1, bfx != 0);
                     }
                     if (write_b && rb < PP) {
                         const float v0 = __fmul_rn(w0, z0), v1 = __fmul_rn(w1, z1);
                         *reinterpret_cast<float2*>(Bhi + ob + off) = make_float2(v0, v1);
-                        store_lo_pair(reinterpret_cast<unsigned char*>(Blo + ob), rti, ttn, v0, v1, bfx);
+                        store_lo_pair(reinterpret_cast<unsigned char*>(Blo + ob), rti, ttn, v0, v1, bfx != 0);
                     }
                 }
             }
@@ -833,6 +895,17 @@ k_gen_panels_rff(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restri
                     v[q] = __fmul_rn(wv4[q], z[q]);
                 }
                 const int off = sw_off(r, tt) / 4;  // floats
+                if (bfx == 2) {
+                    if (rb < MP) {
+                        store_h16_pair(reinterpret_cast<unsigned char*>(Ahi + oa), r, tt, z[0], z[1]);
+                        store_h16_pair(reinterpret_cast<unsigned char*>(Ahi + oa), r, tt + 2, z[2], z[3]);
+                    }
+                    if (write_b && rb < PP) {
+                        store_h16_pair(reinterpret_cast<unsigned char*>(Bhi + ob), r, tt, v[0], v[1]);
+                        store_h16_pair(reinterpret_cast<unsigned char*>(Bhi + ob), r, tt + 2, v[2], v[3]);
+                    }
+                    continue;
+                }
                 if (rb < MP) {
                     *reinterpret_cast<float4*>(Ahi + oa + off) = make_float4(z[0], z[1], z[2], z[3]);
                     if (bfx) {
@@ -888,7 +961,8 @@ struct TcShape {
     // merged sampled columns on the shared panel: the negated leading chunks
     // per sample (mk_info[b].neg_kc) instead of neg_kc
     const MkInfo* mk_info;
-    // BF16 cross terms: the lo tiles' rows hold bf16(x) | bf16(x - tf32(x))
+    // 1: BF16 cross terms (the lo tiles' rows hold bf16(x) | bf16(x - tf32(x)));
+    // 2: FP16 pairs (one tile per operand, rows fp16(x) | fp16(x - fp16(x)))
     int bfx;
     // K-chunks per TMEM accumulation segment (0: a CTA's whole K-range of a
     // sample is one segment).  tcgen05's fp32 accumulation rounds the running
@@ -1042,7 +1116,8 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
 #ifdef MLSK_TC_ABL_NOLD  // ablation (timing only, wrong results): no operand loads
                 bar_arrive(full);
 #else
-                bar_expect_tx(full, STB);
+                const bool h16 = sh.bfx == 2;  // FP16 pairs: one tile per operand (half the bytes)
+                bar_expect_tx(full, h16 ? TA_BYTES + BB : STB);
                 MLSK_DCHECK(b < (kpar ? 1 : sh.nb) && kc < sh.nkc && (int64_t)tm * TBM < sh.MP &&
                             (int64_t)tn * TBN < sh.PP);
                 const int64_t oa = ((b * sh.nkc + kc) * sh.MP + (int64_t)tm * TBM) * TBK;
@@ -1050,9 +1125,9 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 const int64_t ob = ((b * sh.nkc + kc) * sh.PP + (int64_t)tn * TBN + (PAIR ? rank * TBM : 0)) * TBK;
                 const uint32_t st = smem_addr(ring + s * STB);
                 bulk_load(st, Ahi + oa, TA_BYTES, full);
-                bulk_load(st + TA_BYTES, Alo + oa, TA_BYTES, full);
+                if (!h16) bulk_load(st + TA_BYTES, Alo + oa, TA_BYTES, full);
                 bulk_load(st + 2 * TA_BYTES, Bhi + ob, BB, full);
-                bulk_load(st + 2 * TA_BYTES + BB, Blo + ob, BB, full);
+                if (!h16) bulk_load(st + 2 * TA_BYTES + BB, Blo + ob, BB, full);
 #endif
                 if (++s == NST) { s = 0; ph ^= 1; }
                 if (++kc == ke) { kc = kb; b += sh.Gs; }
@@ -1096,7 +1171,23 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 const uint32_t st = smem_addr(ring + s * STB);
                 const uint32_t dcol = tmem + (uint32_t)abuf * TBN;
                 const uint32_t id = sh.kc0 + kc < neg_kc ? idesc | (1u << 14) : idesc;  // negate B
-                if (sh.bfx) {
+                if (sh.bfx == 2) {
+                    // FP16 pairs: hi x hi, hi x lo, lo x hi over the row halves of the one tile
+                    constexpr uint32_t idh0 = f16_idesc(PAIR ? 2 * TBM : TBM, TBN);
+                    const uint32_t idh = sh.kc0 + kc < neg_kc ? idh0 | (1u << 14) : idh0;
+                    const uint32_t sbh = st + 2 * TA_BYTES;
+#ifndef MLSK_TC_ABL_NOMMA
+                    if (PAIR) {
+                        tc_mma_bf16_pair(dcol, sw_desc(st), sw_desc(sbh), idh, sgc > 0 ? 1u : 0u);
+                        tc_mma_bf16_pair(dcol, sw_desc(st), sw_desc(sbh + 32), idh, 1u);
+                        tc_mma_bf16_pair(dcol, sw_desc(st + 32), sw_desc(sbh), idh, 1u);
+                    } else {
+                        tc_mma_bf16(dcol, sw_desc(st), sw_desc(sbh), idh, sgc > 0 ? 1u : 0u);
+                        tc_mma_bf16(dcol, sw_desc(st), sw_desc(sbh + 32), idh, 1u);
+                        tc_mma_bf16(dcol, sw_desc(st + 32), sw_desc(sbh), idh, 1u);
+                    }
+#endif
+                } else if (sh.bfx) {
                     // hi x hi as two TF32 MMAs (K = 8 each), the cross terms a b_lo and
                     // a_lo b as two BF16 MMAs (K = 16) over the row halves of the lo tiles
                     constexpr uint32_t idb0 = bf16_idesc(PAIR ? 2 * TBM : TBM, TBN);
@@ -1491,6 +1582,20 @@ class TcEngine final : public PanelEngine {
         // BF16 cross terms.  MLSK_TC_BF16X=0: three TF32 MMAs per K-step
         const char* bfx_env = std::getenv("MLSK_TC_BF16X");
         bfx_ = !(bfx_env && std::strcmp(bfx_env, "0") == 0) ? 1 : 0;
+        // FP16 pairs for models with bounded entries (fp32 Gaussian draws, random
+        // Fourier features with the fast generator).  MLSK_TC_H16=0: BF16 cross terms
+        const char* h16_env = std::getenv("MLSK_TC_H16");
+        const bool bounded = M.dm.kind == MLSK_MODEL_GAUSS_MEAN ||
+                             (M.dm.kind == MLSK_MODEL_RFF && M.dm.rff_dim <= RFF_DMAX);
+        if (bfx_ && bounded && !(h16_env && std::strcmp(h16_env, "0") == 0)) bfx_ = 2;
+        // panel scale (a power of two): RFF features are ~ sqrt(2 / n); scaled to [1, 2)
+        // so that the lo halves stay normal fp16 numbers
+        pscale_ = 1.0f;
+        if (bfx_ == 2 && M.dm.kind == MLSK_MODEL_RFF && M.dm.rff_scale > 0) {
+            int e = 0;
+            std::frexp(M.dm.rff_scale, &e);  // rff_scale = f 2^e, f in [0.5, 1)
+            pscale_ = std::ldexp(1.0f, 1 - e);
+        }
         once_per_device((const void*)&k_gemm_tf32x3<false, false, false>, [smem, rsmem] {
             for (auto f : {k_gemm_tf32x3<false, false, false>, k_gemm_tf32x3<false, true, false>,
                            k_gemm_tf32x3<true, false, false>, k_gemm_tf32x3<true, true, false>,
@@ -1521,7 +1626,7 @@ class TcEngine final : public PanelEngine {
     int merge_mode(int64_t c, int64_t cc, double w_fine, double w_coarse) const override {
         return shared_panel(c, cc, w_fine, w_coarse) ? 2 : 1;
     }
-    int64_t chunk_bytes() const override { return (MP_ + PP_) * TBK * 8; }  // hi + lo
+    int64_t chunk_bytes() const override { return (MP_ + PP_) * TBK * (bfx_ == 2 ? 4 : 8); }  // hi + lo (FP16 pairs: 4 B)
     bool splits_k() const override { return true; }
     int64_t group_size() const override { return Gs_; }
     void gen(cudaStream_t s, uint64_t seed, uint64_t tag, const int64_t* ks, int nb, int64_t c, int64_t cc,
@@ -1535,7 +1640,7 @@ class TcEngine final : public PanelEngine {
                                                       (int64_t)nsm_ * 5),
                                RFF_T, rff_smem_, s>>>(
                 S_, seed, tag, ks, nb, c, cc, (float)w_fine, (float)w_coarse, MP_, PP_, k, kr.kc0,
-                shared_panel(c, cc, w_fine, w_coarse) ? 0 : 1, Ahi, Alo, Bhi, Blo, idx, kr.mk, kr.mk_stride, kr.mk_info, bfx_);
+                shared_panel(c, cc, w_fine, w_coarse) ? 0 : 1, Ahi, Alo, Bhi, Blo, idx, kr.mk, kr.mk_stride, kr.mk_info, bfx_, pscale_);
         } else {
             const int grid = (int)std::min<int64_t>((int64_t)nb * k, gen_cap_);
             if (M_.dm.kind == MLSK_MODEL_GAUSS_MEAN)
@@ -1566,6 +1671,7 @@ class TcEngine final : public PanelEngine {
             neg_kc = w_coarse < 0 ? cc / TBK : 0;
             escale = (float)std::fabs(w_fine);
         }
+        escale *= 1.0f / (pscale_ * pscale_);  // FP16 pairs: both operands carry the panel scale
         // merged sampled columns: sign groups only on the shared panel (mode 2)
         const MkInfo* mk_info = kr.mk && shared_panel(c, cc, w_fine, w_coarse) ? kr.mk_info : nullptr;
         double* part = ws_.partial.p;
@@ -1583,7 +1689,7 @@ class TcEngine final : public PanelEngine {
         const int64_t w1 = (T_ + nsm_ - 1) / nsm_, w2 = (2 * T_ + nsm_ - 1) / nsm_;
         if (kr.part == 0 && nb == 1 && direct && w2 < 2 * w1 && k >= 16 && !sym_nb_) {
             ws_.ypart.ensure((size_t)2 * T_ * TBM * TBN);
-            TcShape sh{1, k, MP_, PP_, T_, 2, tiles_n_, nullptr, M_.rows, M_.cols, 1, 0, 0, 0, 1.0f, nullptr, bfx_, seg_};
+            TcShape sh{1, k, MP_, PP_, T_, 2, tiles_n_, nullptr, M_.rows, M_.cols, 1, 0, 0, 0, escale, nullptr, bfx_, seg_};
             {
                 Prof p("gemm_tf32x3", s);
                 launch_gemm(true, segmented(k - (k + 1) / 2), 2 * T_, s, Ahi, Alo, Bhi, Blo, sh, part, part_sq, 1,
@@ -1688,6 +1794,12 @@ class TcEngine final : public PanelEngine {
     void split(void* panels, int nb, int64_t k, float*& Ahi, float*& Alo, float*& Bhi, float*& Blo) const {
         const size_t na = (size_t)nb * k * MP_ * TBK, nbp = (size_t)nb * k * PP_ * TBK;
         Ahi = static_cast<float*>(panels);
+        if (bfx_ == 2) {  // FP16 pairs: one array per operand (64-byte rows, like a hi array)
+            Alo = nullptr;
+            Bhi = Ahi + na;
+            Blo = nullptr;
+            return;
+        }
         Alo = Ahi + na;
         Bhi = Alo + na;
         Blo = Bhi + nbp;
@@ -1698,7 +1810,8 @@ class TcEngine final : public PanelEngine {
     int nsm_, T_, Gs_, tiles_n_, smem_, rff_smem_;
     int sym_nb_ = 0;  // symmetric output: 256-blocks per side (0 = full tile grid)
     bool pair_ = false;  // CTA-pair GEMM (cta_group::2)
-    int bfx_ = 0;        // BF16 cross terms (lo tiles as BF16 pairs)
+    int bfx_ = 0;        // 1: BF16 cross terms (lo tiles as BF16 pairs); 2: FP16 pairs (one tile per operand)
+    float pscale_ = 1.0f;  // FP16 pairs: power-of-two scale of the generated entries (undone in the epilogue)
     int seg_ = TC_SEG;
     bool shared_env_ = true;
     int64_t gen_cap_;
