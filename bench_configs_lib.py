@@ -282,19 +282,26 @@ def measure(ids, steps=3, with_cpu=True, device=0):
             blk["algorithmic_tflops"] = flops / (ms * 1e-3) / 1e12
             blk["step_frac_of_peak"] = blk["algorithmic_tflops"] / (peak_t / 3)
             blk["peaks_tf32"] = {"burst": tf32, "sustained": tf32_sus, "used": which}
-            bfx = os.environ.get("MLSK_TC_BF16X", "1") != "0" and os.environ.get("MLSK_TC_PAIR", "1") != "0"
+            bfx = os.environ.get("MLSK_TC_BF16X", "1") != "0"
+            # bounded models (configs 3, 4) run FP16 pairs: 3 K = 16 MMAs per K-chunk (the cost of 1.5 TF32
+            # K-steps of two); config 5 TF32 hi x hi + BF16 cross terms: 4 MMA slots instead of 6
+            h16 = bfx and cid in (3, 4) and os.environ.get("MLSK_TC_H16", "1") != "0"
+            own = (peak_t * 2 / 3) if h16 else (peak_t / 2 if bfx else peak_t / 3)
             blk["roofline"] = {"bound": "tensor", "achieved": ach, "peak": peak_t / 3, "unit": "TFLOP/s",
                                "frac": ach / (peak_t / 3) if ach else None, "traffic": None,
-                               "kernel": ("k_gemm_tf32x3 (tcgen05.mma cta_group::2: per 16-column K-chunk 2 kind::tf32 "
+                               "kernel": ("k_gemm_tf32x3 (tcgen05.mma cta_group::2 kind::f16: per 16-column K-chunk 3 FP16 "
+                                          "MMAs over fp16(x) | fp16(x - fp16(x)) pairs: hi x hi, hi x lo, lo x hi)" if h16 else
+                                          "k_gemm_tf32x3 (tcgen05.mma cta_group::2: per 16-column K-chunk 2 kind::tf32 "
                                           "MMAs for hi x hi + 2 kind::f16 BF16 MMAs for the cross terms)" if bfx else
                                           "k_gemm_tf32x3 (tcgen05.mma kind::tf32, 3 MMAs per K-step)"),
                                "peak_source": f"dense TF32 tcgen05 measured in this run, {which} "
                                               f"({peak_t:.0f} TFLOP/s) / 3",
-                               # SURVEY 8(d)'s fp32 peak is TF32 / 3 (3xTF32).  With BF16 cross terms a K-chunk
-                               # costs 4 MMA slots instead of 6, so the kernel's own ceiling is TF32 / 2 and
-                               # `frac` can approach 1.5 x (tensor time) -- both fractions are given.
-                               "frac_of_own_ceiling": (ach / (peak_t / 2) if ach and bfx else
-                                                       (ach / (peak_t / 3) if ach else None)),
+                               # SURVEY 8(d)'s fp32 peak is TF32 / 3 (3xTF32).  With split 16-bit operands a
+                               # K-chunk costs 3 (FP16 pairs) or 4 (TF32 + BF16) MMA slots instead of 6, so the
+                               # kernel's own ceiling is 2/3 or 1/2 of the TF32 peak and `frac` can exceed 1:
+                               # both fractions are given.
+                               "own_ceiling": own,
+                               "frac_of_own_ceiling": (ach / own) if ach else None,
                                "algorithmic": ("P(P+1) c + 2 P D c flops per level-sample (SYRK + features)"
                                                if cid == 4 else "2 m p c flops per level-sample")}
         if not c.get("inner"):
