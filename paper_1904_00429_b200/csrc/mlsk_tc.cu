@@ -344,6 +344,37 @@ __device__ __forceinline__ void store_h16_pair(unsigned char* t, int r, int k, f
     *reinterpret_cast<uint32_t*>(t + sw_off_b(r, k, 0)) = h;
     *reinterpret_cast<uint32_t*>(t + sw_off_b(r, k, 1)) = f16x2_rn(__fsub_rn(v0, h0), __fsub_rn(v1, h1));
 }
+// ---- FP16 hi + BF16 cross terms (TcShape::bfx == 3, unbounded fp32 models:
+// Student-t).  hi = fp16(x) saturating, and the cross terms as in the BF16 form
+// over bf16(x) and bf16(x - hi): whatever hi cannot hold -- the excess of a tail
+// draw beyond 65504, the low bits of a tiny entry -- lands in the BF16 lo part,
+// which has fp32's exponent range.  6 bytes per entry: the first tile's 64-byte
+// rows are hi(r, 0..15) | bf16(x)(r, 0..15), a second tile of 32-byte rows
+// (K-major SWIZZLE_32B, 4 KB per 128 rows) holds bf16(x - hi); a K-chunk is one
+// FP16 MMA (hi x hi) + two BF16 MMAs (x b_lo: A from the first tile's second row
+// half, B from the second tile; a_lo b the other way round).
+constexpr int LROWB = TBK * 2;        // bytes per row of the BF16 lo tile
+constexpr int LTILE = TBM * LROWB;    // 4 KB per 128 rows
+__device__ __forceinline__ int sw32_off(int r, int k) {  // BF16 element (r, k), SWIZZLE_32B
+    return r * LROWB + ((((k >> 3) ^ ((r * LROWB >> 7) & 1)) << 4) | ((k & 7) << 1));
+}
+__device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
+    uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+    d |= (uint64_t)1 << 16;                   // LBO (unused for swizzled K-major)
+    d |= (uint64_t)((8 * LROWB) >> 4) << 32;  // SBO: 8-row groups
+    d |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
+    d |= (uint64_t)6 << 61;                   // SWIZZLE_32B
+    return d;
+}
+// chunk columns k, k + 1 (k even) of row r: t1 = the hi | bf16(x) tile, t2 = the bf16 lo tile
+__device__ __forceinline__ void store_h16b_pair(unsigned char* t1, unsigned char* t2, int r, int k, float v0, float v1) {
+    const uint32_t h = f16x2_rn(v0, v1);
+    float h0, h1;
+    f16x2_unpack(h, h0, h1);
+    *reinterpret_cast<uint32_t*>(t1 + sw_off_b(r, k, 0)) = h;
+    *reinterpret_cast<uint32_t*>(t1 + sw_off_b(r, k, 1)) = bf16x2_rn(v0, v1);
+    *reinterpret_cast<uint32_t*>(t2 + sw32_off(r, k)) = bf16x2_rn(__fsub_rn(v0, h0), __fsub_rn(v1, h1));
+}
 // kind::f16 instruction descriptor: F32 accumulate, FP16 A / B, K-major, M x N
 __host__ __device__ constexpr uint32_t f16_idesc(int M, int N) {
     return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -466,6 +497,10 @@ __device__ __forceinline__ void gauss_phase_f32(const DevModel& M, const Tables&
             store_h16_pair(thi, r0 + e, 2 * cp, v[0][e], v[1][e]);
             continue;
         }
+        if (bfx == 3) {  // FP16 hi | BF16 values, BF16 lo
+            store_h16b_pair(thi, tlo, r0 + e, 2 * cp, v[0][e], v[1][e]);
+            continue;
+        }
         const int off = sw_off(r0 + e, 2 * cp);  // chunk columns 2cp, 2cp+1: adjacent words
         *reinterpret_cast<float2*>(thi + off) = make_float2(v[0][e], v[1][e]);
         store_lo_pair(tlo, r0 + e, 2 * cp, v[0][e], v[1][e], bfx != 0);
@@ -480,7 +515,7 @@ __device__ __forceinline__ void gauss_phase_f32(const DevModel& M, const Tables&
 template <bool IS_A>
 __device__ __forceinline__ void student_t_phase_f32(const TcModel& S, const Tables& T, uint64_t key, int64_t rb,
                                                     const int* s_j, const float* s_w, unsigned char* thi,
-                                                    unsigned char* tlo, int tid, int bfx) {
+                                                    unsigned char* tlo, int tid, int bfx, float ascale) {
     const int cp = tid & 7, qq = tid >> 3;
     const int r0 = 4 * qq;
     const int64_t lim = (IS_A ? S.M.m : S.M.p) - rb;
@@ -499,7 +534,7 @@ __device__ __forceinline__ void student_t_phase_f32(const TcModel& S, const Tabl
             if (r0 + e < lim) {
                 x = __fadd_rn(st_mean_of(mw[e], S.M.st_lo, S.M.st_w),
                               student_t_draw(key, j, rb + r0 + e, IS_A ? 0 : 1, T));
-                if (!IS_A) x = __fmul_rn(w, x);
+                x = __fmul_rn(IS_A ? ascale : w, x);
             }
             v[u][e] = x;
         }
@@ -508,6 +543,10 @@ __device__ __forceinline__ void student_t_phase_f32(const TcModel& S, const Tabl
     for (int e = 0; e < 4; ++e) {
         if (bfx == 2) {
             store_h16_pair(thi, r0 + e, 2 * cp, v[0][e], v[1][e]);
+            continue;
+        }
+        if (bfx == 3) {
+            store_h16b_pair(thi, tlo, r0 + e, 2 * cp, v[0][e], v[1][e]);
             continue;
         }
         const int off = sw_off(r0 + e, 2 * cp);
@@ -536,8 +575,11 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                   int64_t cc, float w_fine, float w_coarse, int64_t MP, int64_t PP, int64_t nkc, int64_t kc0,
                   float* __restrict__ Ahi, float* __restrict__ Alo, float* __restrict__ Bhi, float* __restrict__ Blo,
                   uint32_t* __restrict__ idx_out, const MkEntry* __restrict__ mk, int64_t mk_stride,
-                  const MkInfo* __restrict__ mk_info, int bfx_i) {
-    const int bfx = bfx_i;  // 0: TF32 lo tiles; 1: BF16 cross-term tiles; 2: FP16 pairs (one tile)
+                  const MkInfo* __restrict__ mk_info, int bfx_i, float ascale, float wscale) {
+    // ascale / wscale (FP16 hi + BF16, bfx == 3): powers of two on the A entries and on the B
+    // weights that keep fp16(x) far from saturation (Student-t tails times weights up to
+    // n / c); the GEMM's epilogue undoes them exactly
+    const int bfx = bfx_i;  // 0: TF32 lo; 1: BF16 cross-term tiles; 2: FP16 pairs (one tile); 3: FP16 hi + BF16
     __shared__ __align__(1024) unsigned char tbuf[2][2][TTILE];  // [buffer][hi / lo], double-buffered
     __shared__ __align__(16) float2 s_sc[256];  // full-circle sincos table
     __shared__ __align__(16) float2 s_lg[64];
@@ -582,7 +624,7 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                 if (idx_out) idx_out[(int64_t)b * c + t] = ix;
             }
             s_j[tid] = j;
-            s_w[tid] = w;
+            s_w[tid] = __fmul_rn(w, wscale);
         }
         __syncthreads();
         for (int ph = 0; ph < a_ph + b_ph; ++ph) {
@@ -595,8 +637,8 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                 if (isA) gauss_phase_f32<true>(M, T, key, rb, s_j, s_w, thi, tlo, tid, bfx);
                 else gauss_phase_f32<false>(M, T, key, rb, s_j, s_w, thi, tlo, tid, bfx);
             } else if (KIND == GK_STUDENT_T) {
-                if (isA) student_t_phase_f32<true>(S, T, key, rb, s_j, s_w, thi, tlo, tid, bfx);
-                else student_t_phase_f32<false>(S, T, key, rb, s_j, s_w, thi, tlo, tid, bfx);
+                if (isA) student_t_phase_f32<true>(S, T, key, rb, s_j, s_w, thi, tlo, tid, bfx, ascale);
+                else student_t_phase_f32<false>(S, T, key, rb, s_j, s_w, thi, tlo, tid, bfx, ascale);
             } else {
                 for (int item = tid; item < TBM * TBK; item += GEN_T) {
                     const int tt = item & (TBK - 1), rr = item / TBK;
@@ -606,15 +648,22 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
                         float x;
                         if (M.kind == MLSK_MODEL_STUDENT_T) x = student_t_entry(S, key, j, rb + rr, isA ? 0 : 1, T);
                         else x = rff_entry(M, j, rb + rr);  // RFF (D > 64): B = A^T
-                        v = isA ? x : __fmul_rn(s_w[tt], x);
+                        v = __fmul_rn(isA ? ascale : s_w[tt], x);
                     }
-                    if (bfx == 2) {
+                    if (bfx == 2 || bfx == 3) {
                         const uint32_t h = f16x2_rn(v, 0.f);
                         float h0, h1;
                         f16x2_unpack(h, h0, h1);
                         *reinterpret_cast<unsigned short*>(thi + sw_off_b(rr, tt, 0)) = (unsigned short)(h & 0xffffu);
-                        *reinterpret_cast<unsigned short*>(thi + sw_off_b(rr, tt, 1)) =
-                            (unsigned short)(f16x2_rn(__fsub_rn(v, h0), 0.f) & 0xffffu);
+                        if (bfx == 2) {
+                            *reinterpret_cast<unsigned short*>(thi + sw_off_b(rr, tt, 1)) =
+                                (unsigned short)(f16x2_rn(__fsub_rn(v, h0), 0.f) & 0xffffu);
+                        } else {
+                            *reinterpret_cast<unsigned short*>(thi + sw_off_b(rr, tt, 1)) =
+                                (unsigned short)(bf16x2_rn(v, 0.f) & 0xffffu);
+                            *reinterpret_cast<unsigned short*>(tlo + sw32_off(rr, tt)) =
+                                (unsigned short)(bf16x2_rn(__fsub_rn(v, h0), 0.f) & 0xffffu);
+                        }
                         continue;
                     }
                     *reinterpret_cast<float*>(thi + sw_off(rr, tt)) = v;
@@ -634,9 +683,9 @@ k_gen_panels_tf32(TcModel S, uint64_t seed, uint64_t tag, const int64_t* __restr
             if (tid == 0) {
                 const int64_t off = (((int64_t)b * nkc + kc) * (isA ? MP : PP) + rb) * TBK;
                 float* dh = (isA ? Ahi : Bhi) + off;
-                float* dl = (isA ? Alo : Blo) + off;
                 bulk_store(dh, thi, TTILE);
-                if (bfx != 2) bulk_store(dl, tlo, TTILE);
+                if (bfx == 3) bulk_store((isA ? Alo : Blo) + off / 2, tlo, LTILE);  // 32-byte rows: half the floats
+                else if (bfx != 2) bulk_store((isA ? Alo : Blo) + off, tlo, TTILE);
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // the other buffer is free
             }
@@ -962,7 +1011,8 @@ struct TcShape {
     // per sample (mk_info[b].neg_kc) instead of neg_kc
     const MkInfo* mk_info;
     // 1: BF16 cross terms (the lo tiles' rows hold bf16(x) | bf16(x - tf32(x)));
-    // 2: FP16 pairs (one tile per operand, rows fp16(x) | fp16(x - fp16(x)))
+    // 2: FP16 pairs (one tile per operand, rows fp16(x) | fp16(x - fp16(x)));
+    // 3: FP16 hi + BF16 cross terms (rows fp16(x) | bf16(x), and a tile of bf16(x - fp16(x)))
     int bfx;
     // K-chunks per TMEM accumulation segment (0: a CTA's whole K-range of a
     // sample is one segment).  tcgen05's fp32 accumulation rounds the running
@@ -1117,7 +1167,8 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 bar_arrive(full);
 #else
                 const bool h16 = sh.bfx == 2;  // FP16 pairs: one tile per operand (half the bytes)
-                bar_expect_tx(full, h16 ? TA_BYTES + BB : STB);
+                const bool h16b = sh.bfx == 3;  // FP16 hi | BF16 values + a BF16 lo tile of half the size
+                bar_expect_tx(full, h16 ? TA_BYTES + BB : h16b ? (TA_BYTES + BB) * 3 / 2 : STB);
                 MLSK_DCHECK(b < (kpar ? 1 : sh.nb) && kc < sh.nkc && (int64_t)tm * TBM < sh.MP &&
                             (int64_t)tn * TBN < sh.PP);
                 const int64_t oa = ((b * sh.nkc + kc) * sh.MP + (int64_t)tm * TBM) * TBK;
@@ -1125,9 +1176,11 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 const int64_t ob = ((b * sh.nkc + kc) * sh.PP + (int64_t)tn * TBN + (PAIR ? rank * TBM : 0)) * TBK;
                 const uint32_t st = smem_addr(ring + s * STB);
                 bulk_load(st, Ahi + oa, TA_BYTES, full);
-                if (!h16) bulk_load(st + TA_BYTES, Alo + oa, TA_BYTES, full);
+                if (h16b) bulk_load(st + TA_BYTES, Alo + oa / 2, TA_BYTES / 2, full);
+                else if (!h16) bulk_load(st + TA_BYTES, Alo + oa, TA_BYTES, full);
                 bulk_load(st + 2 * TA_BYTES, Bhi + ob, BB, full);
-                if (!h16) bulk_load(st + 2 * TA_BYTES + BB, Blo + ob, BB, full);
+                if (h16b) bulk_load(st + 2 * TA_BYTES + BB, Blo + ob / 2, BB / 2, full);
+                else if (!h16) bulk_load(st + 2 * TA_BYTES + BB, Blo + ob, BB, full);
 #endif
                 if (++s == NST) { s = 0; ph ^= 1; }
                 if (++kc == ke) { kc = kb; b += sh.Gs; }
@@ -1185,6 +1238,24 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                         tc_mma_bf16(dcol, sw_desc(st), sw_desc(sbh), idh, sgc > 0 ? 1u : 0u);
                         tc_mma_bf16(dcol, sw_desc(st), sw_desc(sbh + 32), idh, 1u);
                         tc_mma_bf16(dcol, sw_desc(st + 32), sw_desc(sbh), idh, 1u);
+                    }
+#endif
+                } else if (sh.bfx == 3) {
+                    // FP16 hi x hi; the cross terms as BF16 MMAs: bf16(x) is the second row half of
+                    // the first tile, the lo parts are the SWIZZLE_32B tile
+                    constexpr uint32_t idh0 = f16_idesc(PAIR ? 2 * TBM : TBM, TBN);
+                    constexpr uint32_t idb0 = bf16_idesc(PAIR ? 2 * TBM : TBM, TBN);
+                    const uint32_t ng = sh.kc0 + kc < neg_kc ? (1u << 14) : 0u;
+                    const uint32_t sal = st + TA_BYTES, sbh = st + 2 * TA_BYTES, sbl = sbh + BB;
+#ifndef MLSK_TC_ABL_NOMMA
+                    if (PAIR) {
+                        tc_mma_bf16_pair(dcol, sw_desc(st), sw_desc(sbh), idh0 | ng, sgc > 0 ? 1u : 0u);
+                        tc_mma_bf16_pair(dcol, sw_desc(st + 32), sw32_desc(sbl), idb0 | ng, 1u);   // x b_lo
+                        tc_mma_bf16_pair(dcol, sw32_desc(sal), sw_desc(sbh + 32), idb0 | ng, 1u);  // a_lo x
+                    } else {
+                        tc_mma_bf16(dcol, sw_desc(st), sw_desc(sbh), idh0 | ng, sgc > 0 ? 1u : 0u);
+                        tc_mma_bf16(dcol, sw_desc(st + 32), sw32_desc(sbl), idb0 | ng, 1u);
+                        tc_mma_bf16(dcol, sw32_desc(sal), sw_desc(sbh + 32), idb0 | ng, 1u);
                     }
 #endif
                 } else if (sh.bfx) {
@@ -1587,7 +1658,7 @@ class TcEngine final : public PanelEngine {
         const char* h16_env = std::getenv("MLSK_TC_H16");
         const bool bounded = M.dm.kind == MLSK_MODEL_GAUSS_MEAN ||
                              (M.dm.kind == MLSK_MODEL_RFF && M.dm.rff_dim <= RFF_DMAX);
-        if (bfx_ && bounded && !(h16_env && std::strcmp(h16_env, "0") == 0)) bfx_ = 2;
+        if (bfx_ && !(h16_env && std::strcmp(h16_env, "0") == 0)) bfx_ = bounded ? 2 : 3;
         // panel scale (a power of two): RFF features are ~ sqrt(2 / n); scaled to [1, 2)
         // so that the lo halves stay normal fp16 numbers
         pscale_ = 1.0f;
@@ -1619,6 +1690,14 @@ class TcEngine final : public PanelEngine {
             MLSK_CUDA(cudaFuncSetAttribute(k_gen_panels_tf32<GK_GENERIC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         });
     }
+    // FP16 hi + BF16 (bfx_ == 3): entries of A times 2^-6, weights of B times 2^-6 / 2^floor(log2 |w_fine|)
+    float a_scale() const { return bfx_ == 3 ? 0.015625f : 1.0f; }
+    float w_scale(double w_fine) const {
+        if (bfx_ != 3 || !(std::fabs(w_fine) > 0)) return 1.0f;
+        int e = 0;
+        std::frexp(std::fabs(w_fine), &e);  // |w_fine| = f 2^e, f in [0.5, 1)
+        return std::ldexp(0.015625f, 1 - e);
+    }
     int64_t chunk_cols() const override { return TBK; }
     // merged sampled columns: on the shared RFF panel the columns carry the scale
     // sqrt(|W_j| / |w|) in sign groups (mode 2); otherwise the summed weights
@@ -1626,7 +1705,8 @@ class TcEngine final : public PanelEngine {
     int merge_mode(int64_t c, int64_t cc, double w_fine, double w_coarse) const override {
         return shared_panel(c, cc, w_fine, w_coarse) ? 2 : 1;
     }
-    int64_t chunk_bytes() const override { return (MP_ + PP_) * TBK * (bfx_ == 2 ? 4 : 8); }  // hi + lo (FP16 pairs: 4 B)
+    // hi + lo: 8 bytes per entry (FP16 pairs: 4, FP16 hi + BF16: 6)
+    int64_t chunk_bytes() const override { return (MP_ + PP_) * TBK * (bfx_ == 2 ? 4 : bfx_ == 3 ? 6 : 8); }
     bool splits_k() const override { return true; }
     int64_t group_size() const override { return Gs_; }
     void gen(cudaStream_t s, uint64_t seed, uint64_t tag, const int64_t* ks, int nb, int64_t c, int64_t cc,
@@ -1646,15 +1726,15 @@ class TcEngine final : public PanelEngine {
             if (M_.dm.kind == MLSK_MODEL_GAUSS_MEAN)
                 k_gen_panels_tf32<GK_GAUSS><<<grid, GEN_T, 0, s>>>(S_, seed, tag, ks, nb, c, cc, (float)w_fine,
                                                                   (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi,
-                                                                  Blo, idx, kr.mk, kr.mk_stride, kr.mk_info, bfx_);
+                                                                  Blo, idx, kr.mk, kr.mk_stride, kr.mk_info, bfx_, a_scale(), w_scale(w_fine));
             else if (M_.dm.kind == MLSK_MODEL_STUDENT_T)
                 k_gen_panels_tf32<GK_STUDENT_T><<<grid, GEN_T, 0, s>>>(S_, seed, tag, ks, nb, c, cc, (float)w_fine,
                                                                       (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo,
-                                                                      Bhi, Blo, idx, kr.mk, kr.mk_stride, kr.mk_info, bfx_);
+                                                                      Bhi, Blo, idx, kr.mk, kr.mk_stride, kr.mk_info, bfx_, a_scale(), w_scale(w_fine));
             else
                 k_gen_panels_tf32<GK_GENERIC><<<grid, GEN_T, 0, s>>>(S_, seed, tag, ks, nb, c, cc, (float)w_fine,
                                                                     (float)w_coarse, MP_, PP_, k, kr.kc0, Ahi, Alo, Bhi,
-                                                                    Blo, idx, kr.mk, kr.mk_stride, kr.mk_info, bfx_);
+                                                                    Blo, idx, kr.mk, kr.mk_stride, kr.mk_info, bfx_, a_scale(), w_scale(w_fine));
         }
         launched();
     }
@@ -1672,6 +1752,7 @@ class TcEngine final : public PanelEngine {
             escale = (float)std::fabs(w_fine);
         }
         escale *= 1.0f / (pscale_ * pscale_);  // FP16 pairs: both operands carry the panel scale
+        escale *= 1.0f / (a_scale() * w_scale(w_fine));  // FP16 hi + BF16: the A / weight scales (powers of two)
         // merged sampled columns: sign groups only on the shared panel (mode 2)
         const MkInfo* mk_info = kr.mk && shared_panel(c, cc, w_fine, w_coarse) ? kr.mk_info : nullptr;
         double* part = ws_.partial.p;
@@ -1801,6 +1882,11 @@ class TcEngine final : public PanelEngine {
             return;
         }
         Alo = Ahi + na;
+        if (bfx_ == 3) {  // the lo arrays hold 32-byte rows: half the floats
+            Bhi = Alo + na / 2;
+            Blo = Bhi + nbp;
+            return;
+        }
         Bhi = Alo + na;
         Blo = Bhi + nbp;
     }
@@ -1810,7 +1896,7 @@ class TcEngine final : public PanelEngine {
     int nsm_, T_, Gs_, tiles_n_, smem_, rff_smem_;
     int sym_nb_ = 0;  // symmetric output: 256-blocks per side (0 = full tile grid)
     bool pair_ = false;  // CTA-pair GEMM (cta_group::2)
-    int bfx_ = 0;        // 1: BF16 cross terms (lo tiles as BF16 pairs); 2: FP16 pairs (one tile per operand)
+    int bfx_ = 0;        // 1: BF16 cross terms; 2: FP16 pairs (one tile per operand); 3: FP16 hi + BF16 cross terms
     float pscale_ = 1.0f;  // FP16 pairs: power-of-two scale of the generated entries (undone in the epilogue)
     int seg_ = TC_SEG;
     bool shared_env_ = true;
