@@ -283,14 +283,16 @@ def measure(ids, steps=3, with_cpu=True, device=0):
             blk["step_frac_of_peak"] = blk["algorithmic_tflops"] / (peak_t / 3)
             blk["peaks_tf32"] = {"burst": tf32, "sustained": tf32_sus, "used": which}
             bfx = os.environ.get("MLSK_TC_BF16X", "1") != "0"
-            # bounded models (configs 3, 4) run FP16 pairs: 3 K = 16 MMAs per K-chunk (the cost of 1.5 TF32
-            # K-steps of two); config 5 TF32 hi x hi + BF16 cross terms: 4 MMA slots instead of 6
-            h16 = bfx and cid in (3, 4) and os.environ.get("MLSK_TC_H16", "1") != "0"
+            # FP16 pairs (bounded models: configs 3, 4) and FP16 hi + BF16 cross terms (config 5) both run
+            # 3 K = 16 MMAs per K-chunk; MLSK_TC_H16=0: TF32 hi x hi + BF16 cross terms, 4 MMA slots instead of 6
+            h16 = bfx and os.environ.get("MLSK_TC_H16", "1") != "0"
             own = (peak_t * 2 / 3) if h16 else (peak_t / 2 if bfx else peak_t / 3)
             blk["roofline"] = {"bound": "tensor", "achieved": ach, "peak": peak_t / 3, "unit": "TFLOP/s",
                                "frac": ach / (peak_t / 3) if ach else None, "traffic": None,
-                               "kernel": ("k_gemm_tf32x3 (tcgen05.mma cta_group::2 kind::f16: per 16-column K-chunk 3 FP16 "
-                                          "MMAs over fp16(x) | fp16(x - fp16(x)) pairs: hi x hi, hi x lo, lo x hi)" if h16 else
+                               "kernel": ("k_gemm_tf32x3 (tcgen05.mma cta_group::2 kind::f16: per 16-column K-chunk 3 MMAs, "
+                                          + ("one FP16 hi x hi + two BF16 cross terms over fp16(x) | bf16(x) and bf16(x - hi))"
+                                             if cid == 5 else
+                                             "FP16 over fp16(x) | fp16(x - fp16(x)) pairs: hi x hi, hi x lo, lo x hi)")) if h16 else
                                           "k_gemm_tf32x3 (tcgen05.mma cta_group::2: per 16-column K-chunk 2 kind::tf32 "
                                           "MMAs for hi x hi + 2 kind::f16 BF16 MMAs for the cross terms)" if bfx else
                                           "k_gemm_tf32x3 (tcgen05.mma kind::tf32, 3 MMAs per K-step)"),
