@@ -287,15 +287,20 @@ def measure(ids, steps=3, with_cpu=True, device=0):
             # 3 K = 16 MMAs per K-chunk; MLSK_TC_H16=0: TF32 hi x hi + BF16 cross terms, 4 MMA slots instead of 6
             h16 = bfx and os.environ.get("MLSK_TC_H16", "1") != "0"
             own = (peak_t * 2 / 3) if h16 else (peak_t / 2 if bfx else peak_t / 3)
+            if h16 and cid == 5:
+                kernel_desc = ("k_gemm_tf32x3 (tcgen05.mma cta_group::2 kind::f16: per 16-column K-chunk 3 MMAs, one FP16 "
+                               "hi x hi + two BF16 cross terms over fp16(x) | bf16(x) and bf16(x - hi))")
+            elif h16:
+                kernel_desc = ("k_gemm_tf32x3 (tcgen05.mma cta_group::2 kind::f16: per 16-column K-chunk 3 FP16 MMAs over "
+                               "fp16(x) | fp16(x - fp16(x)) pairs: hi x hi, hi x lo, lo x hi)")
+            elif bfx:
+                kernel_desc = ("k_gemm_tf32x3 (tcgen05.mma cta_group::2: per 16-column K-chunk 2 kind::tf32 MMAs for "
+                               "hi x hi + 2 kind::f16 BF16 MMAs for the cross terms)")
+            else:
+                kernel_desc = "k_gemm_tf32x3 (tcgen05.mma kind::tf32, 3 MMAs per K-step)"
             blk["roofline"] = {"bound": "tensor", "achieved": ach, "peak": peak_t / 3, "unit": "TFLOP/s",
                                "frac": ach / (peak_t / 3) if ach else None, "traffic": None,
-                               "kernel": ("k_gemm_tf32x3 (tcgen05.mma cta_group::2 kind::f16: per 16-column K-chunk 3 MMAs, "
-                                          + ("one FP16 hi x hi + two BF16 cross terms over fp16(x) | bf16(x) and bf16(x - hi))"
-                                             if cid == 5 else
-                                             "FP16 over fp16(x) | fp16(x - fp16(x)) pairs: hi x hi, hi x lo, lo x hi)")) if h16 else
-                                          "k_gemm_tf32x3 (tcgen05.mma cta_group::2: per 16-column K-chunk 2 kind::tf32 "
-                                          "MMAs for hi x hi + 2 kind::f16 BF16 MMAs for the cross terms)" if bfx else
-                                          "k_gemm_tf32x3 (tcgen05.mma kind::tf32, 3 MMAs per K-step)"),
+                               "kernel": kernel_desc,
                                "peak_source": f"dense TF32 tcgen05 measured in this run, {which} "
                                               f"({peak_t:.0f} TFLOP/s) / 3",
                                # SURVEY 8(d)'s fp32 peak is TF32 / 3 (3xTF32).  With split 16-bit operands a
