@@ -286,7 +286,15 @@ def measure(ids, steps=3, with_cpu=True, device=0):
             # FP16 pairs (bounded models: configs 3, 4) and FP16 hi + BF16 cross terms (config 5) both run
             # 3 K = 16 MMAs per K-chunk; MLSK_TC_H16=0: TF32 hi x hi + BF16 cross terms, 4 MMA slots instead of 6
             h16 = bfx and os.environ.get("MLSK_TC_H16", "1") != "0"
-            own = (peak_t * 2 / 3) if h16 else (peak_t / 2 if bfx else peak_t / 3)
+            # own ceiling: three 16-bit K = 16 MMAs per K-chunk = the dense bf16 / fp16 rate
+            # (MEASURED_PEAKS.json, cuBLAS bf16: burst, or sustained for a long / power-capped region) / 3;
+            # TF32 + BF16 cross terms: 4 MMA slots instead of 6 -> TF32 / 2
+            own = peak_t / 2 if bfx else peak_t / 3
+            if h16:
+                try:
+                    own = (pk["bf16_tflops_sustained"] if long_region else pk["bf16_tflops"]) / 3
+                except Exception:
+                    own = peak_t * 2 / 3
             if h16 and cid == 5:
                 kernel_desc = ("k_gemm_tf32x3 (tcgen05.mma cta_group::2 kind::f16: per 16-column K-chunk 3 MMAs, one FP16 "
                                "hi x hi + two BF16 cross terms over fp16(x) | bf16(x) and bf16(x - hi))")
@@ -304,9 +312,8 @@ def measure(ids, steps=3, with_cpu=True, device=0):
                                "peak_source": f"dense TF32 tcgen05 measured in this run, {which} "
                                               f"({peak_t:.0f} TFLOP/s) / 3",
                                # SURVEY 8(d)'s fp32 peak is TF32 / 3 (3xTF32).  With split 16-bit operands a
-                               # K-chunk costs 3 (FP16 pairs) or 4 (TF32 + BF16) MMA slots instead of 6, so the
-                               # kernel's own ceiling is 2/3 or 1/2 of the TF32 peak and `frac` can exceed 1:
-                               # both fractions are given.
+                               # K-chunk costs three 16-bit MMAs instead of six TF32 ones, so `frac` can exceed 1;
+                               # the kernel's own ceiling is the measured dense bf16 rate / 3: both are given.
                                "own_ceiling": own,
                                "frac_of_own_ceiling": (ach / own) if ach else None,
                                "algorithmic": ("P(P+1) c + 2 P D c flops per level-sample (SYRK + features)"
