@@ -83,15 +83,15 @@ constexpr int PSTAGE_BYTES = 2 * TA_BYTES + 2 * PB_BYTES;  // 32 KB
 static_assert(PSTAGES * PSTAGE_BYTES + 1024 <= 226 * 1024, "pair ring exceeds the shared memory of a CTA");
 // warpgroup 0: producer (warp 0), TMEM allocation + MMA issue (warp 1), two
 // idle warps; warpgroups 1-4: epilogue.  setmaxnreg moves registers from the
-// control warpgroup to the epilogue (24 / 112 per thread) for its 64-entry
+// control warpgroup to the epilogue (32 / 112 per thread) for its 64-entry
 // running sum / sample Y plus a 16-column TMEM load.  The budget is the
 // launch's own allocation (640 threads x 96 = 61440; a launch of 18 warps
 // or more is capped at 96 registers: five warps share one SMSP's 16 K):
-// 4 x 32 x 24 + 16 x 32 x 112 = 60416 <= 61440, so setmaxnreg.inc cannot
+// 4 x 32 x 32 + 16 x 32 x 112 = 61440 <= 61440, so setmaxnreg.inc cannot
 // wait forever for registers no warp will release.
 constexpr int CTRL_WARPS = 4;
 constexpr int TC_THREADS = 32 * (CTRL_WARPS + EPI_WARPS);
-constexpr int CTRL_REGS = 24, EPI_REGS = 112;
+constexpr int CTRL_REGS = 32, EPI_REGS = 112;
 static_assert(32 * (CTRL_WARPS * CTRL_REGS + EPI_WARPS * EPI_REGS) <= TC_THREADS * 96,
               "setmaxnreg budget exceeds the launch allocation: the epilogue's inc would block forever");
 #ifndef MLSK_TC_FLUSH
@@ -560,6 +560,9 @@ __device__ __forceinline__ void student_t_phase_f32(const TcModel& S, const Tabl
 // by the TMA engine.
 // KIND: GK_GAUSS, GK_STUDENT_T, or GK_GENERIC (per-entry loop: RFF with D > 64)
 constexpr int GK_GAUSS = 0, GK_STUDENT_T = 1, GK_GENERIC = 2;
+#ifndef MLSK_TC_TWO
+#define MLSK_TC_TWO 1
+#endif
 #ifndef MLSK_GEN_CHUNK_MAJOR
 #define MLSK_GEN_CHUNK_MAJOR 1
 #endif
@@ -1108,6 +1111,12 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
     const int64_t iters = (int64_t)my_samples * (ke - kb);
     const int64_t seg = SEGM && sh.seg > 0 && sh.seg < ke - kb ? sh.seg : ke - kb;  // K-chunks per TMEM segment
     const int nseg = (int)((ke - kb + seg - 1) / seg);                             // segments per sample
+    // FP16 pairs: a stage holds TWO K-chunks (the chunk's 16 KB of operands fit
+    // twice in the 32 / 48 KB stage: the second chunk takes the slots of the lo
+    // tiles), so barrier round trips, commits and relays are paid per 32 columns.
+    // Chunks pair up inside a sample and a TMEM segment only.
+    const bool two = MLSK_TC_TWO && sh.bfx == 2;
+    auto step_n = [&](int64_t kc_, int64_t sgc_) { return two && kc_ + 1 < ke && sgc_ + 1 < seg ? 2 : 1; };
 
     const uint32_t full0 = smem_addr(&bars[0]), empty0 = smem_addr(&bars[NST]);
     const uint32_t tfull0 = smem_addr(&bars[2 * NST]), tempty0 = smem_addr(&bars[2 * NST + 2]);
@@ -1157,8 +1166,9 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            int64_t b = kpar ? 0 : grp, kc = kb;
-            for (int64_t it = 0; it < iters; ++it) {
+            int64_t b = kpar ? 0 : grp, kc = kb, sgc = 0;
+            for (int64_t it = 0; it < iters;) {
+                const int n = step_n(kc, sgc);  // K-chunks of this stage
                 // (pair: freed by the leader's multicast commit)
                 if (PAIR) bar_wait_cluster(empty0 + 8 * s, ph ^ 1);
                 else bar_wait(empty0 + 8 * s, ph ^ 1);
@@ -1168,8 +1178,8 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
 #else
                 const bool h16 = sh.bfx == 2;  // FP16 pairs: one tile per operand (half the bytes)
                 const bool h16b = sh.bfx == 3;  // FP16 hi | BF16 values + a BF16 lo tile of half the size
-                bar_expect_tx(full, h16 ? TA_BYTES + BB : h16b ? (TA_BYTES + BB) * 3 / 2 : STB);
-                MLSK_DCHECK(b < (kpar ? 1 : sh.nb) && kc < sh.nkc && (int64_t)tm * TBM < sh.MP &&
+                bar_expect_tx(full, h16 ? n * (TA_BYTES + BB) : h16b ? (TA_BYTES + BB) * 3 / 2 : STB);
+                MLSK_DCHECK(b < (kpar ? 1 : sh.nb) && kc + n <= sh.nkc && (int64_t)tm * TBM < sh.MP &&
                             (int64_t)tn * TBN < sh.PP);
                 const int64_t oa = ((b * sh.nkc + kc) * sh.MP + (int64_t)tm * TBM) * TBK;
                 // (pair: this CTA's half of the B tile, columns tn 256 + rank 128 ..)
@@ -1181,9 +1191,17 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 bulk_load(st + 2 * TA_BYTES, Bhi + ob, BB, full);
                 if (h16b) bulk_load(st + 2 * TA_BYTES + BB, Blo + ob / 2, BB / 2, full);
                 else if (!h16) bulk_load(st + 2 * TA_BYTES + BB, Blo + ob, BB, full);
+                if (n == 2) {  // FP16 pairs: the next chunk in the slots of the lo tiles
+                    bulk_load(st + TA_BYTES, Ahi + oa + sh.MP * TBK, TA_BYTES, full);
+                    bulk_load(st + 2 * TA_BYTES + BB, Bhi + ob + sh.PP * TBK, BB, full);
+                }
 #endif
                 if (++s == NST) { s = 0; ph ^= 1; }
-                if (++kc == ke) { kc = kb; b += sh.Gs; }
+                it += n;
+                kc += n;
+                sgc += n;
+                if (kc == ke) { kc = kb; b += sh.Gs; sgc = 0; }
+                else if (sgc >= seg) sgc = 0;
             }
         }
     } else if (warp == 1) {
@@ -1195,10 +1213,17 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 int s = 0;
                 uint32_t ph = 0;
                 const uint32_t lead_pfull0 = cluster_addr(pfull0, 0);
-                for (int64_t it = 0; it < iters; ++it) {
+                int64_t kc = kb, sgc = 0;
+                for (int64_t it = 0; it < iters;) {
+                    const int n = step_n(kc, sgc);
                     bar_wait(full0 + 8 * s, ph);
                     bar_arrive_remote(lead_pfull0 + 8 * s);
                     if (++s == NST) { s = 0; ph ^= 1; }
+                    it += n;
+                    kc += n;
+                    sgc += n;
+                    if (kc == ke) { kc = kb; sgc = 0; }
+                    else if (sgc >= seg) sgc = 0;
                 }
             }
         } else if (lane == 0) {
@@ -1211,7 +1236,8 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
             uint32_t aph = 0;  // bit a = phase of accumulator a (no indexed local array)
             int sb = kpar ? 0 : grp;  // current sample (merged shared panel: its negated chunks)
             int64_t neg_kc = sh.mk_info ? (sb < sh.nb ? sh.mk_info[sb].neg_kc : 0) : sh.neg_kc;
-            for (int64_t it = 0; it < iters; ++it) {
+            for (int64_t it = 0; it < iters;) {
+                const int n = step_n(kc, sgc);  // K-chunks of this stage (FP16 pairs: up to two)
                 if (sgc == 0) {  // first K-chunk of a segment (kpar: this CTA's range starts at kb > 0)
                     // the epilogue(s) released this accumulator
                     if (PAIR) bar_wait_cluster(tempty0 + 8 * abuf, ((aph >> abuf) & 1u) ^ 1u);
@@ -1225,19 +1251,23 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 const uint32_t dcol = tmem + (uint32_t)abuf * TBN;
                 const uint32_t id = sh.kc0 + kc < neg_kc ? idesc | (1u << 14) : idesc;  // negate B
                 if (sh.bfx == 2) {
-                    // FP16 pairs: hi x hi, hi x lo, lo x hi over the row halves of the one tile
+                    // FP16 pairs: hi x hi, hi x lo, lo x hi over the row halves of the one tile;
+                    // the stage's second chunk (n == 2) sits in the slots of the lo tiles
                     constexpr uint32_t idh0 = f16_idesc(PAIR ? 2 * TBM : TBM, TBN);
-                    const uint32_t idh = sh.kc0 + kc < neg_kc ? idh0 | (1u << 14) : idh0;
-                    const uint32_t sbh = st + 2 * TA_BYTES;
 #ifndef MLSK_TC_ABL_NOMMA
-                    if (PAIR) {
-                        tc_mma_bf16_pair(dcol, sw_desc(st), sw_desc(sbh), idh, sgc > 0 ? 1u : 0u);
-                        tc_mma_bf16_pair(dcol, sw_desc(st), sw_desc(sbh + 32), idh, 1u);
-                        tc_mma_bf16_pair(dcol, sw_desc(st + 32), sw_desc(sbh), idh, 1u);
-                    } else {
-                        tc_mma_bf16(dcol, sw_desc(st), sw_desc(sbh), idh, sgc > 0 ? 1u : 0u);
-                        tc_mma_bf16(dcol, sw_desc(st), sw_desc(sbh + 32), idh, 1u);
-                        tc_mma_bf16(dcol, sw_desc(st + 32), sw_desc(sbh), idh, 1u);
+                    for (int q = 0; q < n; ++q) {
+                        const uint32_t idh = sh.kc0 + kc + q < neg_kc ? idh0 | (1u << 14) : idh0;
+                        const uint32_t sa = st + q * TA_BYTES, sbh = st + 2 * TA_BYTES + q * BB;
+                        const uint32_t acc0 = sgc + q > 0 ? 1u : 0u;
+                        if (PAIR) {
+                            tc_mma_bf16_pair(dcol, sw_desc(sa), sw_desc(sbh), idh, acc0);
+                            tc_mma_bf16_pair(dcol, sw_desc(sa), sw_desc(sbh + 32), idh, 1u);
+                            tc_mma_bf16_pair(dcol, sw_desc(sa + 32), sw_desc(sbh), idh, 1u);
+                        } else {
+                            tc_mma_bf16(dcol, sw_desc(sa), sw_desc(sbh), idh, acc0);
+                            tc_mma_bf16(dcol, sw_desc(sa), sw_desc(sbh + 32), idh, 1u);
+                            tc_mma_bf16(dcol, sw_desc(sa + 32), sw_desc(sbh), idh, 1u);
+                        }
                     }
 #endif
                 } else if (sh.bfx == 3) {
@@ -1299,14 +1329,16 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 if (PAIR) tc_commit_pair(empty0 + 8 * s);
                 else tc_commit(empty0 + 8 * s);
                 if (++s == NST) { s = 0; ph ^= 1; }
-                ++sgc;
-                const bool sample_end = ++kc == ke;
+                it += n;
+                sgc += n;
+                kc += n;
+                const bool sample_end = kc == ke;
                 if (sample_end) {
                     kc = kb;
                     sb += sh.Gs;
                     if (sh.mk_info && sb < sh.nb) neg_kc = sh.mk_info[sb].neg_kc;
                 }
-                if (sample_end || sgc == seg) {
+                if (sample_end || sgc >= seg) {
                     sgc = 0;
                     if (PAIR) tc_commit_pair(tfull0 + 8 * abuf);  // accumulator segment complete
                     else tc_commit(tfull0 + 8 * abuf);
