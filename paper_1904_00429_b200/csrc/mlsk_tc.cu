@@ -1115,7 +1115,13 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
     // twice in the 32 / 48 KB stage: the second chunk takes the slots of the lo
     // tiles), so barrier round trips, commits and relays are paid per 32 columns.
     // Chunks pair up inside a sample and a TMEM segment only.
-    const bool two = MLSK_TC_TWO && sh.bfx == 2;
+    // FP16 hi + BF16 (a chunk is 24 KB of operands per CTA of a pair): stages of two
+    // chunks, 48 KB each, four of them.
+    const bool two3 = MLSK_TC_TWO && PAIR && sh.bfx == 3;
+    const bool two = (MLSK_TC_TWO && sh.bfx == 2) || two3;
+    constexpr int CH3 = (TA_BYTES + BB) * 3 / 2;  // one chunk's operands, FP16 hi + BF16: A1 | A2 | B1 | B2
+    const int stb = two3 ? 2 * CH3 : STB;         // stage stride
+    const int nst = two3 ? 4 : NST;               // stages in the ring
     auto step_n = [&](int64_t kc_, int64_t sgc_) { return two && kc_ + 1 < ke && sgc_ + 1 < seg ? 2 : 1; };
 
     const uint32_t full0 = smem_addr(&bars[0]), empty0 = smem_addr(&bars[NST]);
@@ -1178,25 +1184,35 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
 #else
                 const bool h16 = sh.bfx == 2;  // FP16 pairs: one tile per operand (half the bytes)
                 const bool h16b = sh.bfx == 3;  // FP16 hi | BF16 values + a BF16 lo tile of half the size
-                bar_expect_tx(full, h16 ? n * (TA_BYTES + BB) : h16b ? (TA_BYTES + BB) * 3 / 2 : STB);
+                bar_expect_tx(full, h16 ? n * (TA_BYTES + BB) : h16b ? n * CH3 : STB);
                 MLSK_DCHECK(b < (kpar ? 1 : sh.nb) && kc + n <= sh.nkc && (int64_t)tm * TBM < sh.MP &&
                             (int64_t)tn * TBN < sh.PP);
                 const int64_t oa = ((b * sh.nkc + kc) * sh.MP + (int64_t)tm * TBM) * TBK;
                 // (pair: this CTA's half of the B tile, columns tn 256 + rank 128 ..)
                 const int64_t ob = ((b * sh.nkc + kc) * sh.PP + (int64_t)tn * TBN + (PAIR ? rank * TBM : 0)) * TBK;
-                const uint32_t st = smem_addr(ring + s * STB);
-                bulk_load(st, Ahi + oa, TA_BYTES, full);
-                if (h16b) bulk_load(st + TA_BYTES, Alo + oa / 2, TA_BYTES / 2, full);
-                else if (!h16) bulk_load(st + TA_BYTES, Alo + oa, TA_BYTES, full);
-                bulk_load(st + 2 * TA_BYTES, Bhi + ob, BB, full);
-                if (h16b) bulk_load(st + 2 * TA_BYTES + BB, Blo + ob / 2, BB / 2, full);
-                else if (!h16) bulk_load(st + 2 * TA_BYTES + BB, Blo + ob, BB, full);
-                if (n == 2) {  // FP16 pairs: the next chunk in the slots of the lo tiles
-                    bulk_load(st + TA_BYTES, Ahi + oa + sh.MP * TBK, TA_BYTES, full);
-                    bulk_load(st + 2 * TA_BYTES + BB, Bhi + ob + sh.PP * TBK, BB, full);
+                const uint32_t st = smem_addr(ring + s * stb);
+                if (h16b) {
+                    // FP16 hi + BF16: per chunk a block A1 | A2 | B1 | B2 (A2, B2: the half-size lo tiles)
+                    for (int q = 0; q < n; ++q) {
+                        const uint32_t blk = st + q * CH3;
+                        const int64_t qa = oa + q * sh.MP * TBK, qb = ob + q * sh.PP * TBK;
+                        bulk_load(blk, Ahi + qa, TA_BYTES, full);
+                        bulk_load(blk + TA_BYTES, Alo + qa / 2, TA_BYTES / 2, full);
+                        bulk_load(blk + TA_BYTES * 3 / 2, Bhi + qb, BB, full);
+                        bulk_load(blk + TA_BYTES * 3 / 2 + BB, Blo + qb / 2, BB / 2, full);
+                    }
+                } else {
+                    bulk_load(st, Ahi + oa, TA_BYTES, full);
+                    if (!h16) bulk_load(st + TA_BYTES, Alo + oa, TA_BYTES, full);
+                    bulk_load(st + 2 * TA_BYTES, Bhi + ob, BB, full);
+                    if (!h16) bulk_load(st + 2 * TA_BYTES + BB, Blo + ob, BB, full);
+                    if (n == 2) {  // FP16 pairs: the next chunk in the slots of the lo tiles
+                        bulk_load(st + TA_BYTES, Ahi + oa + sh.MP * TBK, TA_BYTES, full);
+                        bulk_load(st + 2 * TA_BYTES + BB, Bhi + ob + sh.PP * TBK, BB, full);
+                    }
                 }
 #endif
-                if (++s == NST) { s = 0; ph ^= 1; }
+                if (++s == nst) { s = 0; ph ^= 1; }
                 it += n;
                 kc += n;
                 sgc += n;
@@ -1218,7 +1234,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                     const int n = step_n(kc, sgc);
                     bar_wait(full0 + 8 * s, ph);
                     bar_arrive_remote(lead_pfull0 + 8 * s);
-                    if (++s == NST) { s = 0; ph ^= 1; }
+                    if (++s == nst) { s = 0; ph ^= 1; }
                     it += n;
                     kc += n;
                     sgc += n;
@@ -1247,7 +1263,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 bar_wait(full0 + 8 * s, ph);
                 if (PAIR) bar_wait_cluster(pfull0 + 8 * s, ph);  // the peer's half of the stage
                 tc_fence_after();
-                const uint32_t st = smem_addr(ring + s * STB);
+                const uint32_t st = smem_addr(ring + s * stb);
                 const uint32_t dcol = tmem + (uint32_t)abuf * TBN;
                 const uint32_t id = sh.kc0 + kc < neg_kc ? idesc | (1u << 14) : idesc;  // negate B
                 if (sh.bfx == 2) {
@@ -1275,17 +1291,21 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                     // the first tile, the lo parts are the SWIZZLE_32B tile
                     constexpr uint32_t idh0 = f16_idesc(PAIR ? 2 * TBM : TBM, TBN);
                     constexpr uint32_t idb0 = bf16_idesc(PAIR ? 2 * TBM : TBM, TBN);
-                    const uint32_t ng = sh.kc0 + kc < neg_kc ? (1u << 14) : 0u;
-                    const uint32_t sal = st + TA_BYTES, sbh = st + 2 * TA_BYTES, sbl = sbh + BB;
 #ifndef MLSK_TC_ABL_NOMMA
-                    if (PAIR) {
-                        tc_mma_bf16_pair(dcol, sw_desc(st), sw_desc(sbh), idh0 | ng, sgc > 0 ? 1u : 0u);
-                        tc_mma_bf16_pair(dcol, sw_desc(st + 32), sw32_desc(sbl), idb0 | ng, 1u);   // x b_lo
-                        tc_mma_bf16_pair(dcol, sw32_desc(sal), sw_desc(sbh + 32), idb0 | ng, 1u);  // a_lo x
-                    } else {
-                        tc_mma_bf16(dcol, sw_desc(st), sw_desc(sbh), idh0 | ng, sgc > 0 ? 1u : 0u);
-                        tc_mma_bf16(dcol, sw_desc(st + 32), sw32_desc(sbl), idb0 | ng, 1u);
-                        tc_mma_bf16(dcol, sw32_desc(sal), sw_desc(sbh + 32), idb0 | ng, 1u);
+                    for (int q = 0; q < n; ++q) {
+                        const uint32_t ng = sh.kc0 + kc + q < neg_kc ? (1u << 14) : 0u;
+                        const uint32_t blk = st + q * CH3;  // A1 | A2 | B1 | B2
+                        const uint32_t sal = blk + TA_BYTES, sbh = blk + TA_BYTES * 3 / 2, sbl = sbh + BB;
+                        const uint32_t acc0 = sgc + q > 0 ? 1u : 0u;
+                        if (PAIR) {
+                            tc_mma_bf16_pair(dcol, sw_desc(blk), sw_desc(sbh), idh0 | ng, acc0);
+                            tc_mma_bf16_pair(dcol, sw_desc(blk + 32), sw32_desc(sbl), idb0 | ng, 1u);   // x b_lo
+                            tc_mma_bf16_pair(dcol, sw32_desc(sal), sw_desc(sbh + 32), idb0 | ng, 1u);  // a_lo x
+                        } else {
+                            tc_mma_bf16(dcol, sw_desc(blk), sw_desc(sbh), idh0 | ng, acc0);
+                            tc_mma_bf16(dcol, sw_desc(blk + 32), sw32_desc(sbl), idb0 | ng, 1u);
+                            tc_mma_bf16(dcol, sw32_desc(sal), sw_desc(sbh + 32), idb0 | ng, 1u);
+                        }
                     }
 #endif
                 } else if (sh.bfx) {
@@ -1328,7 +1348,7 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 // smem stage free once these MMAs complete (pair: in both CTAs)
                 if (PAIR) tc_commit_pair(empty0 + 8 * s);
                 else tc_commit(empty0 + 8 * s);
-                if (++s == NST) { s = 0; ph ^= 1; }
+                if (++s == nst) { s = 0; ph ^= 1; }
                 it += n;
                 sgc += n;
                 kc += n;
