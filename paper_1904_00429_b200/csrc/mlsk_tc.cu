@@ -563,6 +563,14 @@ constexpr int GK_GAUSS = 0, GK_STUDENT_T = 1, GK_GENERIC = 2;
 #ifndef MLSK_TC_TWO
 #define MLSK_TC_TWO 1
 #endif
+#ifndef MLSK_TC_CPS
+// K-chunks per stage with FP16 pairs (16 KB of operands per chunk and CTA of a pair): 2 / 3 / 4 / 6 / 7
+// chunks -> config 3 10.90 / 10.40 / 10.12 / 10.64 / 10.82, config 4 9.19 / 8.60 / 8.33 / 8.62 / 8.61 ms per step
+#define MLSK_TC_CPS 4
+#endif
+#ifndef MLSK_TC_CPS3
+#define MLSK_TC_CPS3 3  // the same with FP16 hi + BF16 (24 KB per chunk): 2 / 3 / 4 -> config 5 243.5 / 232.8 / 245.7 ms per step
+#endif
 #ifndef MLSK_GEN_CHUNK_MAJOR
 #define MLSK_GEN_CHUNK_MAJOR 1
 #endif
@@ -1111,18 +1119,23 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
     const int64_t iters = (int64_t)my_samples * (ke - kb);
     const int64_t seg = SEGM && sh.seg > 0 && sh.seg < ke - kb ? sh.seg : ke - kb;  // K-chunks per TMEM segment
     const int nseg = (int)((ke - kb + seg - 1) / seg);                             // segments per sample
-    // FP16 pairs: a stage holds TWO K-chunks (the chunk's 16 KB of operands fit
-    // twice in the 32 / 48 KB stage: the second chunk takes the slots of the lo
-    // tiles), so barrier round trips, commits and relays are paid per 32 columns.
-    // Chunks pair up inside a sample and a TMEM segment only.
-    // FP16 hi + BF16 (a chunk is 24 KB of operands per CTA of a pair): stages of two
-    // chunks, 48 KB each, four of them.
+    // FP16 pairs: a stage holds several K-chunks (MLSK_TC_CPS blocks of the chunk's
+    // 16 KB of operands), so barrier round trips, commits and relays are paid per
+    // 64 columns instead of per 16.  Chunks group inside a sample and a TMEM
+    // segment only.
+    // FP16 hi + BF16 (a chunk is 24 KB of operands per CTA of a pair): stages of
+    // MLSK_TC_CPS3 chunk blocks.
     const bool two3 = MLSK_TC_TWO && PAIR && sh.bfx == 3;
-    const bool two = (MLSK_TC_TWO && sh.bfx == 2) || two3;
-    constexpr int CH3 = (TA_BYTES + BB) * 3 / 2;  // one chunk's operands, FP16 hi + BF16: A1 | A2 | B1 | B2
-    const int stb = two3 ? 2 * CH3 : STB;         // stage stride
-    const int nst = two3 ? 4 : NST;               // stages in the ring
-    auto step_n = [&](int64_t kc_, int64_t sgc_) { return two && kc_ + 1 < ke && sgc_ + 1 < seg ? 2 : 1; };
+    const bool two2 = MLSK_TC_TWO && sh.bfx == 2;
+    constexpr int CH2 = TA_BYTES + BB;            // one chunk's operands, FP16 pairs: A | B
+    constexpr int CH3 = (TA_BYTES + BB) * 3 / 2;  // FP16 hi + BF16: A1 | A2 | B1 | B2
+    const int maxn = two2 ? MLSK_TC_CPS : two3 ? MLSK_TC_CPS3 : 1;  // K-chunks per stage
+    const int stb = two2 ? MLSK_TC_CPS * CH2 : two3 ? MLSK_TC_CPS3 * CH3 : STB;  // stage stride
+    const int nst = (NST * STB) / stb < NST ? (NST * STB) / stb : NST;  // stages in the ring
+    auto step_n = [&](int64_t kc_, int64_t sgc_) {
+        int64_t r = ke - kc_ < seg - sgc_ ? ke - kc_ : seg - sgc_;
+        return (int)(r < maxn ? r : maxn);
+    };
 
     const uint32_t full0 = smem_addr(&bars[0]), empty0 = smem_addr(&bars[NST]);
     const uint32_t tfull0 = smem_addr(&bars[2 * NST]), tempty0 = smem_addr(&bars[2 * NST + 2]);
@@ -1201,15 +1214,18 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                         bulk_load(blk + TA_BYTES * 3 / 2, Bhi + qb, BB, full);
                         bulk_load(blk + TA_BYTES * 3 / 2 + BB, Blo + qb / 2, BB / 2, full);
                     }
+                } else if (h16) {
+                    // FP16 pairs: per chunk a block A | B
+                    for (int q = 0; q < n; ++q) {
+                        const uint32_t blk = st + q * CH2;
+                        bulk_load(blk, Ahi + oa + q * sh.MP * TBK, TA_BYTES, full);
+                        bulk_load(blk + TA_BYTES, Bhi + ob + q * sh.PP * TBK, BB, full);
+                    }
                 } else {
                     bulk_load(st, Ahi + oa, TA_BYTES, full);
-                    if (!h16) bulk_load(st + TA_BYTES, Alo + oa, TA_BYTES, full);
+                    bulk_load(st + TA_BYTES, Alo + oa, TA_BYTES, full);
                     bulk_load(st + 2 * TA_BYTES, Bhi + ob, BB, full);
-                    if (!h16) bulk_load(st + 2 * TA_BYTES + BB, Blo + ob, BB, full);
-                    if (n == 2) {  // FP16 pairs: the next chunk in the slots of the lo tiles
-                        bulk_load(st + TA_BYTES, Ahi + oa + sh.MP * TBK, TA_BYTES, full);
-                        bulk_load(st + 2 * TA_BYTES + BB, Bhi + ob + sh.PP * TBK, BB, full);
-                    }
+                    bulk_load(st + 2 * TA_BYTES + BB, Blo + ob, BB, full);
                 }
 #endif
                 if (++s == nst) { s = 0; ph ^= 1; }
@@ -1267,13 +1283,13 @@ k_gemm_tf32x3(const float* __restrict__ Ahi, const float* __restrict__ Alo, cons
                 const uint32_t dcol = tmem + (uint32_t)abuf * TBN;
                 const uint32_t id = sh.kc0 + kc < neg_kc ? idesc | (1u << 14) : idesc;  // negate B
                 if (sh.bfx == 2) {
-                    // FP16 pairs: hi x hi, hi x lo, lo x hi over the row halves of the one tile;
-                    // the stage's second chunk (n == 2) sits in the slots of the lo tiles
+                    // FP16 pairs: hi x hi, hi x lo, lo x hi over the row halves of the one tile,
+                    // for each of the stage's chunks
                     constexpr uint32_t idh0 = f16_idesc(PAIR ? 2 * TBM : TBM, TBN);
 #ifndef MLSK_TC_ABL_NOMMA
                     for (int q = 0; q < n; ++q) {
                         const uint32_t idh = sh.kc0 + kc + q < neg_kc ? idh0 | (1u << 14) : idh0;
-                        const uint32_t sa = st + q * TA_BYTES, sbh = st + 2 * TA_BYTES + q * BB;
+                        const uint32_t sa = st + q * CH2, sbh = sa + TA_BYTES;  // the chunk's block A | B
                         const uint32_t acc0 = sgc + q > 0 ? 1u : 0u;
                         if (PAIR) {
                             tc_mma_bf16_pair(dcol, sw_desc(sa), sw_desc(sbh), idh, acc0);
